@@ -1,0 +1,208 @@
+"""Synthetic pools and replay scenarios for the SURVEY.md 8(d) configs C1-C5.
+
+* :func:`synthetic_cluster` reproduces ``pkg/src/swarmsched/bench.py:91-130``
+  draw for draw (``random.Random(seed)``: capacity ``randint(4, 32)``, flops
+  ``uniform(6e13, 2.4e14)``, round-robin regions, 1 ms intra-region links,
+  10 ms default across), so a pool built here is the reference's pool.
+* Scenario states (C4/C5) are the base pool after churn (a seeded set of plan
+  GPUs leaves, as ``MembershipManager.on_leave`` would, no rebalance) and with
+  a seeded per-pair RTT jitter.  The jitter factor is an exactly representable
+  dyadic rational derived from a splitmix64 hash, so the device generator
+  (``ss_scenario_rtt``) and the host/oracle produce bit-identical RTTs:
+  ``rtt_ab * ((768 + h % 512) / 1024)``, i.e. a uniform factor in [0.75, 1.25).
+"""
+
+from __future__ import annotations
+
+import random
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .topology import ClusterSnapshot, GpuNode, ModelSpec
+
+CAPACITY_RANGE = (4, 32)
+FLOPS_RANGE = (6e13, 2.4e14)
+INTRA_REGION_RTT_S = 0.001
+MASK64 = (1 << 64) - 1
+
+
+def bench_model(layer_count: int = 48, name: Optional[str] = None) -> ModelSpec:
+    """The bench's model shape (bench.py:116-121) at a given depth."""
+    return ModelSpec(name or f"bench-{layer_count}l", layer_count, 1.2e9, 2.8e10)
+
+
+def default_region_count(gpu_count: int) -> int:
+    return max(1, min(4, gpu_count // 8))
+
+
+def synthetic_cluster(gpu_count: int, *, seed: int = 0, region_count: Optional[int] = None,
+                      model: Optional[ModelSpec] = None, homogeneous_flops: Optional[float] = None,
+                      id_prefix: str = "gpu-", links: Optional[Dict] = None) -> Tuple[ClusterSnapshot, ModelSpec]:
+    """Pool drawn exactly like the reference bench (bench.py:114-138).
+
+    ``homogeneous_flops`` overrides every GPU's flops after the draw (the
+    tie-heavy fixture of SURVEY.md 8(d)); the random stream is unchanged.
+    ``links`` replaces the intra-region link table (used for jittered pools).
+    """
+    model = model or bench_model()
+    rc = default_region_count(gpu_count) if region_count is None else region_count
+    rng = random.Random(seed)
+    names = [f"region-{chr(ord('a') + i)}" for i in range(rc)]
+    nodes = []
+    for i in range(gpu_count):
+        cap = rng.randint(*CAPACITY_RANGE)
+        flops = rng.uniform(*FLOPS_RANGE)
+        nodes.append(GpuNode(id=f"{id_prefix}{i:04d}", region=names[i % rc],
+                             vram_bytes=cap * model.bytes_per_layer / 0.8,
+                             flops=homogeneous_flops if homogeneous_flops else flops,
+                             reserve_fraction=0.2))
+    if links is None:
+        links = {}
+        for i, a in enumerate(nodes):
+            for b in nodes[i + 1:]:
+                if a.region == b.region:
+                    links[(a.id, b.id)] = INTRA_REGION_RTT_S
+    return ClusterSnapshot(gpus=tuple(nodes), links=links), model
+
+
+# ---------------------------------------------------------------------------
+# deterministic hashing shared with the device generator
+# ---------------------------------------------------------------------------
+
+def splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & MASK64
+    return x ^ (x >> 31)
+
+
+def pair_hash(seed: int, i: int, j: int) -> int:
+    """Hash of an unordered GPU pair (i < j) under a scenario seed."""
+    return splitmix64((splitmix64(seed & MASK64) ^ ((i << 32) | j)) & MASK64)
+
+
+def jitter_factor(seed: int, i: int, j: int) -> float:
+    if i > j:
+        i, j = j, i
+    return (768 + pair_hash(seed, i, j) % 512) / 1024.0
+
+
+def jitter_factor_matrix(seed: int, n: int) -> np.ndarray:
+    """Vectorised jitter_factor over all pairs (diagonal 1.0) -- numpy uint64 arithmetic."""
+    i, j = np.triu_indices(n, 1)
+    s = np.uint64(splitmix64(seed & MASK64))
+    with np.errstate(over="ignore"):
+        x = s ^ ((i.astype(np.uint64) << np.uint64(32)) | j.astype(np.uint64))
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    f = (768.0 + (x % np.uint64(512)).astype(np.float64)) / 1024.0
+    out = np.ones((n, n))
+    out[i, j] = f
+    out[j, i] = f
+    return out
+
+
+def churn_set(seed: int, plan_gpus: Sequence[int], slices: Dict[int, Tuple[int, int]], layer_count: int,
+              fraction: float = 0.05) -> List[int]:
+    """Seeded leave set: up to ``fraction`` of the plan GPUs, never uncovering a layer.
+
+    Candidates are visited in ascending splitmix64(seed, gpu) order; one is
+    accepted when every layer keeps at least one host afterwards.
+    """
+    want = int(len(plan_gpus) * fraction)
+    cover = np.zeros(layer_count + 2, dtype=np.int64)
+    for g in plan_gpus:
+        a, b = slices[g]
+        cover[a:b + 1] += 1
+    order = sorted(plan_gpus, key=lambda g: (splitmix64((splitmix64(seed) ^ (0xC4 << 40) ^ g) & MASK64), g))
+    out = []
+    for g in order:
+        if len(out) >= want:
+            break
+        a, b = slices[g]
+        if np.all(cover[a:b + 1] >= 2):
+            cover[a:b + 1] -= 1
+            out.append(g)
+    return sorted(out)
+
+
+# ---------------------------------------------------------------------------
+# scenario description (what the replay consumes)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ScenarioSet:
+    """Scenario batch over one base pool (GPU index = position in sorted-id order).
+
+    base_rtt[N, N]   ground-truth rtt_s over all pool GPUs (diag 0)
+    base_tau[N]      flops_per_layer_per_token / flops
+    slice_lo/hi[N]   1-based inclusive layer range per GPU, 0/-1 when not serving
+    seeds[S]         per-scenario jitter / churn seed
+    leave[S, N]      bool, GPU departed in scenario s
+    """
+
+    layer_count: int
+    ids: List[str]
+    base_rtt: np.ndarray
+    base_tau: np.ndarray
+    slice_lo: np.ndarray
+    slice_hi: np.ndarray
+    seeds: np.ndarray
+    leave: np.ndarray
+    jitter: bool = True
+
+    @property
+    def n_scenarios(self) -> int:
+        return int(self.seeds.shape[0])
+
+    @property
+    def n_gpus(self) -> int:
+        return len(self.ids)
+
+    def scenario_rtt(self, s: int) -> np.ndarray:
+        if not self.jitter:
+            return self.base_rtt.copy()
+        return self.base_rtt * jitter_factor_matrix(int(self.seeds[s]), self.n_gpus)
+
+    def columns(self, s: int) -> List[np.ndarray]:
+        alive = ~self.leave[s]
+        return [np.nonzero(alive & (self.slice_lo <= l) & (self.slice_hi >= l))[0]
+                for l in range(1, self.layer_count + 1)]
+
+
+def base_rtt_matrix(cluster: ClusterSnapshot, ids: Sequence[str]) -> np.ndarray:
+    n = len(ids)
+    out = np.empty((n, n))
+    for a in range(n):
+        for b in range(n):
+            out[a, b] = cluster.rtt_s(ids[a], ids[b])
+    return out
+
+
+def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenarios: int, *,
+                    seed0: int = 0, churn: float = 0.05, jitter: bool = True) -> ScenarioSet:
+    """C4-style scenario batch over a placed pool."""
+    ids = sorted(g.id for g in cluster.gpus)
+    pos = {g: i for i, g in enumerate(ids)}
+    n = len(ids)
+    by_id = {g.id: g for g in cluster.gpus}
+    base_tau = np.array([model.flops_per_layer_per_token / by_id[g].flops for g in ids])
+    lo = np.zeros(n, dtype=np.int32)
+    hi = np.full(n, -1, dtype=np.int32)
+    slices = {}
+    for gid, sl in plan.gpu_slices().items():
+        lo[pos[gid]] = sl.start_layer
+        hi[pos[gid]] = sl.end_layer
+        slices[pos[gid]] = (sl.start_layer, sl.end_layer)
+    rtt = base_rtt_matrix(cluster, ids)
+    seeds = np.arange(seed0, seed0 + n_scenarios, dtype=np.int64)
+    leave = np.zeros((n_scenarios, n), dtype=bool)
+    plan_gpus = sorted(slices)
+    if churn > 0:
+        for s in range(n_scenarios):
+            leave[s, churn_set(int(seeds[s]), plan_gpus, slices, model.layer_count, churn)] = True
+    return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter)
