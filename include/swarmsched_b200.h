@@ -1,0 +1,138 @@
+/*
+ * swarmsched_b200.h -- C ABI of the B200 scheduling hot path.
+ *
+ * The reference (arxiv/paper_2509_26182, package `swarmsched`) is pure Python
+ * and has no FFI; these entry points are what its Python entry points bind
+ * through ctypes.  Each export cites the reference
+ * function(s) whose arithmetic it replaces.
+ *
+ * Conventions
+ *   - every function returns an ss_status (int); per-item status arrays carry
+ *     item-level failures so one bad scenario never aborts a batch
+ *     (sim.py:326-329 records rejections rather than aborting);
+ *   - all array pointers are DEVICE pointers unless the name ends in _h;
+ *     structs are passed by host pointer and copied into kernel parameters;
+ *   - every launch is stream-ordered on the `stream` argument (a cudaStream_t,
+ *     NULL = legacy default stream); nothing allocates persistent memory;
+ *   - GPU indices are dense positions in Python sorted() order of gpu ids, so
+ *     index order == tie-break order (router.py:74,110);
+ *   - floating point is IEEE fp64 with no FMA contraction (built -fmad=false),
+ *     so results are bit-identical to CPython/numpy.
+ */
+#ifndef SWARMSCHED_B200_H
+#define SWARMSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python shim maps them onto errors.py (errors.py:11-95). */
+enum ss_status {
+    SS_OK = 0,
+    SS_UNCOVERED_LAYER = 1,      /* aux = lowest uncovered 1-based layer (router.py:106-109) */
+    SS_NO_PATH = 2,              /* router.py:180-181 */
+    SS_OCC_UNDERFLOW = 3,        /* aux = gpu index (perfmap.py:370-374) */
+    SS_NO_FEASIBLE_PIPELINE = 4, /* allocator.py:608-611 */
+    SS_INFEASIBLE_CAPACITY = 5,  /* waterfill.py:64-65 ; aux = capacity total */
+    SS_ROUNDING_OVERFLOW = 6,    /* waterfill.py:86,112,127,167 */
+    SS_DEGENERATE_OBJECTIVE = 7, /* allocator.py:109-110 */
+    SS_BAD_INPUT = 8,
+    SS_CUDA_ERROR = 9,
+    SS_WORKSPACE = 10,           /* caller-provided scratch too small; aux = needed units */
+    SS_ZERO_CAPACITY = 11        /* waterfill.py:155-157 ; aux = member position */
+};
+
+const char* ss_status_str(int status);
+int ss_version(void);
+/* Hard limits of the device kernels (hosts per DAG column, layers, gpus per DAG). */
+int ss_limits(int32_t* max_hosts_h, int32_t* max_layers_h, int32_t* max_gpus_h);
+
+/* ------------------------------------------------------------------------ */
+/* Phase-2 layout: a set of layer DAGs           */
+/* ------------------------------------------------------------------------ */
+typedef struct ss_dag_set {
+    int32_t n_dags;
+    int32_t max_hosts;          /* max col_len over the set (<= 256) */
+    int32_t max_layers;         /* max layers of one DAG (<= 1024) */
+    int32_t max_gpus;           /* max DAG-local gpu count (replay; <= 4096) */
+    const int32_t* layer_ptr;   /* [n_dags+1]  DAG d owns flat layers [layer_ptr[d], layer_ptr[d+1]) */
+    const int32_t* col_off;     /* [total_layers] first node slot of the layer's host column */
+    const int32_t* col_len;     /* [total_layers] hosts in the column, sorted-id order */
+    const int32_t* node_gpu;    /* [node slots] DAG-local gpu index of each host */
+    const double*  node_tau;    /* [node slots] tau(gpu, layer) (select) or NULL (replay) */
+    const int64_t* edge_off;    /* [total_layers] offset (doubles, even) of block l -> l+1 */
+    const double*  edge_val;    /* row-major R_l x R_{l+1}: row = source host, col = destination */
+} ss_dag_set;
+
+/* Dense RTT matrices, one per item (router.py:118-143 rtt_matrix and
+ * topology.py:133-142 rtt_s share one rule): out[a][b] = direct (a,b) entry if
+ * given, else the (b,a) entry, else `default_value`; diagonal 0; self-links
+ * ignored.  Link keys must be unique per item (they come from a dict). */
+int ss_rtt_fill(int32_t n_items, const int64_t* mat_off, const int32_t* mat_dim, double* out,
+                double default_value, int32_t n_links, const int32_t* link_item,
+                const int32_t* link_a, const int32_t* link_b, const double* link_v, void* stream);
+
+/* build_dag (router.py:87-115) on device: host columns from a dense
+ * per-DAG tau table (layer-major [L_d x G_d], NaN = no live entry) and an
+ * optional exclude mask.  Writes col_len / node_gpu / node_tau into the slots
+ * given by col_off (capacity G_d per layer is always enough); status[d] =
+ * SS_UNCOVERED_LAYER with aux[d] = lowest empty layer. */
+int ss_dag_columns(int32_t n_dags, const int32_t* layer_ptr, const int32_t* gpu_ptr,
+                   const int64_t* tau_off, const double* tau_table, const uint8_t* exclude,
+                   const int32_t* col_off, int32_t* col_len, int32_t* node_gpu, double* node_tau,
+                   int32_t* status, int32_t* aux, void* stream);
+
+/* Scenario columns (C4/C5 replay states): host set of layer l in scenario s =
+ * gpus g (pool order) with !leave[s][g] and slice_lo[g] <= l <= slice_hi[g];
+ * the base pool is shared, scenario s owns flat layers [s*L, (s+1)*L). */
+int ss_scenario_columns(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
+                        const int32_t* slice_hi, const uint8_t* leave, const int32_t* col_off,
+                        int32_t* col_len, int32_t* node_gpu, int32_t* status, int32_t* aux, void* stream);
+
+/* Edge blocks E_l = RTT[col_l, col_{l+1}] (router.py:169 gather).  RTT source:
+ * per-DAG dense matrices at rtt + rtt_off[d] (dim = gpu count of the DAG), or,
+ * when jitter_seed != NULL, one shared pool matrix `rtt` (dim n_pool_gpus)
+ * scaled per scenario by the splitmix64 pair factor of scenarios.py. */
+int ss_dag_edges(const ss_dag_set* dags, const int64_t* rtt_off, const int32_t* rtt_dim, const double* rtt,
+                 const int64_t* jitter_seed, int32_t n_pool_gpus, double* edge_val, void* stream);
+
+/* Batched no-feedback chain DP (router.py:157-197 _relax, used by
+ * select_chain 200-205): one CTA per DAG.  pick_out[flat layer] = position of
+ * the chosen host in the column; cost_out[d] = chain cost; status_out[d]. */
+int ss_select(const ss_dag_set* dags, int32_t* pick_out, double* cost_out, int32_t* status_out, void* stream);
+
+/* Replay with on-device load update (router.py:247-260 route/release +
+ * perfmap.py:353-382 on_chain_event + sim.py:182-183 latency law).
+ * tau(g) = base_tau[g] * occpow[occ[g]].  Op script per scenario: before
+ * request i, release chain i-W when W > 0 and i >= W; W == 0 releases right
+ * after select; W < 0 never releases.  State (occ, ring, next_req) persists
+ * across calls so long replays can be chunked. */
+typedef struct ss_replay_state {
+    const int32_t* gpu_ptr;     /* [n_dags+1] offsets of per-scenario gpu arrays */
+    const double*  base_tau;    /* [sum G] flops_per_layer_per_token / flops */
+    int32_t*       occ;         /* [sum G] occupancy, in/out */
+    int32_t*       ring;        /* [n_dags * max(W,1) * (max_layers+1)] live chains' distinct gpus */
+    int64_t*       next_req;    /* [n_dags] requests routed so far, in/out */
+    int32_t*       status;      /* [n_dags] sticky per-scenario status */
+    int32_t*       aux;         /* [n_dags] */
+} ss_replay_state;
+
+typedef struct ss_replay_out {
+    double*   cost;             /* [n_dags * n_req] or NULL */
+    uint64_t* chain_hash;       /* [n_dags * n_req] or NULL: sum_l splitmix64(l<<32 | gpu_l) */
+    int16_t*  gpus;             /* [n_dags * n_req * max_layers] or NULL: chosen gpu per layer */
+} ss_replay_out;
+
+int ss_replay(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
+              int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
+
+/* Kernel tuning knobs (0 = default); returns previous values via *_h. */
+int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWARMSCHED_B200_H */

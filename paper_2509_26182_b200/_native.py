@@ -1,0 +1,114 @@
+"""ctypes binding of ``libswarmsched_b200.so`` (declared in include/swarmsched_b200.h).
+
+This is the only place Python touches the C ABI.  There is no fallback: if the
+library is missing or no CUDA device is present, every compute entry point
+raises :class:`NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import DeviceError, SS_OK
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libswarmsched_b200.so")
+
+i32p = C.POINTER(C.c_int32)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is not built / no B200 is visible.  No CPU fallback exists."""
+
+
+class DagSet(C.Structure):
+    _fields_ = [
+        ("n_dags", C.c_int32), ("max_hosts", C.c_int32), ("max_layers", C.c_int32), ("max_gpus", C.c_int32),
+        ("layer_ptr", C.c_void_p), ("col_off", C.c_void_p), ("col_len", C.c_void_p), ("node_gpu", C.c_void_p),
+        ("node_tau", C.c_void_p), ("edge_off", C.c_void_p), ("edge_val", C.c_void_p),
+    ]
+
+
+class ReplayState(C.Structure):
+    _fields_ = [
+        ("gpu_ptr", C.c_void_p), ("base_tau", C.c_void_p), ("occ", C.c_void_p), ("ring", C.c_void_p),
+        ("next_req", C.c_void_p), ("status", C.c_void_p), ("aux", C.c_void_p),
+    ]
+
+
+class ReplayOut(C.Structure):
+    _fields_ = [("cost", C.c_void_p), ("chain_hash", C.c_void_p), ("gpus", C.c_void_p)]
+
+
+_SIGS = {
+    "ss_status_str": (C.c_char_p, [C.c_int]),
+    "ss_version": (C.c_int, []),
+    "ss_limits": (C.c_int, [i32p, i32p, i32p]),
+    "ss_rtt_fill": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_dag_columns": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
+    "ss_scenario_columns": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_dag_edges": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                               C.c_void_p, C.c_void_p]),
+    "ss_select": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_replay": (C.c_int, [C.POINTER(DagSet), C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
+                            C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
+    "ss_set_tiling": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p]),
+}
+
+# Phase-1 exports are appended by phase1 bindings (see _SIGS_P1 below).
+_SIGS_P1 = {}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def exported_symbols():
+    return sorted(set(_SIGS) | set(_SIGS_P1))
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen the library and attach signatures (works without a GPU)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(f"{path} is missing; run __graft_entry__.build() (nvcc, sm_100a)")
+        lib = C.CDLL(path)
+        for name, (res, args) in {**_SIGS, **_SIGS_P1}.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    """The loaded library, after checking that a CUDA device is usable."""
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the scheduler kernels need a B200 (sm_100a)")
+    return load_library()
+
+
+def check(status: int, what: str) -> None:
+    if status != SS_OK:
+        msg = load_library().ss_status_str(status).decode()
+        raise DeviceError(f"{what}: {msg} (status {status})")
+
+
+def ptr(t) -> C.c_void_p:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def stream_handle(stream=None) -> C.c_void_p:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)

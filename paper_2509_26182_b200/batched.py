@@ -1,0 +1,166 @@
+"""Batched device APIs (additive; no reference equivalent).
+
+:class:`ScenarioReplayer` is the Phase-2 throughput path: many independent
+cluster states (C4/C5) or one long stream (C2), each replaying
+``route`` / ``release(i - W)`` op scripts with occupancy feedback entirely on
+the device.  It is defined to be element-wise equal to looping the
+reference's ``ChainRouter.route`` / ``release`` (router.py:247-260) on a
+``PerfMap`` whose latency law is ``base_s(g) * (1 + occ) ** e``
+(sim.py:182-183; bench.py:150-151) -- tests/test_gpu_parity.py checks that
+against the oracle and the reference's golden replays.
+
+Device layout per scenario s (capacity layout, no host sync needed):
+  * layer columns at node slots ``s * cap_nodes + prefix(cap)[l]`` where cap_l
+    = hosts of layer l in the base plan (churn only removes hosts);
+  * edge block l -> l+1 at ``s * edge_stride + prefix(cap_l * cap_{l+1})``,
+    actual R_l(s) x R_{l+1}(s) doubles row-major;
+  * per-gpu arrays (base tau, occupancy) at ``s * N``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .errors import raise_for_status
+from .scenarios import ScenarioSet
+
+
+def occ_power_table(size: int, exponent: float = 1.0) -> np.ndarray:
+    """occpow[o] = (1 + o) ** e with Python semantics (sim.py:183); exact for e = 1."""
+    return np.array([float((1 + o) ** exponent) for o in range(size)], dtype=np.float64)
+
+
+@dataclass
+class ReplayResult:
+    cost: Optional[object]        # torch float64 [S, n_req] (device)
+    chain_hash: Optional[object]  # torch uint64 as int64 [S, n_req]
+    gpus: Optional[object]        # torch int16 [S, n_req, L]
+    status: object                # torch int32 [S]
+
+
+class ScenarioReplayer:
+    def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
+                 max_requests: Optional[int] = None, stream=None):
+        import torch
+        self.torch = torch
+        self.scen = scen
+        self.window = int(window)
+        self.stream = stream
+        dev = torch.device("cuda")
+        self.dev = dev
+        S, G, L = scen.n_scenarios, scen.n_gpus, scen.layer_count
+        self.S, self.G, self.L = S, G, L
+        lo, hi = scen.slice_lo.astype(np.int64), scen.slice_hi.astype(np.int64)
+        layers = np.arange(1, L + 1)
+        cap = ((lo[None, :] <= layers[:, None]) & (hi[None, :] >= layers[:, None])).sum(axis=1)
+        if (cap == 0).any():
+            raise ValueError("base plan leaves a layer uncovered")
+        self.cap = cap
+        cap_nodes = int(cap.sum())
+        node_pre = np.concatenate([[0], np.cumsum(cap)[:-1]])
+        blk = cap[:-1] * cap[1:]
+        blk = blk + (blk & 1)
+        edge_pre = np.concatenate([[0], np.cumsum(blk)]) if L > 1 else np.zeros(1, dtype=np.int64)
+        edge_stride = int(edge_pre[-1]) if L > 1 else 2
+        self.edge_stride = edge_stride
+        s_idx = np.arange(S, dtype=np.int64)
+        col_off = (s_idx[:, None] * cap_nodes + node_pre[None, :]).reshape(-1)
+        edge_off = (s_idx[:, None] * edge_stride + edge_pre[None, :L]).reshape(-1)
+        layer_ptr = np.arange(S + 1, dtype=np.int64) * L
+        gpu_ptr = np.arange(S + 1, dtype=np.int64) * G
+
+        def up(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+
+        t32, t64, f64 = torch.int32, torch.int64, torch.float64
+        self.layer_ptr = up(layer_ptr, t32)
+        self.col_off = up(col_off, t32)
+        self.edge_off = up(edge_off, t64)
+        self.gpu_ptr = up(gpu_ptr, t32)
+        self.col_len = torch.empty(S * L, dtype=t32, device=dev)
+        self.node_gpu = torch.empty(S * cap_nodes, dtype=t32, device=dev)
+        self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
+        self.base_tau = up(np.tile(scen.base_tau, S), f64)
+        self.slice_lo = up(lo, t32)
+        self.slice_hi = up(hi, t32)
+        self.leave = up(scen.leave.astype(np.uint8), torch.uint8)
+        self.seeds = up(scen.seeds.astype(np.int64), t64)
+        self.base_rtt = up(scen.base_rtt.reshape(-1), f64)
+        self.occ = torch.zeros(S * G, dtype=t32, device=dev)
+        self.ring = torch.zeros(S * max(self.window, 1) * (L + 1), dtype=t32, device=dev)
+        self.next_req = torch.zeros(S, dtype=t64, device=dev)
+        self.status = torch.zeros(S, dtype=t32, device=dev)
+        self.aux = torch.zeros(S, dtype=t32, device=dev)
+        if self.window > 0:
+            size = self.window + 2
+        else:
+            size = (max_requests or 1 << 16) + 2
+        self.occpow_len = size
+        self.occpow = up(occ_power_table(size, exponent), f64)
+        self.max_hosts = int(cap.max())
+        self.built = False
+
+    # ------------------------------------------------------------------
+    def dag_set(self) -> N.DagSet:
+        return N.DagSet(self.S, self.max_hosts, self.L, self.G, N.ptr(self.layer_ptr), N.ptr(self.col_off),
+                        N.ptr(self.col_len), N.ptr(self.node_gpu), None, N.ptr(self.edge_off),
+                        N.ptr(self.edge_val))
+
+    def build(self) -> None:
+        """Scenario columns + jittered edge blocks, fully on device (ss_scenario_columns, ss_dag_edges)."""
+        lib = N.lib()
+        st = N.stream_handle(self.stream)
+        N.check(lib.ss_scenario_columns(self.S, self.L, self.G, N.ptr(self.slice_lo), N.ptr(self.slice_hi),
+                                        N.ptr(self.leave), N.ptr(self.col_off), N.ptr(self.col_len),
+                                        N.ptr(self.node_gpu), N.ptr(self.status), N.ptr(self.aux), st),
+                "ss_scenario_columns")
+        if self.scen.jitter:
+            N.check(lib.ss_dag_edges(self.dag_set(), None, None, N.ptr(self.base_rtt), N.ptr(self.seeds), self.G,
+                                     N.ptr(self.edge_val), st), "ss_dag_edges")
+        else:
+            torch = self.torch
+            if not hasattr(self, "_rtt_off"):
+                self._rtt_off = torch.zeros(self.S, dtype=torch.int64, device=self.dev)
+                self._rtt_dim = torch.full((self.S,), self.G, dtype=torch.int32, device=self.dev)
+            N.check(lib.ss_dag_edges(self.dag_set(), N.ptr(self._rtt_off), N.ptr(self._rtt_dim), N.ptr(self.base_rtt),
+                                     None, 0, N.ptr(self.edge_val), st), "ss_dag_edges")
+        self.built = True
+
+    def reset(self) -> None:
+        self.occ.zero_()
+        self.ring.zero_()
+        self.next_req.zero_()
+
+    def run(self, n_req: int, *, cost: bool = True, hashes: bool = True, gpus: bool = False,
+            out: Optional[ReplayResult] = None) -> ReplayResult:
+        torch = self.torch
+        if not self.built:
+            self.build()
+        S, L = self.S, self.L
+        if out is None:
+            out = ReplayResult(
+                torch.empty((S, n_req), dtype=torch.float64, device=self.dev) if cost else None,
+                torch.empty((S, n_req), dtype=torch.int64, device=self.dev) if hashes else None,
+                torch.empty((S, n_req, L), dtype=torch.int16, device=self.dev) if gpus else None,
+                self.status)
+        st = N.ReplayState(N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self.occ), N.ptr(self.ring),
+                           N.ptr(self.next_req), N.ptr(self.status), N.ptr(self.aux))
+        ro = N.ReplayOut(N.ptr(out.cost), N.ptr(out.chain_hash), N.ptr(out.gpus))
+        N.check(N.lib().ss_replay(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window, n_req, ro,
+                                  N.stream_handle(self.stream)), "ss_replay")
+        return out
+
+    def raise_first_failure(self) -> None:
+        st = self.status.cpu().numpy()
+        bad = np.nonzero(st)[0]
+        if bad.size:
+            raise_for_status(int(st[bad[0]]), int(self.aux.cpu()[bad[0]]))
+
+    # algorithmic bytes: B2 = 8*sum R_l R_{l+1} + 8*sum R_l + 4*L per selection
+    def bytes_per_selection(self) -> np.ndarray:
+        cl = self.col_len.view(self.S, self.L).cpu().numpy().astype(np.int64)
+        return 8 * (cl[:, :-1] * cl[:, 1:]).sum(axis=1) + 8 * cl.sum(axis=1) + 4 * self.L

@@ -1,0 +1,64 @@
+"""CPU-only checks of the C-ABI boundary and the host-side generators."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import hx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    text = open(os.path.join(ROOT, "include", "swarmsched_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ss_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_builds_and_exports_every_header_symbol():
+    from paper_2509_26182_b200 import _build, _native
+    _build.build()
+    lib = _native.load_library()
+    declared = _header_symbols()
+    assert declared, "header parse failed"
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) <= set(_native.exported_symbols()) | {"ss_status_str"}
+    assert lib.ss_version() >= 100
+    assert lib.ss_status_str(1) == b"uncovered layer"
+    h, l, g = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert lib.ss_limits(ctypes.byref(h), ctypes.byref(l), ctypes.byref(g)) == 0
+    assert h.value == 256
+
+
+def test_compute_entry_points_refuse_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    from paper_2509_26182_b200 import _native
+    with pytest.raises(_native.NativeUnavailable):
+        _native.lib()
+
+
+def test_synthetic_cluster_matches_reference_pools(phase1_cases):
+    from paper_2509_26182_b200 import scenarios as scen
+    for rec in phase1_cases["allocate"]:
+        m = re.match(r"bench_n(\d+)_s(\d+)_L(\d+)", rec["name"])
+        if not m:
+            continue
+        n, seed, L = map(int, m.groups())
+        cl, _ = scen.synthetic_cluster(n, seed=seed, model=scen.bench_model(L))
+        got = [[g.id, g.region, g.vram_bytes.hex(), g.flops.hex(), g.reserve_fraction.hex()] for g in cl.gpus]
+        assert got == rec["gpus"], rec["name"]
+        assert [[a, b, v.hex()] for (a, b), v in sorted(cl.links.items())] == rec["links"]
+
+
+def test_jitter_vectorised_equals_scalar():
+    from paper_2509_26182_b200 import scenarios as scen
+    m = scen.jitter_factor_matrix(12345, 40)
+    for i in range(40):
+        for j in range(40):
+            if i != j:
+                assert m[i, j] == scen.jitter_factor(12345, i, j)
