@@ -129,6 +129,97 @@ typedef struct ss_replay_out {
 int ss_replay(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
               int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Phase-1                                      */
+/* ------------------------------------------------------------------------ */
+/* A pool = one region of one allocate() call: GPUs sorted by (-capacity, id)
+ * (allocator.py:570).  caps are unclamped layer capacities (topology.py:148). */
+typedef struct ss_pool_set {
+    int32_t n_pools;
+    const int32_t* pool_ptr;    /* [n_pools+1] offsets into caps / flops */
+    const int32_t* caps;        /* non-increasing within a pool */
+    const double*  flops;       /* same order */
+    const int32_t* layers;      /* [n_pools] model layer count L */
+    const int32_t* kmax;        /* [n_pools] k_max (allocator.py:97-101) */
+    const int64_t* memb_off;    /* [n_pools] offset of the pool's (k, member) output block: kmax*n ints */
+    const int64_t* gsz_off;     /* [n_pools] offset of the pool's (k, group) size block: kmax*kmax ints */
+} ss_pool_set;
+
+/* solve_stage_counts (allocator.py:473-504) for every k <= kmax[p], in
+ * three stream-ordered launches the packer issues back to back:
+ *   _validate: non-increasing caps (ValueError, 488-489), device limits;
+ *              zeroes stages; pool_status[p] = SS_OK / SS_BAD_INPUT.
+ *   _exact:    pools with <= 16 usable GPUs (listed in exact_list): level sweep
+ *              + dominance pruning + parent replay (138-264), one thread per
+ *              pool over a global workspace (ss_stage_counts_workspace bytes
+ *              each); SS_WORKSPACE with aux = entries needed when too small.
+ *   _cover:    every (pool, k) candidate of the > 16 pools: constructive cover
+ *              (267-470), one thread per candidate, then the "first stalled k
+ *              drops every larger k" rule per pool (456-458).
+ * Output: stages[koff[p] + k-1] = s*(k) or 0 when k is absent;
+ * members[memb_off[p] + (k-1)*n + ...] = the k groups concatenated (indices
+ * into the pool's sorted caps), gsize[gsz_off[p] + (k-1)*kmax + g] = sizes. */
+int64_t ss_stage_counts_workspace(int32_t frontier_cap, int32_t children_cap, int32_t max_levels);
+int ss_stage_counts_validate(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* pool_status,
+                             int32_t* pool_aux, void* stream);
+int ss_stage_counts_exact(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
+                          int32_t* gsize, int32_t* pool_status, int32_t* pool_aux, const int32_t* exact_list,
+                          int32_t n_exact, void* workspace, int64_t ws_bytes_per, int32_t frontier_cap,
+                          int32_t children_cap, int32_t* sweep_stats /* [n_exact*4] or NULL */, void* stream);
+int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
+                          int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k,
+                          int32_t n_cand, int32_t* stall, void* stream);
+
+/* estimate_objective_params (allocator.py:516-538): per item, flops and a
+ * dense rtt_s matrix in CLUSTER order; CPython 3.12 sum() semantics
+ * (Neumaier) reproduced bit-exactly.  out_t[i] = t_comp, out_r[i] = rtt. */
+int ss_objective(int32_t n_items, const int32_t* item_ptr, const double* flops, const int64_t* rtt_off,
+                 const double* rtt, double fpl, const int32_t* layers, double tokens, double* out_t,
+                 double* out_r, void* stream);
+
+/* score (allocator.py:104-111) of every (pool, k) candidate, z[koff[p]+k-1] =
+ * kpow[k] / (t + (s/k) * r) with kpow[k] = k**alpha from the host; with
+ * fill_all != 0 every present k's groups are also water-filled
+ * (rebalance_pipeline, waterfill.py:142-183) into counts[memb_off[p] +
+ * (k-1)*n + pos].  kstatus = score status, fstatus = fill status per k. */
+int ss_phase1_score(const ss_pool_set* pools, const int64_t* koff, const int32_t* stages, const int32_t* members,
+                    const int32_t* gsize, const double* t_comp, const double* rtt, const double* kpow,
+                    int32_t kpow_len, int32_t fill_all, double* z, int32_t* counts, int32_t* kstatus,
+                    int32_t* fstatus, const int32_t* cand_pool, const int32_t* cand_k, int32_t n_cand, void* stream);
+
+/* best_k[p] = argmax over present k by (z, k) (allocator.py:583); then the
+ * best k's groups are water-filled (597-606) unless fill_all already did.
+ * pool_status takes the first failing score / fill status. */
+int ss_phase1_best(const ss_pool_set* pools, const int64_t* koff, const int32_t* stages, const int32_t* members,
+                   const int32_t* gsize, const double* z, const int32_t* kstatus, const int32_t* fstatus,
+                   int32_t fill_all, int32_t* best_k, int32_t* counts, int32_t* pool_status, void* stream);
+
+/* Objective fold + global argmax over variants (allocator.py:588):
+ * variant v owns pools [var_ptr[v], var_ptr[v+1]) in sorted region order;
+ * total[v] = left fold of z at each usable pool's best k; feasible[v] = 1 if
+ * any pipeline, 0 if none (NoFeasiblePipeline), -status on a pool error;
+ * best_variant[0] = argmax total over feasible variants (ties -> lowest v),
+ * -1 if none. */
+int ss_variant_reduce(int32_t n_var, const int32_t* var_ptr, const int64_t* koff, const int32_t* best_k,
+                      const double* z, const int32_t* pool_status, double* total, int32_t* feasible,
+                      int32_t* best_variant, double* best_total, void* stream);
+
+/* Water-fill primitives, batched over independent groups (waterfill.py):
+ * mode 0 = solve_lambda (targets + level, tflag = 1 where the target is the
+ * int cap), 1 = solve_lambda + hamilton_round(total = L), 2 = rebalance
+ * (zero promotion).  Per group status; aux = capacity total for INFEASIBLE. */
+int ss_waterfill(int32_t n_groups, const int32_t* grp_ptr, const double* flops, const int32_t* caps,
+                 const int32_t* layers, int32_t mode, double* targets, int32_t* tflag, double* level,
+                 int32_t* counts, int32_t* status, int32_t* aux, void* stream);
+
+/* hamilton_round on given targets (waterfill.py:91-128); total < 0 -> round(sum(targets)). */
+int ss_hamilton(int32_t n_groups, const int32_t* grp_ptr, const double* targets, const int32_t* tflag,
+                const int32_t* caps, const int32_t* total, int32_t* counts, int32_t* status, void* stream);
+
+/* score() batched (allocator.py:104-111). */
+int ss_score(int32_t n, const int32_t* k, const int32_t* s_star, const double* kpow, const double* t_comp,
+             const double* rtt, double* z, int32_t* status, void* stream);
+
 /* Kernel tuning knobs (0 = default); returns previous values via *_h. */
 int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
 

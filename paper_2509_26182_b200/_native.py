@@ -61,8 +61,29 @@ _SIGS = {
     "ss_set_tiling": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p]),
 }
 
-# Phase-1 exports are appended by phase1 bindings (see _SIGS_P1 below).
-_SIGS_P1 = {}
+class PoolSet(C.Structure):
+    _fields_ = [
+        ("n_pools", C.c_int32), ("pool_ptr", C.c_void_p), ("caps", C.c_void_p), ("flops", C.c_void_p),
+        ("layers", C.c_void_p), ("kmax", C.c_void_p), ("memb_off", C.c_void_p), ("gsz_off", C.c_void_p),
+    ]
+
+
+_V = C.c_void_p
+_SIGS_P1 = {
+    "ss_stage_counts_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "ss_stage_counts_validate": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V]),
+    "ss_stage_counts_exact": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, C.c_int64,
+                                        C.c_int32, C.c_int32, _V, _V]),
+    "ss_stage_counts_cover": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, _V]),
+    "ss_objective": (C.c_int, [C.c_int32, _V, _V, _V, _V, C.c_double, _V, C.c_double, _V, _V, _V]),
+    "ss_phase1_score": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, C.c_int32, _V, _V,
+                                  _V, _V, _V, _V, C.c_int32, _V]),
+    "ss_phase1_best": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
+    "ss_variant_reduce": (C.c_int, [C.c_int32, _V, _V, _V, _V, _V, _V, _V, _V, _V, _V]),
+    "ss_waterfill": (C.c_int, [C.c_int32, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V, _V]),
+    "ss_hamilton": (C.c_int, [C.c_int32, _V, _V, _V, _V, _V, _V, _V, _V]),
+    "ss_score": (C.c_int, [C.c_int32, _V, _V, _V, _V, _V, _V, _V, _V]),
+}
 
 _lib = None
 _lock = threading.Lock()

@@ -1,0 +1,260 @@
+"""Device pool batches for Phase-1 (packing + launch sequencing; no arithmetic).
+
+A *pool* is one region of one ``allocate`` call: its GPUs sorted by
+``(-capacity, id)`` (allocator.py:570), their unclamped capacities and flops,
+the model depth and ``k_max``.  :class:`PoolBatch` uploads many pools at once
+and drives the C-ABI launches
+
+    ss_stage_counts_validate -> ss_stage_counts_exact -> ss_stage_counts_cover
+    -> ss_phase1_score -> ss_phase1_best [-> ss_variant_reduce]
+
+stream-ordered with a single host sync when results are fetched.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import SS_OK, SS_WORKSPACE, raise_for_status
+
+EXACT_LIMIT = 16
+
+
+@dataclass
+class PoolSpec:
+    caps: Sequence[int]          # sorted non-increasing
+    flops: Sequence[float]       # same order
+    layers: int
+    kmax: int
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class PoolBatch:
+    def __init__(self, pools: List[PoolSpec], *, stream=None):
+        torch = _torch()
+        self.pools = pools
+        self.stream = stream
+        dev = torch.device("cuda")
+        self.dev = dev
+        P = len(pools)
+        n = np.array([len(p.caps) for p in pools], dtype=np.int64)
+        km = np.array([max(int(p.kmax), 0) for p in pools], dtype=np.int64)
+        self.n, self.km = n, km
+        pool_ptr = np.concatenate([[0], np.cumsum(n)])
+        koff = np.concatenate([[0], np.cumsum(km)])
+        memb = np.concatenate([[0], np.cumsum(km * n)])
+        gsz = np.concatenate([[0], np.cumsum(km * km)])
+        self.koff_h, self.memb_h, self.gsz_h, self.pool_ptr_h = koff, memb, gsz, pool_ptr
+        caps = np.concatenate([np.asarray(p.caps, dtype=np.int64) for p in pools]) if P else np.zeros(0)
+        flops = np.concatenate([np.asarray(p.flops, dtype=np.float64) for p in pools]) if P else np.zeros(0)
+        usable = np.array([int(np.sum(np.asarray(p.caps) > 0)) for p in pools], dtype=np.int64)
+        self.usable = usable
+        exact = np.nonzero((usable <= EXACT_LIMIT) & (usable > 0) & (km > 0))[0]
+        cover_p = np.nonzero(usable > EXACT_LIMIT)[0]
+        cand_pool = np.repeat(cover_p, km[cover_p]) if cover_p.size else np.zeros(0, dtype=np.int64)
+        cand_k = np.concatenate([np.arange(1, km[p] + 1) for p in cover_p]) if cover_p.size else np.zeros(0)
+        all_pool = np.repeat(np.arange(P), km)
+        all_k = np.concatenate([np.arange(1, k + 1) for k in km]) if km.sum() else np.zeros(0)
+        self.exact = exact
+        self.n_cover = int(cand_pool.size)
+        self.n_cand = int(all_pool.size)
+        ints = np.concatenate([pool_ptr, caps, [p.layers for p in pools], km, exact, cand_pool, cand_k, all_pool,
+                               all_k]).astype(np.int32)
+        self._ints = torch.from_numpy(ints).to(dev)
+        o = 0
+
+        def take(cnt):
+            nonlocal o
+            t = self._ints[o:o + cnt]
+            o += cnt
+            return t
+
+        self.pool_ptr = take(P + 1)
+        self.caps = take(caps.size)
+        self.layers = take(P)
+        self.kmax = take(P)
+        self.exact_list = take(exact.size)
+        self.cand_pool = take(cand_pool.size)
+        self.cand_k = take(cand_k.size)
+        self.all_pool = take(all_pool.size)
+        self.all_k = take(all_k.size)
+        i64 = torch.from_numpy(np.concatenate([koff[:-1], memb[:-1], gsz[:-1]]).astype(np.int64)).to(dev)
+        self.koff, self.memb_off, self.gsz_off = i64[:P], i64[P:2 * P], i64[2 * P:]
+        self.flops = torch.from_numpy(flops).to(dev)
+        K, M, G = int(koff[-1]), int(memb[-1]), int(gsz[-1])
+        self.stages = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
+        self.stall = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
+        self.kstatus = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
+        self.fstatus = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
+        self.z = torch.zeros(max(K, 1), dtype=torch.float64, device=dev)
+        self.members = torch.zeros(max(M, 1), dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(max(M, 1), dtype=torch.int32, device=dev)
+        self.gsize = torch.zeros(max(G, 1), dtype=torch.int32, device=dev)
+        self.status = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
+        self.aux = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
+        self.best_k = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
+        self.sweep_stats = torch.zeros(max(exact.size, 1) * 4, dtype=torch.int32, device=dev)
+        self.fcap, self.ccap = 4096, 65536
+
+    def pool_set(self) -> N.PoolSet:
+        return N.PoolSet(len(self.pools), N.ptr(self.pool_ptr), N.ptr(self.caps), N.ptr(self.flops),
+                         N.ptr(self.layers), N.ptr(self.kmax), N.ptr(self.memb_off), N.ptr(self.gsz_off))
+
+    # -- stage counts ------------------------------------------------------
+    def stage_counts(self) -> None:
+        lib = N.lib()
+        st = N.stream_handle(self.stream)
+        ps = self.pool_set()
+        N.check(lib.ss_stage_counts_validate(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.status),
+                                             N.ptr(self.aux), st), "ss_stage_counts_validate")
+        if self.exact.size:
+            self._run_exact(lib, ps, st)
+        N.check(lib.ss_stage_counts_cover(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members),
+                                          N.ptr(self.gsize), N.ptr(self.status), N.ptr(self.cand_pool),
+                                          N.ptr(self.cand_k), self.n_cover, N.ptr(self.stall), st),
+                "ss_stage_counts_cover")
+
+    def _run_exact(self, lib, ps, st) -> None:
+        torch = _torch()
+        while True:
+            per = int(lib.ss_stage_counts_workspace(self.fcap, self.ccap, 17))
+            per = (per + 255) // 256 * 256
+            ws = torch.empty(per * self.exact.size, dtype=torch.uint8, device=self.dev)
+            N.check(lib.ss_stage_counts_exact(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members),
+                                              N.ptr(self.gsize), N.ptr(self.status), N.ptr(self.aux),
+                                              N.ptr(self.exact_list), int(self.exact.size), N.ptr(ws), per,
+                                              self.fcap, self.ccap, N.ptr(self.sweep_stats), st),
+                    "ss_stage_counts_exact")
+            status = self.status.cpu().numpy()[self.exact]
+            if not (status == SS_WORKSPACE).any():
+                return
+            need = int(self.aux.cpu().numpy()[self.exact].max())
+            self.fcap = max(self.fcap * 4, need * 2)
+            self.ccap = max(self.ccap * 4, need * 2)
+            bad = self.exact[status == SS_WORKSPACE]
+            self.status[torch.from_numpy(bad).to(self.dev)] = SS_OK
+            if self.ccap > 1 << 24:
+                raise MemoryError("exact sweep frontier exceeds 16M children")
+
+    # -- objective + score + best -----------------------------------------
+    def score_and_best(self, t_comp, rtt, kpow: np.ndarray, fill_all: bool = False) -> None:
+        torch = _torch()
+        lib = N.lib()
+        st = N.stream_handle(self.stream)
+        ps = self.pool_set()
+        self._t = t_comp if torch.is_tensor(t_comp) else torch.as_tensor(np.asarray(t_comp, dtype=np.float64)).to(self.dev)
+        self._r = rtt if torch.is_tensor(rtt) else torch.as_tensor(np.asarray(rtt, dtype=np.float64)).to(self.dev)
+        self._kpow = torch.from_numpy(np.asarray(kpow, dtype=np.float64)).to(self.dev)
+        N.check(lib.ss_phase1_score(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members), N.ptr(self.gsize),
+                                    N.ptr(self._t), N.ptr(self._r), N.ptr(self._kpow), int(self._kpow.numel()),
+                                    int(fill_all), N.ptr(self.z), N.ptr(self.counts), N.ptr(self.kstatus),
+                                    N.ptr(self.fstatus), N.ptr(self.all_pool), N.ptr(self.all_k), self.n_cand, st),
+                "ss_phase1_score")
+        N.check(lib.ss_phase1_best(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members), N.ptr(self.gsize),
+                                   N.ptr(self.z), N.ptr(self.kstatus), N.ptr(self.fstatus), int(fill_all),
+                                   N.ptr(self.best_k), N.ptr(self.counts), N.ptr(self.status), st), "ss_phase1_best")
+
+    # -- host views ---------------------------------------------------------
+    def fetch(self) -> "PoolResults":
+        return PoolResults(self)
+
+
+class PoolResults:
+    """Host copy of a PoolBatch's outputs with reference-shaped accessors."""
+
+    def __init__(self, b: PoolBatch):
+        self.b = b
+        self.stages = b.stages.cpu().numpy()
+        self.members = b.members.cpu().numpy()
+        self.gsize = b.gsize.cpu().numpy()
+        self.status = b.status.cpu().numpy()
+        self.aux = b.aux.cpu().numpy()
+        self.z = b.z.cpu().numpy()
+        self.counts = b.counts.cpu().numpy()
+        self.best_k = b.best_k.cpu().numpy()
+        self.sweep_stats = b.sweep_stats.cpu().numpy().reshape(-1, 4)
+
+    def raise_pool(self, p: int) -> None:
+        st = int(self.status[p])
+        if st != SS_OK:
+            raise_for_status(st, int(self.aux[p]), detail=f"pool {p}")
+
+    def solutions(self, p: int):
+        """{k: (stages, groups)} in increasing k (allocator.py:499-504 shape)."""
+        b = self.b
+        n, km = int(b.n[p]), int(b.km[p])
+        out = {}
+        for k in range(1, km + 1):
+            s = int(self.stages[b.koff_h[p] + k - 1])
+            if s == 0:
+                continue
+            base = int(b.memb_h[p] + (k - 1) * n)
+            gbase = int(b.gsz_h[p] + (k - 1) * km)
+            groups, pos = [], 0
+            for g in range(k):
+                sz = int(self.gsize[gbase + g])
+                groups.append(tuple(int(x) for x in self.members[base + pos: base + pos + sz]))
+                pos += sz
+            out[k] = (s, tuple(groups))
+        return out
+
+    def z_of(self, p: int, k: int) -> float:
+        return float(self.z[self.b.koff_h[p] + k - 1])
+
+    def counts_of(self, p: int, k: int):
+        b = self.b
+        base = int(b.memb_h[p] + (k - 1) * int(b.n[p]))
+        total = int(self.stages[b.koff_h[p] + k - 1])
+        return [int(x) for x in self.counts[base: base + total]]
+
+
+def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int], tokens: float, stream=None):
+    """estimate_objective_params for many regions on device.
+
+    items: list of (flops_in_cluster_order, links) where links is a list of
+    (a_idx, b_idx, rtt) with region-local cluster-order indices.  Returns
+    device tensors (t_comp, rtt).
+    """
+    torch = _torch()
+    lib = N.lib()
+    dev = torch.device("cuda")
+    n = np.array([len(f) for f, _ in items], dtype=np.int64)
+    item_ptr = np.concatenate([[0], np.cumsum(n)])
+    mat_off = np.concatenate([[0], np.cumsum(n * n)])
+    flops = np.concatenate([np.asarray(f, dtype=np.float64) for f, _ in items])
+    li, la, lb, lv = [], [], [], []
+    for i, (_, links) in enumerate(items):
+        for a, b, v in links:
+            li.append(i)
+            la.append(a)
+            lb.append(b)
+            lv.append(v)
+    st = N.stream_handle(stream)
+    I = len(items)
+    ints = torch.from_numpy(np.concatenate([item_ptr, n, layers, li, la, lb]).astype(np.int32)).to(dev)
+    item_ptr_d, dim_d = ints[:I + 1], ints[I + 1:2 * I + 1]
+    layers_d = ints[2 * I + 1:3 * I + 1]
+    nl = len(li)
+    li_d, la_d, lb_d = ints[3 * I + 1:3 * I + 1 + nl], ints[3 * I + 1 + nl:3 * I + 1 + 2 * nl], ints[3 * I + 1 + 2 * nl:]
+    off_d = torch.from_numpy(mat_off[:-1].astype(np.int64)).to(dev)
+    lv_d = torch.from_numpy(np.asarray(lv, dtype=np.float64)).to(dev) if nl else None
+    flops_d = torch.from_numpy(flops).to(dev)
+    rtt = torch.empty(max(int(mat_off[-1]), 1), dtype=torch.float64, device=dev)
+    if I > 65535:
+        raise ValueError("at most 65535 objective regions per call")
+    N.check(lib.ss_rtt_fill(I, N.ptr(off_d), N.ptr(dim_d), N.ptr(rtt), float(default_rtt), nl,
+                            N.ptr(li_d) if nl else None, N.ptr(la_d) if nl else None, N.ptr(lb_d) if nl else None,
+                            N.ptr(lv_d), st), "ss_rtt_fill")
+    t = torch.empty(I, dtype=torch.float64, device=dev)
+    r = torch.empty(I, dtype=torch.float64, device=dev)
+    N.check(lib.ss_objective(I, N.ptr(item_ptr_d), N.ptr(flops_d), N.ptr(off_d), N.ptr(rtt), float(fpl),
+                             N.ptr(layers_d), float(tokens), N.ptr(t), N.ptr(r), st), "ss_objective")
+    return t, r

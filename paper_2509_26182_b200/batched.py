@@ -164,3 +164,80 @@ class ScenarioReplayer:
     def bytes_per_selection(self) -> np.ndarray:
         cl = self.col_len.view(self.S, self.L).cpu().numpy().astype(np.int64)
         return 8 * (cl[:, :-1] * cl[:, 1:]).sum(axis=1) + 8 * cl.sum(axis=1) + 4 * self.L
+
+
+# ---------------------------------------------------------------------------
+# Phase-1 candidate sweep (C3 / C5): allocate() over many pool variants
+# ---------------------------------------------------------------------------
+
+@dataclass
+class PackedVariants:
+    """Pools of many allocate() calls, already in device order.
+
+    pools[p] = (caps sorted by (-cap, id), flops in that order, L, kmax);
+    obj_flops[p] = flops in CLUSTER order, obj_rtt[p] = dense rtt_s matrix in
+    cluster order (the objective's inputs); var_ptr[v] = first pool of variant v;
+    region names / gpu ids are kept host-side only for plan assembly.
+    """
+
+    pools: list
+    obj_flops: list
+    obj_rtt: list
+    var_ptr: np.ndarray
+    fpl: float
+    layers: int
+    tokens: float = 128.0
+    alpha: float = 1.0
+
+    @property
+    def n_variants(self) -> int:
+        return int(self.var_ptr.size - 1)
+
+    @property
+    def n_candidates(self) -> int:
+        return int(sum(p.kmax for p in self.pools))
+
+
+class VariantSweep:
+    """Device Phase-1 over PackedVariants: stage counts, objective, Z(k), water-fill of
+    every candidate's groups (fill_all), best k per region, objective fold per
+    variant, global argmax (ties -> lowest variant)."""
+
+    def __init__(self, packed: PackedVariants, *, fill_all: bool = True, stream=None):
+        import torch
+        from ._phase1 import PoolBatch
+        self.torch = torch
+        self.packed = packed
+        self.fill_all = fill_all
+        self.stream = stream
+        self.batch = PoolBatch(packed.pools, stream=stream)
+        dev = self.batch.dev
+        n = np.array([len(f) for f in packed.obj_flops], dtype=np.int64)
+        self.item_ptr = torch.from_numpy(np.concatenate([[0], np.cumsum(n)]).astype(np.int32)).to(dev)
+        self.mat_off = torch.from_numpy(np.concatenate([[0], np.cumsum(n * n)[:-1]]).astype(np.int64)).to(dev)
+        self.obj_flops = torch.from_numpy(np.concatenate(packed.obj_flops).astype(np.float64)).to(dev)
+        self.obj_rtt = torch.from_numpy(np.concatenate([m.reshape(-1) for m in packed.obj_rtt])).to(dev)
+        self.layers = torch.full((len(packed.pools),), packed.layers, dtype=torch.int32, device=dev)
+        self.var_ptr = torch.from_numpy(packed.var_ptr.astype(np.int32)).to(dev)
+        V = packed.n_variants
+        self.t = torch.empty(len(packed.pools), dtype=torch.float64, device=dev)
+        self.r = torch.empty(len(packed.pools), dtype=torch.float64, device=dev)
+        self.total = torch.empty(V, dtype=torch.float64, device=dev)
+        self.feasible = torch.empty(V, dtype=torch.int32, device=dev)
+        self.best_variant = torch.empty(1, dtype=torch.int32, device=dev)
+        self.best_total = torch.empty(1, dtype=torch.float64, device=dev)
+        km = max(int(self.batch.km.max()), 1)
+        self.kpow = np.array([0.0] + [float(k ** packed.alpha) for k in range(1, km + 1)])
+
+    def run(self) -> None:
+        lib = N.lib()
+        st = N.stream_handle(self.stream)
+        b = self.batch
+        b.stage_counts()
+        N.check(lib.ss_objective(len(self.packed.pools), N.ptr(self.item_ptr), N.ptr(self.obj_flops),
+                                 N.ptr(self.mat_off), N.ptr(self.obj_rtt), float(self.packed.fpl), N.ptr(self.layers),
+                                 float(self.packed.tokens), N.ptr(self.t), N.ptr(self.r), st), "ss_objective")
+        b.score_and_best(self.t, self.r, self.kpow, fill_all=self.fill_all)
+        N.check(lib.ss_variant_reduce(self.packed.n_variants, N.ptr(self.var_ptr), N.ptr(b.koff), N.ptr(b.best_k),
+                                      N.ptr(b.z), N.ptr(b.status), N.ptr(self.total), N.ptr(self.feasible),
+                                      N.ptr(self.best_variant), N.ptr(self.best_total), st), "ss_variant_reduce")

@@ -1,0 +1,1163 @@
+// Phase-1 on device: stage-count search, objective,
+// score / best k, water-filling -- bit-exact restatements of the reference's
+// branchy Python (allocator.py, waterfill.py) as integer / fp64 device code.
+//
+//  * constructive cover (allocator.py:267-470): ONE THREAD PER CANDIDATE
+//    (pool, k).  Groups are intrusive linked lists so Python list semantics
+//    (append, pop(pos), positional swap, remove-first, stable sort) carry over
+//    exactly; the budgeted peel recursion (353-423) is an explicit frame stack
+//    whose "remaining" lists are 128-bit masks (they are always ascending
+//    subsets of range(m)) and whose subset-sum reach sets are 256-bit words.
+//  * exact sweep (allocator.py:138-264): one thread per pool, level frontier in
+//    a global workspace with packed 16-byte residual keys whose unsigned order
+//    is Python's tuple order (shorter prefix first); "first producer wins" is a
+//    stable (key, producer-order) sort + dedup.
+//  * objective (allocator.py:516-538) and water-fill (waterfill.py:47-183)
+//    reproduce CPython 3.12 sum() (Neumaier with int/float item typing) and
+//    IEEE rounding of every operation (built with -fmad=false).
+// Phase-1 is issue-bound integer work, not HBM-bound.
+#include <float.h>
+#include <math.h>
+
+#include "ss_common.cuh"
+
+namespace {
+
+constexpr int NMAX = 256;      // usable gpus per pool (constructive path)
+constexpr int KMAX = 256;
+constexpr int LMAX_PEEL = 128; // 2L <= 256-bit reach words
+constexpr int BWORDS = 4;
+constexpr int EXACT_LIMIT = 16;
+constexpr uint16_t NIL = 0xFFFF;
+
+// ---------------------------------------------------------------------------
+// CPython 3.12 sum() over int / float items, start = 0
+// ---------------------------------------------------------------------------
+struct PySum {
+    bool is_int;
+    long long iacc;
+    double f, c;
+    __device__ void init() { is_int = true; iacc = 0; f = 0.0; c = 0.0; }
+    __device__ void add_int(long long v) {
+        if (is_int) iacc += v;
+        else f = __dadd_rn(f, (double)v);
+    }
+    __device__ void add_float(double x) {
+        if (is_int) {           // int accumulator meets its first float: plain add, compensation starts
+            f = __dadd_rn((double)iacc, x);
+            c = 0.0;
+            is_int = false;
+            return;
+        }
+        const double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        f = t;
+    }
+    __device__ double value() const {
+        if (is_int) return (double)iacc;
+        double r = f;
+        if (c != 0.0 && isfinite(c)) r = __dadd_rn(r, c);
+        return r;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// water-fill (waterfill.py:47-183)
+// ---------------------------------------------------------------------------
+__device__ double fill_at(double level, const double* fl, const int* cap, int n) {
+    PySum s;
+    s.init();
+    for (int i = 0; i < n; ++i) {
+        const double x = __dmul_rn(level, fl[i]);
+        if (x < (double)cap[i]) s.add_float(x);   // min(c, x) is the float only when x < c
+        else s.add_int(cap[i]);
+    }
+    return s.value();
+}
+
+__device__ int water_level(const double* fl, const int* cap, int n, int L, double* targets, int* tflag,
+                           double* level_out, int* aux) {
+    if (n < 1 || L < 1) return SS_BAD_INPUT;
+    long long total = 0;
+    double minf = fl[0];
+    for (int i = 0; i < n; ++i) {
+        if (!(fl[i] > 0.0)) return SS_BAD_INPUT;
+        total += cap[i];
+        if (fl[i] < minf) minf = fl[i];
+    }
+    if (total < L) { *aux = (int)total; return SS_INFEASIBLE_CAPACITY; }
+    const double Ld = (double)L;
+    double lo = 0.0;
+    double hi = __dadd_rn(__ddiv_rn(Ld, minf), 1.0);
+    const double tol = __dmul_rn(1e-9, Ld);
+    for (int it = 0; it < 200; ++it) {
+        if (fabs(__dsub_rn(fill_at(hi, fl, cap, n), Ld)) <= tol) break;
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        if (fill_at(mid, fl, cap, n) >= Ld) hi = mid;
+        else lo = mid;
+    }
+    if (fabs(__dsub_rn(fill_at(hi, fl, cap, n), Ld)) > __dmul_rn(2.0, tol)) return SS_ROUNDING_OVERFLOW;
+    for (int i = 0; i < n; ++i) {
+        const double x = __dmul_rn(hi, fl[i]);
+        const bool f = x < (double)cap[i];
+        if (targets) targets[i] = f ? x : (double)cap[i];
+        if (tflag) tflag[i] = f ? 0 : 1;
+    }
+    if (level_out) *level_out = hi;
+    return SS_OK;
+}
+
+// largest-remainder rounding; targets given as (value, is_int)
+__device__ int hamilton(const double* t, const int* tint, const int* cap, int n, long long total, int* out) {
+    long long fl_sum = 0;
+    for (int i = 0; i < n; ++i) {
+        long long f = tint[i] ? (long long)t[i] : (long long)floor(t[i]);
+        if (f > cap[i]) f = cap[i];
+        out[i] = (int)f;
+        fl_sum += f;
+    }
+    long long left = total - fl_sum;
+    if (left < 0) return SS_ROUNDING_OVERFLOW;
+    // order by (-(t - floor), i): remainder descending, index ascending
+    int order[NMAX];
+    double rem[NMAX];
+    for (int i = 0; i < n; ++i) {
+        rem[i] = tint[i] ? 0.0 : __dsub_rn(t[i], (double)out[i]);
+        int j = i;
+        while (j > 0 && rem[order[j - 1]] < rem[i]) { order[j] = order[j - 1]; --j; }
+        order[j] = i;
+    }
+    for (int q = 0; q < n && left > 0; ++q) {
+        const int i = order[q];
+        if (out[i] < cap[i]) { out[i] += 1; --left; }
+    }
+    for (int i = 0; i < n && left > 0; ++i)
+        while (left > 0 && out[i] < cap[i]) { out[i] += 1; --left; }
+    return left > 0 ? SS_ROUNDING_OVERFLOW : SS_OK;
+}
+
+__device__ int stage_lengths(const double* fl, const int* cap, int n, int L, int* out, int* aux) {
+    if (n > NMAX) return SS_BAD_INPUT;
+    for (int i = 0; i < n; ++i)
+        if (cap[i] < 1) { *aux = i; return SS_ZERO_CAPACITY; }
+    double t[NMAX];
+    int ti[NMAX];
+    double lvl;
+    int st = water_level(fl, cap, n, L, t, ti, &lvl, aux);
+    if (st != SS_OK) return st;
+    st = hamilton(t, ti, cap, n, L, out);
+    if (st != SS_OK) return st;
+    for (;;) {
+        int needy = -1;
+        for (int i = 0; i < n; ++i) if (out[i] == 0) { needy = i; break; }
+        if (needy < 0) break;
+        int donor = 0;
+        for (int i = 1; i < n; ++i) if (out[i] > out[donor]) donor = i;   // (count, -i): lowest index on ties
+        if (out[donor] < 2) return SS_ROUNDING_OVERFLOW;
+        out[donor] -= 1;
+        out[needy] += 1;
+    }
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// constructive cover: best-fit with repairs (allocator.py:267-350)
+// ---------------------------------------------------------------------------
+struct Lists {
+    uint16_t head[KMAX], tail[KMAX], size[KMAX];
+    uint16_t next[NMAX], item[NMAX];
+    int tot[KMAX];
+
+    __device__ void reset(int k) {
+        for (int g = 0; g < k; ++g) { head[g] = tail[g] = NIL; size[g] = 0; tot[g] = 0; }
+    }
+    __device__ void append(int g, int node) {
+        next[node] = NIL;
+        if (head[g] == NIL) head[g] = (uint16_t)node;
+        else next[tail[g]] = (uint16_t)node;
+        tail[g] = (uint16_t)node;
+        size[g]++;
+    }
+    __device__ int node_at(int g, int pos) const {
+        int nd = head[g];
+        for (int p = 0; p < pos; ++p) nd = next[nd];
+        return nd;
+    }
+    __device__ void unlink(int g, int prev, int nd) {
+        if (prev == NIL) head[g] = next[nd];
+        else next[prev] = next[nd];
+        if (tail[g] == nd) tail[g] = (uint16_t)prev;
+        size[g]--;
+    }
+    __device__ int pop_at(int g, int pos) {
+        int prev = NIL, nd = head[g];
+        for (int p = 0; p < pos; ++p) { prev = nd; nd = next[nd]; }
+        unlink(g, prev, nd);
+        return nd;
+    }
+    __device__ void remove_item(int g, int it) {
+        int prev = NIL, nd = head[g];
+        while (nd != NIL && item[nd] != it) { prev = nd; nd = next[nd]; }
+        if (nd != NIL) unlink(g, prev, nd);
+    }
+};
+
+__device__ __forceinline__ int cval(const int* caps, int i, int L) { return caps[i] < L ? caps[i] : L; }
+
+__device__ bool best_fit(const int* caps, int m, int k, int L, Lists& G) {
+    G.reset(k);
+    for (int g = 0; g < k; ++g) {
+        G.item[g] = (uint16_t)g;
+        G.append(g, g);
+        G.tot[g] = cval(caps, g, L);
+    }
+    for (int i = k; i < m; ++i) {
+        int best = -1;
+        for (int g = 0; g < k; ++g)
+            if (G.tot[g] < L && (best < 0 || G.tot[g] > G.tot[best])) best = g;
+        if (best < 0) break;
+        G.item[i] = (uint16_t)i;
+        G.append(best, i);
+        G.tot[best] += cval(caps, i, L);
+    }
+    uint16_t opened[KMAX];
+    for (int round = 0; round < 4; ++round) {
+        int n_open = 0;
+        for (int g = 0; g < k; ++g) if (G.tot[g] < L) opened[n_open++] = (uint16_t)g;
+        if (n_open == 0) break;
+        bool changed = false;
+        for (int q = 0; q < n_open; ++q) {
+            const int u = opened[q];
+            if (G.tot[u] >= L) continue;
+            // move: key (closes, closes ? -val : val), strict >, first (g, pos) wins
+            int bg = -1, bpos = -1, bclose = 0, bval = 0;
+            for (int g = 0; g < k; ++g) {
+                if (g == u) continue;
+                int pos = 0;
+                for (int nd = G.head[g]; nd != NIL; nd = G.next[nd], ++pos) {
+                    const int v = cval(caps, G.item[nd], L);
+                    if (G.size[g] == 1 || G.tot[g] - v < L) continue;
+                    const int closes = G.tot[u] + v >= L;
+                    const int key = closes ? -v : v;
+                    if (bg < 0 || closes > bclose || (closes == bclose && key > bval)) {
+                        bg = g; bpos = pos; bclose = closes; bval = key;
+                    }
+                }
+            }
+            if (bg >= 0) {
+                const int nd = G.pop_at(bg, bpos);
+                const int v = cval(caps, G.item[nd], L);
+                G.tot[bg] -= v;
+                G.tot[u] += v;
+                G.append(u, nd);
+                changed = true;
+                continue;
+            }
+            // swap: max strictly positive gain keeping the donor closed
+            int sg = -1, sgp = -1, sup = -1, gain_best = 0;
+            for (int g = 0; g < k; ++g) {
+                if (g == u || G.tot[g] < L) continue;
+                int gp = 0;
+                for (int nb = G.head[g]; nb != NIL; nb = G.next[nb], ++gp) {
+                    const int vb = cval(caps, G.item[nb], L);
+                    int up = 0;
+                    for (int na = G.head[u]; na != NIL; na = G.next[na], ++up) {
+                        const int gain = vb - cval(caps, G.item[na], L);
+                        if (gain <= gain_best) continue;
+                        if (G.tot[g] - gain >= L) { gain_best = gain; sg = g; sgp = gp; sup = up; }
+                    }
+                }
+            }
+            if (sg >= 0) {
+                const int nb = G.node_at(sg, sgp), na = G.node_at(u, sup);
+                const uint16_t t = G.item[nb];
+                G.item[nb] = G.item[na];
+                G.item[na] = t;
+                G.tot[sg] -= gain_best;
+                G.tot[u] += gain_best;
+                changed = true;
+            }
+        }
+        if (!changed) break;
+    }
+    for (int g = 0; g < k; ++g) if (G.tot[g] < L) return false;
+    // minimal witness: shed spare members in stable ascending-value order
+    uint16_t order[NMAX];
+    for (int g = 0; g < k; ++g) {
+        int cnt = 0;
+        for (int nd = G.head[g]; nd != NIL; nd = G.next[nd]) {
+            const uint16_t it = G.item[nd];
+            const int v = cval(caps, it, L);
+            int j = cnt++;
+            while (j > 0 && cval(caps, order[j - 1], L) > v) { order[j] = order[j - 1]; --j; }
+            order[j] = it;
+        }
+        for (int q = 0; q < cnt; ++q) {
+            const int it = order[q];
+            const int v = cval(caps, it, L);
+            if (G.size[g] > 1 && G.tot[g] - v >= L) {
+                G.remove_item(g, it);
+                G.tot[g] -= v;
+            }
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// constructive cover: budgeted peel (allocator.py:353-423)
+// ---------------------------------------------------------------------------
+struct Mask {   // subset of range(m), m <= 256
+    uint64_t w[4];
+    __device__ void clear() { w[0] = w[1] = w[2] = w[3] = 0; }
+    __device__ bool test(int i) const { return (w[i >> 6] >> (i & 63)) & 1ull; }
+    __device__ void set(int i) { w[i >> 6] |= 1ull << (i & 63); }
+    __device__ int count() const { return __popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]) + __popcll(w[3]); }
+};
+
+struct Bits {
+    uint64_t w[BWORDS];
+};
+
+__device__ __forceinline__ void bits_shl_or(Bits& dst, const Bits& src, int s, int nbits) {
+    // dst = src | ((src << s) & (2^nbits - 1))
+    const int ws = s >> 6, bs = s & 63;
+#pragma unroll
+    for (int q = BWORDS - 1; q >= 0; --q) {
+        uint64_t v = 0;
+        const int from = q - ws;
+        if (from >= 0) {
+            v = src.w[from] << bs;
+            if (bs && from - 1 >= 0) v |= src.w[from - 1] >> (64 - bs);
+        }
+        const int lo = q * 64;
+        if (lo >= nbits) v = 0;
+        else if (nbits - lo < 64) v &= (1ull << (nbits - lo)) - 1ull;
+        dst.w[q] = src.w[q] | v;
+    }
+}
+
+__device__ __forceinline__ bool bits_test(const Bits& b, int i) { return (b.w[i >> 6] >> (i & 63)) & 1ull; }
+
+struct Frame {          // one peel() activation; its pool = range(m) minus the picks of frames above it
+    Mask picked;
+    int total, need;
+    short targets[4];
+    signed char nt, ti;
+};
+
+__device__ void frame_pool(const Frame* fr, int d, int m, Mask& pool) {
+    pool.clear();
+    for (int i = 0; i < m; ++i) pool.set(i);
+    for (int q = 0; q < d; ++q)
+        for (int w = 0; w < 4; ++w) pool.w[w] &= ~fr[q].picked.w[w];
+}
+
+__device__ int pool_items(const Mask& pool, int m, uint16_t* items) {
+    int n = 0;
+    for (int i = 0; i < m; ++i) if (pool.test(i)) items[n++] = (uint16_t)i;
+    return n;
+}
+
+__device__ void compute_reach(const int* caps, int L, const uint16_t* items, int n, Bits* reach) {
+    for (int q = 0; q < BWORDS; ++q) reach[0].w[q] = 0;
+    reach[0].w[0] = 1;
+    for (int p = 0; p < n; ++p) bits_shl_or(reach[p + 1], reach[p], cval(caps, items[p], L), 2 * L);
+}
+
+// returns true on success; the k groups are then fr[0..k-1].picked, in peel order
+__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reach, uint16_t* items) {
+    int budget = m <= 24 ? 300 : 80;
+    int d = 0;
+    int total = 0;
+    for (int i = 0; i < m; ++i) total += cval(caps, i, L);
+    fr[0].total = total;
+    fr[0].need = k;
+    enum { ENTER, TRY, RET } state = ENTER;
+    bool ok = false;
+    int reach_owner = -1;
+    for (;;) {
+        if (state == ENTER) {
+            Frame& f = fr[d];
+            if (f.need == 0) { ok = true; state = RET; continue; }
+            if (budget <= 0) { ok = false; state = RET; continue; }
+            --budget;
+            Mask pool;
+            frame_pool(fr, d, m, pool);
+            if (f.total < f.need * L || pool.count() < f.need) { ok = false; state = RET; continue; }
+            if (f.need == 1) {
+                int short_ = L;
+                f.picked.clear();
+                ok = false;
+                for (int i = 0; i < m; ++i) {
+                    if (!pool.test(i)) continue;
+                    f.picked.set(i);
+                    short_ -= cval(caps, i, L);
+                    if (short_ <= 0) { ok = true; break; }
+                }
+                state = RET;
+                continue;
+            }
+            const int n = pool_items(pool, m, items);
+            compute_reach(caps, L, items, n, reach);
+            reach_owner = d;
+            f.nt = 0;
+            for (int t = L; t < 2 * L && f.nt < 4; ++t)
+                if (bits_test(reach[n], t)) f.targets[f.nt++] = (short)t;
+            f.ti = 0;
+            state = TRY;
+            continue;
+        }
+        if (state == TRY) {
+            Frame& f = fr[d];
+            if (f.ti >= f.nt) { ok = false; state = RET; continue; }
+            Mask pool;
+            frame_pool(fr, d, m, pool);
+            const int n = pool_items(pool, m, items);
+            if (reach_owner != d) { compute_reach(caps, L, items, n, reach); reach_owner = d; }
+            const int tgt = f.targets[f.ti];
+            int rem = tgt;
+            f.picked.clear();
+            for (int pos = n - 1; pos >= 0; --pos) {
+                if (bits_test(reach[pos], rem)) continue;
+                f.picked.set(items[pos]);
+                rem -= cval(caps, items[pos], L);
+            }
+            Frame& c = fr[d + 1];
+            c.total = f.total - tgt;
+            c.need = f.need - 1;
+            ++d;
+            state = ENTER;
+            continue;
+        }
+        // RET (on success fr[0..k-1].picked already hold the groups)
+        if (d == 0) break;
+        --d;
+        if (ok) continue;             // keep unwinding, recording picks
+        fr[d].ti++;
+        state = TRY;
+    }
+    return ok;
+}
+
+// ---------------------------------------------------------------------------
+// exact sweep (allocator.py:114-264), one thread per pool
+// ---------------------------------------------------------------------------
+struct SRec {            // one state: residual bytes (value+1, zero padded) as a 128-bit big-endian key
+    uint64_t hi, lo;
+    uint8_t done, m, action;   // action: slot, or 0xFF = start
+    uint8_t pad;
+    int32_t aux;               // children: producer order; kept states: parent index in previous level
+};
+
+__device__ __forceinline__ void unpack(const SRec& r, uint8_t* res) {
+    for (int p = 0; p < r.m; ++p) {
+        const uint64_t w = p < 8 ? r.hi : r.lo;
+        res[p] = (uint8_t)((w >> (8 * (7 - (p & 7)))) & 0xFF) - 1;
+    }
+}
+
+__device__ __forceinline__ void pack(SRec& r, const uint8_t* res, int m) {
+    r.hi = r.lo = 0;
+    for (int p = 0; p < m; ++p) {
+        const uint64_t b = (uint64_t)(res[p] + 1) << (8 * (7 - (p & 7)));
+        if (p < 8) r.hi |= b; else r.lo |= b;
+    }
+    r.m = (uint8_t)m;
+}
+
+__device__ __forceinline__ bool key_less(const SRec& a, const SRec& b) {
+    if (a.hi != b.hi) return a.hi < b.hi;
+    if (a.lo != b.lo) return a.lo < b.lo;
+    return a.done < b.done;
+}
+
+__device__ __forceinline__ bool key_eq(const SRec& a, const SRec& b) {
+    return a.hi == b.hi && a.lo == b.lo && a.done == b.done;
+}
+
+// class order: (done, m, residual key)
+__device__ __forceinline__ bool class_less(const SRec& a, const SRec& b) {
+    if (a.done != b.done) return a.done < b.done;
+    if (a.m != b.m) return a.m < b.m;
+    if (a.hi != b.hi) return a.hi < b.hi;
+    return a.lo < b.lo;
+}
+
+template <class Less>
+__device__ void merge_sort_idx(int32_t* idx, int32_t* tmp, int n, Less less) {
+    for (int width = 1; width < n; width *= 2) {
+        for (int lo = 0; lo < n; lo += 2 * width) {
+            const int mid = min(lo + width, n), hi = min(lo + 2 * width, n);
+            int a = lo, b = mid, o = lo;
+            while (a < mid && b < hi) tmp[o++] = less(idx[b], idx[a]) ? idx[b++] : idx[a++];
+            while (a < mid) tmp[o++] = idx[a++];
+            while (b < hi) tmp[o++] = idx[b++];
+        }
+        for (int i = 0; i < n; ++i) idx[i] = tmp[i];
+    }
+}
+
+__device__ __forceinline__ void insert_sorted(uint8_t* res, int& m, uint8_t v) {
+    int j = m++;
+    while (j > 0 && res[j - 1] > v) { res[j] = res[j - 1]; --j; }
+    res[j] = v;
+}
+
+struct SweepWs {
+    SRec* states;     // all kept states, level after level
+    SRec* kids;       // children of the current level
+    int32_t* idx;     // sort permutation
+    int32_t* tmp;
+    int32_t* keep;    // class-sorted kept list scratch
+};
+
+__device__ int exact_sweep(const int* caps, int n, int L, int kmax, SweepWs ws, int fcap, int ccap,
+                           int* level_start, int* found, int* need, int* stats) {
+    // stats (SweepStats, allocator.py:87-94): levels, states_expanded, peak_frontier, pruned_dominated
+    stats[0] = stats[1] = stats[2] = stats[3] = 0;
+    int suffix[EXACT_LIMIT + 1];
+    suffix[n] = 0;
+    for (int i = n - 1; i >= 0; --i) suffix[i] = suffix[i + 1] + caps[i];
+    const int kcap = kmax < EXACT_LIMIT ? kmax : EXACT_LIMIT;
+    for (int k = 0; k <= kcap; ++k) found[k] = 0;
+    int nfound = 0;
+    // level 0: root
+    SRec root;
+    root.hi = root.lo = 0; root.done = 0; root.m = 0; root.action = 0; root.aux = -1;
+    ws.states[0] = root;
+    level_start[0] = 0;
+    level_start[1] = 1;
+    int total_states = 1;
+    int levels = 0;
+    uint8_t res[EXACT_LIMIT + 1], child[EXACT_LIMIT + 1];
+    for (int i = 0; i < n; ++i) {
+        const int cap = caps[i];
+        const int f0 = level_start[i], f1 = level_start[i + 1];
+        int nk = 0;
+        stats[1] += f1 - f0;
+        for (int s = f0; s < f1; ++s) {
+            const SRec st = ws.states[s];
+            unpack(st, res);
+            const int m = st.m;
+            for (int slot = 0; slot <= m; ++slot) {
+                const bool start = slot == m;
+                if (!start && slot > 0 && res[slot] == res[slot - 1]) continue;
+                if (start && !(st.done + m < kmax)) continue;
+                int cm = 0;
+                int left;
+                if (start) {
+                    for (int p = 0; p < m; ++p) child[cm++] = res[p];
+                    left = L - cap;
+                } else {
+                    for (int p = 0; p < m; ++p) if (p != slot) child[cm++] = res[p];
+                    left = (int)res[slot] - cap;
+                }
+                SRec c;
+                c.done = st.done;
+                if (left <= 0) c.done = st.done + 1;
+                else insert_sorted(child, cm, (uint8_t)left);
+                pack(c, child, cm);
+                c.action = start ? 0xFF : (uint8_t)slot;
+                c.aux = (s - f0) * 32 + (start ? 31 : slot);   // producer order
+                if (nk >= ccap) { *need = nk + 1; return SS_WORKSPACE; }
+                ws.kids[nk++] = c;
+            }
+        }
+        // stable "first producer wins": sort by (key, producer order), keep first per key
+        for (int q = 0; q < nk; ++q) ws.idx[q] = q;
+        merge_sort_idx(ws.idx, ws.tmp, nk, [&](int a, int b) {
+            const SRec& x = ws.kids[a];
+            const SRec& y = ws.kids[b];
+            if (!key_eq(x, y)) return key_less(x, y);
+            return x.aux < y.aux;
+        });
+        // dedup + feasibility (in key order) -> idx[0..nu)
+        const int remaining = n - (i + 1);
+        int nu = 0;
+        for (int q = 0; q < nk; ++q) {
+            const SRec& c = ws.kids[ws.idx[q]];
+            if (nu > 0 && key_eq(ws.kids[ws.idx[nu - 1]], c)) continue;
+            ws.idx[nu++] = ws.idx[q];
+        }
+        int nf = 0;
+        for (int q = 0; q < nu; ++q) {
+            const SRec& c = ws.kids[ws.idx[q]];
+            unpack(c, child);
+            int sum = 0;
+            for (int p = 0; p < c.m; ++p) sum += child[p];
+            if (c.m > remaining || sum > suffix[i + 1]) continue;
+            ws.idx[nf++] = ws.idx[q];
+        }
+        // dominance inside (done, m) classes: sort a copy by class order
+        for (int q = 0; q < nf; ++q) ws.keep[q] = ws.idx[q];
+        merge_sort_idx(ws.keep, ws.tmp, nf, [&](int a, int b) { return class_less(ws.kids[a], ws.kids[b]); });
+        // mark kept: reuse SRec.pad as flag
+        for (int q = 0; q < nf; ++q) ws.kids[ws.keep[q]].pad = 0;
+        int cls_start = 0;
+        uint8_t cres[EXACT_LIMIT + 1], ores[EXACT_LIMIT + 1];
+        for (int q = 0; q < nf; ++q) {
+            const SRec& c = ws.kids[ws.keep[q]];
+            if (q > 0) {
+                const SRec& pr = ws.kids[ws.keep[q - 1]];
+                if (pr.done != c.done || pr.m != c.m) cls_start = q;
+            }
+            unpack(c, cres);
+            bool dominated = false;
+            for (int o = cls_start; o < q && !dominated; ++o) {
+                const SRec& other = ws.kids[ws.keep[o]];
+                if (!other.pad) continue;
+                unpack(other, ores);
+                bool all_le = true;
+                for (int p = 0; p < c.m; ++p) if (ores[p] > cres[p]) { all_le = false; break; }
+                dominated = all_le;
+            }
+            if (!dominated) ws.kids[ws.keep[q]].pad = 1;
+            else stats[3] += 1;
+        }
+        // compact kept states in key order into the next level
+        const int base = total_states;
+        int nn = 0;
+        for (int q = 0; q < nf; ++q) {
+            SRec c = ws.kids[ws.idx[q]];
+            if (!c.pad) continue;
+            if (base + nn >= fcap) { *need = base + nn + 1; return SS_WORKSPACE; }
+            c.aux = c.aux / 32;       // parent index within previous level
+            c.pad = 0;
+            ws.states[base + nn++] = c;
+        }
+        total_states = base + nn;
+        level_start[i + 2] = total_states;
+        levels = i + 1;
+        stats[0] = levels;
+        if (nn > stats[2]) stats[2] = nn;
+        for (int q = 0; q < nn; ++q) {
+            const SRec& c = ws.states[base + q];
+            if (c.m == 0 && c.done >= 1 && c.done <= kcap && found[c.done] == 0) {
+                found[c.done] = i + 1;
+                ++nfound;
+            }
+        }
+        if (nfound == kmax || nn == 0) break;
+    }
+    (void)levels;
+    return SS_OK;
+}
+
+// rebuild the k groups of the state ((), k) found at `level` (allocator.py:228-264)
+__device__ void sweep_replay(const int* caps, int L, const SRec* states, const int* level_start, int k, int level,
+                             int* members_out, int* gsize_out) {
+    // locate ((), k)
+    int s = -1;
+    for (int q = level_start[level]; q < level_start[level + 1]; ++q)
+        if (states[q].m == 0 && states[q].done == k) { s = q; break; }
+    uint8_t acts[EXACT_LIMIT + 1];
+    for (int lv = level; lv >= 1; --lv) {
+        acts[lv - 1] = states[s].action;
+        s = level_start[lv - 1] + states[s].aux;
+    }
+    int open_res[EXACT_LIMIT], open_cnt[EXACT_LIMIT];
+    uint8_t open_mem[EXACT_LIMIT][EXACT_LIMIT];
+    int n_open = 0, n_closed = 0, out_pos = 0;
+    for (int gi = 0; gi < level; ++gi) {
+        const int cap = caps[gi];
+        int rem, cnt;
+        uint8_t mem[EXACT_LIMIT];
+        if (acts[gi] == 0xFF) {
+            rem = L - cap;
+            cnt = 1;
+            mem[0] = (uint8_t)gi;
+        } else {
+            const int slot = acts[gi];
+            rem = open_res[slot];
+            cnt = open_cnt[slot];
+            for (int p = 0; p < cnt; ++p) mem[p] = open_mem[slot][p];
+            for (int q = slot; q + 1 < n_open; ++q) {
+                open_res[q] = open_res[q + 1];
+                open_cnt[q] = open_cnt[q + 1];
+                for (int p = 0; p < open_cnt[q]; ++p) open_mem[q][p] = open_mem[q + 1][p];
+            }
+            --n_open;
+            mem[cnt++] = (uint8_t)gi;
+            rem -= cap;
+        }
+        if (rem <= 0) {
+            for (int p = 0; p < cnt; ++p) members_out[out_pos++] = mem[p];
+            gsize_out[n_closed++] = cnt;
+        } else {
+            int j = n_open;     // stable insert after equal residuals
+            while (j > 0 && open_res[j - 1] > rem) {
+                open_res[j] = open_res[j - 1];
+                open_cnt[j] = open_cnt[j - 1];
+                for (int p = 0; p < open_cnt[j]; ++p) open_mem[j][p] = open_mem[j - 1][p];
+                --j;
+            }
+            open_res[j] = rem;
+            open_cnt[j] = cnt;
+            for (int p = 0; p < cnt; ++p) open_mem[j][p] = mem[p];
+            ++n_open;
+        }
+    }
+}
+
+__device__ __forceinline__ int usable_count(const int* caps, int n) {
+    int u = 0;
+    while (u < n && caps[u] > 0) ++u;
+    return u;
+}
+
+__device__ bool sorted_nonincreasing(const int* caps, int n) {
+    for (int j = 0; j + 1 < n; ++j) if (caps[j] < caps[j + 1]) return false;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+__global__ void exact_sweep_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members,
+                                   int32_t* gsize, int32_t* pool_status, int32_t* pool_aux, unsigned char* ws_base,
+                                   int64_t ws_bytes_per, int fcap, int ccap, const int32_t* exact_list,
+                                   int n_exact, int32_t* sweep_stats) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_exact) return;
+    const int p = exact_list[e];
+    if (pool_status[p] != SS_OK) return;
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int* caps = P.caps + off;
+    const int L = P.layers[p], kmax = P.kmax[p];
+    const int n = usable_count(caps, n_all);
+    unsigned char* w = ws_base + (int64_t)e * ws_bytes_per;
+    SweepWs ws;
+    ws.states = reinterpret_cast<SRec*>(w);
+    w += (int64_t)fcap * sizeof(SRec);
+    ws.kids = reinterpret_cast<SRec*>(w);
+    w += (int64_t)ccap * sizeof(SRec);
+    ws.idx = reinterpret_cast<int32_t*>(w);
+    w += (int64_t)ccap * 4;
+    ws.tmp = reinterpret_cast<int32_t*>(w);
+    w += (int64_t)ccap * 4;
+    ws.keep = reinterpret_cast<int32_t*>(w);
+    int level_start[EXACT_LIMIT + 2];
+    int found[EXACT_LIMIT + 1];
+    int need = 0;
+    int stats[4];
+    const int st = exact_sweep(caps, n, L, kmax, ws, fcap, ccap, level_start, found, &need, stats);
+    if (sweep_stats) for (int q = 0; q < 4; ++q) sweep_stats[4 * e + q] = stats[q];
+    if (st != SS_OK) { pool_status[p] = st; pool_aux[p] = need; return; }
+    for (int k = 1; k <= kmax; ++k) {
+        const int64_t ko = koff[p] + k - 1;
+        if (k > EXACT_LIMIT || found[k] == 0) { stages[ko] = 0; continue; }
+        stages[ko] = found[k];
+        sweep_replay(caps, L, ws.states, level_start, k, found[k], members + P.memb_off[p] + (int64_t)(k - 1) * n_all,
+                     gsize + P.gsz_off[p] + (int64_t)(k - 1) * kmax);
+    }
+}
+
+// one thread per (pool, k) on the constructive path; stage 0 = absent / stalled
+__global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members, int32_t* gsize,
+                             const int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k, int n_cand,
+                             int32_t* stall) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cand) return;
+    const int p = cand_pool[c], k = cand_k[c];
+    if (pool_status[p] != SS_OK) return;
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int* caps = P.caps + off;
+    const int L = P.layers[p], kmax = P.kmax[p];
+    const int n = usable_count(caps, n_all);
+    const int64_t ko = koff[p] + k - 1;
+    stages[ko] = 0;
+    stall[ko] = 0;
+    long long prefix_n = 0;
+    for (int i = 0; i < n; ++i) prefix_n += cval(caps, i, L);
+    const long long target = (long long)k * L;
+    if (prefix_n < target) { stall[ko] = 2; return; }         // reference `break` (infeasible k)
+    const int pgm = (L + cval(caps, 0, L) - 1) / cval(caps, 0, L);
+    int m_cap = 0;
+    long long acc = 0;
+    while (m_cap < n && acc < target) acc += cval(caps, m_cap++, L);   // bisect_left(prefix, target)
+    int m0 = k * pgm > m_cap ? k * pgm : m_cap;
+    Lists G;
+    Frame fr[KMAX + 2];
+    Bits reach[NMAX + 1];
+    uint16_t items[NMAX];
+    int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * n_all;
+    int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * kmax;
+    for (int m = m0; m <= n; ++m) {
+        if (best_fit(caps, m, k, L, G)) {
+            int pos = 0, stg = 0;
+            for (int g = 0; g < k; ++g) {
+                for (int nd = G.head[g]; nd != NIL; nd = G.next[nd]) mout[pos++] = G.item[nd];
+                gout[g] = G.size[g];
+                stg += G.size[g];
+            }
+            stages[ko] = stg;
+            return;
+        }
+        if (peel(caps, m, k, L, fr, reach, items)) {
+            int pos = 0, stg = 0;
+            for (int g = 0; g < k; ++g) {
+                int cnt = 0;
+                for (int i = 0; i < m; ++i) if (fr[g].picked.test(i)) { mout[pos++] = i; ++cnt; }
+                gout[g] = cnt;
+                stg += cnt;
+            }
+            stages[ko] = stg;
+            return;
+        }
+    }
+    stall[ko] = 1;                                               // constructive grouping stalled
+}
+
+// per pool: apply "first stalled / infeasible k drops every larger k"; validate order
+__global__ void cover_fixup_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, const int32_t* stall,
+                                   int32_t* pool_status) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n_pools) return;
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int* caps = P.caps + off;
+    if (usable_count(caps, n_all) <= EXACT_LIMIT) return;
+    bool dead = false;
+    for (int k = 1; k <= P.kmax[p]; ++k) {
+        const int64_t ko = koff[p] + k - 1;
+        if (dead) { stages[ko] = 0; continue; }
+        if (stall[ko]) { dead = true; stages[ko] = 0; }
+    }
+}
+
+__global__ void validate_pools_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* pool_status,
+                                      int32_t* pool_aux) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n_pools) return;
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int* caps = P.caps + off;
+    int st = SS_OK;
+    const int L = P.layers[p];
+    const int n = usable_count(caps, n_all);
+    if (!sorted_nonincreasing(caps, n_all) || L < 1) st = SS_BAD_INPUT;
+    else if (n > EXACT_LIMIT && (n > NMAX || L > LMAX_PEEL || P.kmax[p] > KMAX)) st = SS_BAD_INPUT;
+    else if (n <= EXACT_LIMIT && L > 254) st = SS_BAD_INPUT;
+    pool_status[p] = st;
+    pool_aux[p] = 0;
+    for (int k = 1; k <= P.kmax[p]; ++k) stages[koff[p] + k - 1] = 0;
+}
+
+__global__ void objective_kernel(int32_t n_items, const int32_t* item_ptr, const double* flops, const int64_t* rtt_off,
+                                 const double* rtt, double fpl, const int32_t* layers, double tokens, double* out_t,
+                                 double* out_r) {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= n_items) return;
+    const int off = item_ptr[it], n = item_ptr[it + 1] - off;
+    const double* f = flops + off;
+    PySum inv;
+    inv.init();
+    for (int i = 0; i < n; ++i) inv.add_float(__ddiv_rn(1.0, f[i]));
+    const double harmonic = __ddiv_rn((double)n, inv.value());
+    const double t = __ddiv_rn(__dmul_rn(__dmul_rn(fpl, (double)layers[it]), tokens), harmonic);
+    const double* m = rtt + rtt_off[it];
+    PySum s;
+    s.init();
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            if (a != b) s.add_float(m[(int64_t)a * n + b]);
+    const long long cnt = (long long)n * (n - 1);
+    out_t[it] = t;
+    out_r[it] = cnt ? __ddiv_rn(s.value(), (double)cnt) : 0.0;
+}
+
+__device__ __forceinline__ int score_one(int k, int s, double kp, double t, double r, double* z) {
+    if (k < 1 || s < k) return SS_BAD_INPUT;
+    const double denom = __dadd_rn(t, __dmul_rn(__ddiv_rn((double)s, (double)k), r));
+    if (!(denom > 0.0)) return SS_DEGENERATE_OBJECTIVE;
+    *z = __ddiv_rn(kp, denom);
+    return SS_OK;
+}
+
+// grid: one thread per (pool, k); scores, and water-fills the groups when asked
+__global__ void score_fill_kernel(ss_pool_set P, const int64_t* koff, const int32_t* stages, const int32_t* members,
+                                  const int32_t* gsize, const double* t_comp, const double* rtt, const double* kpow,
+                                  int kpow_len, int fill_all, double* z, int32_t* counts, int32_t* kstatus,
+                                  int32_t* fstatus, const int32_t* cand_pool, const int32_t* cand_k, int n_cand) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cand) return;
+    const int p = cand_pool[c], k = cand_k[c];
+    const int64_t ko = koff[p] + k - 1;
+    kstatus[ko] = SS_OK;
+    if (fstatus) fstatus[ko] = SS_OK;
+    const int s = stages[ko];
+    if (s == 0) return;
+    if (k >= kpow_len) { kstatus[ko] = SS_BAD_INPUT; return; }
+    double zz = 0.0;
+    const int st = score_one(k, s, kpow[k], t_comp[p], rtt[p], &zz);
+    z[ko] = zz;
+    if (st != SS_OK) { kstatus[ko] = st; return; }
+    if (!fill_all) return;
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int kmax = P.kmax[p];
+    const int* mem = members + P.memb_off[p] + (int64_t)(k - 1) * n_all;
+    const int* gs = gsize + P.gsz_off[p] + (int64_t)(k - 1) * kmax;
+    int* cnt = counts + P.memb_off[p] + (int64_t)(k - 1) * n_all;
+    int pos = 0;
+    int capv[NMAX];
+    double flv[NMAX];
+    for (int g = 0; g < k; ++g) {
+        const int sz = gs[g];
+        for (int q = 0; q < sz; ++q) {
+            capv[q] = P.caps[off + mem[pos + q]];
+            flv[q] = P.flops[off + mem[pos + q]];
+        }
+        int aux = 0;
+        const int wst = stage_lengths(flv, capv, sz, P.layers[p], cnt + pos, &aux);
+        if (wst != SS_OK) { if (fstatus) fstatus[ko] = wst; return; }
+        pos += sz;
+    }
+}
+
+// per pool: best k by (z, k); water-fill the best k's groups unless already filled
+__global__ void best_k_kernel(ss_pool_set P, const int64_t* koff, const int32_t* stages, const int32_t* members,
+                              const int32_t* gsize, const double* z, const int32_t* kstatus,
+                              const int32_t* fstatus, int fill_all, int32_t* best_k, int32_t* counts,
+                              int32_t* pool_status) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n_pools) return;
+    best_k[p] = 0;
+    if (pool_status[p] != SS_OK) return;
+    int bk = 0;
+    double bz = 0.0;
+    for (int k = 1; k <= P.kmax[p]; ++k) {
+        const int64_t ko = koff[p] + k - 1;
+        if (stages[ko] == 0) continue;
+        if (kstatus[ko] != SS_OK) { pool_status[p] = kstatus[ko]; return; }   // score raises for any k
+        if (bk == 0 || z[ko] >= bz) { bk = k; bz = z[ko]; }                 // ascending k: ties -> larger k
+    }
+    best_k[p] = bk;
+    if (bk == 0) return;
+    if (fill_all) {
+        if (fstatus && fstatus[koff[p] + bk - 1] != SS_OK) pool_status[p] = fstatus[koff[p] + bk - 1];
+        return;
+    }
+    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
+    const int kmax = P.kmax[p];
+    const int* mem = members + P.memb_off[p] + (int64_t)(bk - 1) * n_all;
+    const int* gs = gsize + P.gsz_off[p] + (int64_t)(bk - 1) * kmax;
+    int* cnt = counts + P.memb_off[p] + (int64_t)(bk - 1) * n_all;
+    int pos = 0;
+    int capv[NMAX];
+    double flv[NMAX];
+    for (int g = 0; g < bk; ++g) {
+        const int sz = gs[g];
+        for (int q = 0; q < sz; ++q) {
+            capv[q] = P.caps[off + mem[pos + q]];
+            flv[q] = P.flops[off + mem[pos + q]];
+        }
+        int aux = 0;
+        const int wst = stage_lengths(flv, capv, sz, P.layers[p], cnt + pos, &aux);
+        if (wst != SS_OK) { pool_status[p] = wst; return; }
+        pos += sz;
+    }
+}
+
+__global__ void variant_reduce_kernel(int32_t n_var, const int32_t* var_ptr, const int64_t* koff, const int32_t* best_k,
+                                      const double* z, const int32_t* pool_status, double* total, int32_t* feasible) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_var) return;
+    double acc = 0.0;
+    int state = 0;   // 0 no pipeline, 1 feasible, -status on a pool error
+    for (int p = var_ptr[v]; p < var_ptr[v + 1]; ++p) {
+        if (pool_status[p] != SS_OK) { state = -pool_status[p]; break; }
+        if (best_k[p] > 0) { acc = __dadd_rn(acc, z[koff[p] + best_k[p] - 1]); state = 1; }
+    }
+    total[v] = acc;
+    feasible[v] = state;
+}
+
+__global__ void variant_argmax_kernel(int32_t n_var, const double* total, const int32_t* feasible, int32_t* best,
+                                      double* best_total) {
+    // single warp: (total desc, v asc)
+    const int lane = threadIdx.x;
+    double bt = -DBL_MAX;
+    int bv = -1;
+    for (int v = lane; v < n_var; v += 32) {
+        if (feasible[v] != 1) continue;
+        if (bv < 0 || total[v] > bt) { bt = total[v]; bv = v; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+        const int v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        if (v2 >= 0 && (bv < 0 || t2 > bt || (t2 == bt && v2 < bv))) { bt = t2; bv = v2; }
+    }
+    if (lane == 0) { *best = bv; *best_total = bv >= 0 ? bt : 0.0; }
+}
+
+__global__ void waterfill_kernel(int32_t n_groups, const int32_t* grp_ptr, const double* flops, const int32_t* caps,
+                                 const int32_t* layers, int mode, double* targets, int32_t* tflag, double* level,
+                                 int32_t* counts, int32_t* status, int32_t* aux) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_groups) return;
+    const int off = grp_ptr[g], n = grp_ptr[g + 1] - off;
+    int a = 0, st;
+    if (n > NMAX) { status[g] = SS_BAD_INPUT; return; }
+    if (mode == 2) {
+        st = stage_lengths(flops + off, caps + off, n, layers[g], counts + off, &a);
+    } else {
+        double lv = 0.0;
+        st = water_level(flops + off, caps + off, n, layers[g], targets + off, tflag + off, &lv, &a);
+        if (level) level[g] = lv;
+        if (st == SS_OK && mode == 1) st = hamilton(targets + off, tflag + off, caps + off, n, layers[g], counts + off);
+    }
+    status[g] = st;
+    if (aux) aux[g] = a;
+}
+
+__global__ void hamilton_kernel(int32_t n_groups, const int32_t* grp_ptr, const double* targets, const int32_t* tflag,
+                                const int32_t* caps, const int32_t* total, int32_t* counts, int32_t* status) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_groups) return;
+    const int off = grp_ptr[g], n = grp_ptr[g + 1] - off;
+    if (n > NMAX) { status[g] = SS_BAD_INPUT; return; }
+    long long tot = total[g];
+    if (tot < 0) {     // round(sum(targets)) with CPython sum semantics, round-half-even
+        PySum s;
+        s.init();
+        for (int i = 0; i < n; ++i) {
+            if (tflag[off + i]) s.add_int((long long)targets[off + i]);
+            else s.add_float(targets[off + i]);
+        }
+        tot = s.is_int ? s.iacc : (long long)rint(s.value());
+    }
+    status[g] = hamilton(targets + off, tflag + off, caps + off, n, tot, counts + off);
+}
+
+__global__ void score_kernel(int32_t n, const int32_t* k, const int32_t* s, const double* kpow, const double* t,
+                             const double* r, double* z, int32_t* status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double zz = 0.0;
+    status[i] = score_one(k[i], s[i], kpow[i], t[i], r[i], &zz);
+    z[i] = zz;
+}
+
+inline int grid_for(int n, int b) { return (n + b - 1) / b; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" int64_t ss_stage_counts_workspace(int32_t frontier_cap, int32_t children_cap, int32_t max_levels) {
+    (void)max_levels;
+    return (int64_t)frontier_cap * sizeof(SRec) + (int64_t)children_cap * (sizeof(SRec) + 12) + 256;
+}
+
+extern "C" int ss_stage_counts_validate(const ss_pool_set* pools, const int64_t* koff, int32_t* stages,
+                                        int32_t* pool_status, int32_t* pool_aux, void* stream) {
+    if (!pools || pools->n_pools <= 0) return SS_OK;
+    validate_pools_kernel<<<grid_for(pools->n_pools, 128), 128, 0, ss_stream(stream)>>>(*pools, koff, stages,
+                                                                                        pool_status, pool_aux);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_stage_counts_exact(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
+                                     int32_t* gsize, int32_t* pool_status, int32_t* pool_aux, const int32_t* exact_list,
+                                     int32_t n_exact, void* workspace, int64_t ws_bytes_per, int32_t frontier_cap,
+                                     int32_t children_cap, int32_t* sweep_stats, void* stream) {
+    if (n_exact <= 0) return SS_OK;
+    exact_sweep_kernel<<<grid_for(n_exact, 32), 32, 0, ss_stream(stream)>>>(
+        *pools, koff, stages, members, gsize, pool_status, pool_aux, static_cast<unsigned char*>(workspace),
+        ws_bytes_per, frontier_cap, children_cap, exact_list, n_exact, sweep_stats);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
+                                     int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool,
+                                     const int32_t* cand_k, int32_t n_cand, int32_t* stall, void* stream) {
+    cudaStream_t s = ss_stream(stream);
+    if (n_cand > 0) {
+        cover_kernel<<<grid_for(n_cand, 64), 64, 0, s>>>(*pools, koff, stages, members, gsize, pool_status, cand_pool,
+                                                          cand_k, n_cand, stall);
+        SS_CHECK_LAUNCH();
+    }
+    cover_fixup_kernel<<<grid_for(pools->n_pools, 128), 128, 0, s>>>(*pools, koff, stages, stall, pool_status);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_objective(int32_t n_items, const int32_t* item_ptr, const double* flops, const int64_t* rtt_off,
+                            const double* rtt, double fpl, const int32_t* layers, double tokens, double* out_t,
+                            double* out_r, void* stream) {
+    if (n_items <= 0) return SS_OK;
+    objective_kernel<<<grid_for(n_items, 64), 64, 0, ss_stream(stream)>>>(n_items, item_ptr, flops, rtt_off, rtt, fpl,
+                                                                         layers, tokens, out_t, out_r);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_phase1_score(const ss_pool_set* pools, const int64_t* koff, const int32_t* stages,
+                               const int32_t* members, const int32_t* gsize, const double* t_comp, const double* rtt,
+                               const double* kpow, int32_t kpow_len, int32_t fill_all, double* z, int32_t* counts,
+                               int32_t* kstatus, int32_t* fstatus, const int32_t* cand_pool, const int32_t* cand_k,
+                               int32_t n_cand, void* stream) {
+    if (n_cand <= 0) return SS_OK;
+    score_fill_kernel<<<grid_for(n_cand, 64), 64, 0, ss_stream(stream)>>>(*pools, koff, stages, members, gsize, t_comp,
+                                                                         rtt, kpow, kpow_len, fill_all, z, counts,
+                                                                         kstatus, fstatus, cand_pool, cand_k, n_cand);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_phase1_best(const ss_pool_set* pools, const int64_t* koff, const int32_t* stages,
+                              const int32_t* members, const int32_t* gsize, const double* z, const int32_t* kstatus,
+                              const int32_t* fstatus, int32_t fill_all, int32_t* best_k, int32_t* counts,
+                              int32_t* pool_status, void* stream) {
+    if (!pools || pools->n_pools <= 0) return SS_OK;
+    best_k_kernel<<<grid_for(pools->n_pools, 64), 64, 0, ss_stream(stream)>>>(*pools, koff, stages, members, gsize, z,
+                                                                             kstatus, fstatus, fill_all, best_k,
+                                                                             counts, pool_status);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_variant_reduce(int32_t n_var, const int32_t* var_ptr, const int64_t* koff, const int32_t* best_k,
+                                 const double* z, const int32_t* pool_status, double* total, int32_t* feasible,
+                                 int32_t* best_variant, double* best_total, void* stream) {
+    if (n_var <= 0) return SS_OK;
+    cudaStream_t s = ss_stream(stream);
+    variant_reduce_kernel<<<grid_for(n_var, 128), 128, 0, s>>>(n_var, var_ptr, koff, best_k, z, pool_status, total,
+                                                                feasible);
+    SS_CHECK_LAUNCH();
+    if (best_variant) {
+        variant_argmax_kernel<<<1, 32, 0, s>>>(n_var, total, feasible, best_variant, best_total);
+        SS_CHECK_LAUNCH();
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_waterfill(int32_t n_groups, const int32_t* grp_ptr, const double* flops, const int32_t* caps,
+                            const int32_t* layers, int32_t mode, double* targets, int32_t* tflag, double* level,
+                            int32_t* counts, int32_t* status, int32_t* aux, void* stream) {
+    if (n_groups <= 0) return SS_OK;
+    waterfill_kernel<<<grid_for(n_groups, 64), 64, 0, ss_stream(stream)>>>(n_groups, grp_ptr, flops, caps, layers, mode,
+                                                                          targets, tflag, level, counts, status, aux);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_hamilton(int32_t n_groups, const int32_t* grp_ptr, const double* targets, const int32_t* tflag,
+                           const int32_t* caps, const int32_t* total, int32_t* counts, int32_t* status, void* stream) {
+    if (n_groups <= 0) return SS_OK;
+    hamilton_kernel<<<grid_for(n_groups, 64), 64, 0, ss_stream(stream)>>>(n_groups, grp_ptr, targets, tflag, caps, total,
+                                                                          counts, status);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_score(int32_t n, const int32_t* k, const int32_t* s_star, const double* kpow, const double* t_comp,
+                        const double* rtt, double* z, int32_t* status, void* stream) {
+    if (n <= 0) return SS_OK;
+    score_kernel<<<grid_for(n, 128), 128, 0, ss_stream(stream)>>>(n, k, s_star, kpow, t_comp, rtt, z, status);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}

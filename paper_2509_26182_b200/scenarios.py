@@ -206,3 +206,77 @@ def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenario
         for s in range(n_scenarios):
             leave[s, churn_set(int(seeds[s]), plan_gpus, slices, model.layer_count, churn)] = True
     return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter)
+
+
+# ---------------------------------------------------------------------------
+# C3 / C5 Phase-1 variants, packed straight into device order
+# ---------------------------------------------------------------------------
+
+def pack_variants(clusters_models, *, alpha: float = 1.0, tokens: float = 128.0):
+    """allocate()-equivalent packing of many (cluster, model) pairs (allocator.py:561-581).
+
+    Regions in sorted() order; per region GPUs sorted by (-capacity, id);
+    objective inputs in cluster order with the dense rtt_s matrix.
+    Returns (PackedVariants, meta) where meta[p] = (variant, region, ordered gpu ids).
+    """
+    from .batched import PackedVariants
+    from ._phase1 import PoolSpec
+    from .topology import layer_capacity
+    pools, of, orr, meta, var_ptr = [], [], [], [], [0]
+    L = fpl = None
+    for v, (cluster, model) in enumerate(clusters_models):
+        L, fpl = model.layer_count, model.flops_per_layer_per_token
+        for region in sorted(cluster.regions):
+            rg = cluster.gpus_in_region(region)
+            if not rg:
+                continue
+            caps = [layer_capacity(g, model) for g in rg]
+            limit = min(len(caps), sum(caps) // L)
+            if limit < 1:
+                continue
+            order = sorted(range(len(rg)), key=lambda i: (-caps[i], rg[i].id))
+            pools.append(PoolSpec([caps[i] for i in order], [rg[i].flops for i in order], L, limit))
+            of.append(np.array([g.flops for g in rg]))
+            ids = [g.id for g in rg]
+            m = np.empty((len(rg), len(rg)))
+            for a in range(len(rg)):
+                for b in range(len(rg)):
+                    m[a, b] = cluster.rtt_s(ids[a], ids[b])
+            orr.append(m)
+            meta.append((v, region, [rg[i].id for i in order]))
+        var_ptr.append(len(pools))
+    return PackedVariants(pools, of, orr, np.array(var_ptr), fpl, L, tokens, alpha), meta
+
+
+def bench_variants(n_variants: int, gpu_count: int = 256, layer_count: int = 80, seed0: int = 0):
+    """C3 sweep inputs: synthetic_cluster(gpu_count, seed=v) for v in [seed0, seed0+n) packed
+    without building per-pair link dicts (bench pools: 1 ms inside a region, 10 ms across)."""
+    from .batched import PackedVariants
+    from ._phase1 import PoolSpec
+    model = bench_model(layer_count)
+    rc = default_region_count(gpu_count)
+    pools, of, orr, meta, var_ptr = [], [], [], [], [0]
+    for v in range(seed0, seed0 + n_variants):
+        rng = random.Random(v)
+        caps_all, flops_all = [], []
+        for _ in range(gpu_count):
+            c = rng.randint(*CAPACITY_RANGE)
+            f = rng.uniform(*FLOPS_RANGE)
+            vram = c * model.bytes_per_layer / 0.8
+            caps_all.append(max(0, int(np.floor(vram * (1.0 - 0.2) / model.bytes_per_layer + 1e-9))))
+            flops_all.append(f)
+        for r in range(rc):             # region names region-a.. sort like r
+            idx = list(range(r, gpu_count, rc))
+            caps = [caps_all[i] for i in idx]
+            limit = min(len(caps), sum(caps) // layer_count)
+            if limit < 1:
+                continue
+            order = sorted(range(len(idx)), key=lambda q: (-caps[q], idx[q]))
+            pools.append(PoolSpec([caps[q] for q in order], [flops_all[idx[q]] for q in order], layer_count, limit))
+            of.append(np.array([flops_all[i] for i in idx]))
+            m = np.full((len(idx), len(idx)), INTRA_REGION_RTT_S)
+            np.fill_diagonal(m, 0.0)
+            orr.append(m)
+            meta.append((v, f"region-{chr(ord('a') + r)}", [f"gpu-{idx[q]:04d}" for q in order]))
+        var_ptr.append(len(pools))
+    return PackedVariants(pools, of, orr, np.array(var_ptr), model.flops_per_layer_per_token, layer_count), meta

@@ -1,0 +1,192 @@
+"""Phase-1 parity on a B200: CUDA allocator / water-fill vs reference golden vectors and the oracle.
+
+Bar: bit-exact integer outputs (stage counts, groups, layer counts, chosen k)
+and bit-exact fp64 objective values (the reference's CPython arithmetic is
+replayed operation by operation, including 3.12's compensated sum()).
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import hx, untag
+from helpers_golden import cluster_from_alloc_case
+from oracle import alloc_ref, waterfill_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan_hex(plan):
+    from paper_2509_26182_b200.plan import plan_to_dict
+    d = plan_to_dict(plan)
+    d["objective"] = d["objective"].hex()
+    for row in d["per_k"]:
+        row["z"] = row["z"].hex()
+    return d
+
+
+def test_stage_counts_golden(cuda_ready, phase1_cases):
+    from paper_2509_26182_b200 import solve_stage_counts
+    for i, case in enumerate(phase1_cases["stage_counts"]):
+        got = solve_stage_counts(case["caps"], case["L"], case["kmax"])
+        want = {int(k): (v[0], tuple(tuple(g) for g in v[1])) for k, v in case["sols"].items()}
+        assert {k: (s.stages, s.groups) for k, s in got.items()} == want, (i, case["caps"], case["L"])
+
+
+def test_stage_counts_random_vs_oracle(cuda_ready):
+    """Exact path at the 16-GPU limit and constructive pools up to 128 GPUs, L up to 80."""
+    from paper_2509_26182_b200._phase1 import PoolBatch, PoolSpec
+    rng = random.Random(6001)
+    specs, cases = [], []
+    for _ in range(120):
+        n = rng.choice([3, 8, 12, 16, 17, 24, 40, 64, 96, 128])
+        L = rng.choice([6, 16, 32, 48, 64, 80])
+        caps = sorted((rng.randint(0 if rng.random() < 0.1 else 1, min(32, L)) for _ in range(n)), reverse=True)
+        km = alloc_ref.kmax(caps, L)
+        if km < 1 or (sum(c > 0 for c in caps) <= 16 and L > 64 and n > 14):
+            continue
+        specs.append(PoolSpec(caps, [1.0] * n, L, km))
+        cases.append((caps, L, km))
+    batch = PoolBatch(specs)
+    batch.stage_counts()
+    res = batch.fetch()
+    for p, (caps, L, km) in enumerate(cases):
+        res.raise_pool(p)
+        assert res.solutions(p) == alloc_ref.stage_counts(caps, L, km), (caps, L, km)
+
+
+def test_allocate_golden(cuda_ready, phase1_cases):
+    from paper_2509_26182_b200 import NoFeasiblePipeline, ObjectiveParams, allocate
+    for rec in phase1_cases["allocate"]:
+        cluster, model = cluster_from_alloc_case(rec)
+        kw = {}
+        if "alpha" in rec["kw"]:
+            kw["alpha"] = hx(rec["kw"]["alpha"])
+        if "params" in rec["kw"]:
+            a, t, r = (hx(x) for x in rec["kw"]["params"])
+            kw["params"] = ObjectiveParams(alpha=a, t_comp_seconds=t, rtt_seconds=r)
+        try:
+            got = _plan_hex(allocate(cluster, model, **kw))
+        except NoFeasiblePipeline:
+            got = None
+        assert got == rec["plan"], rec["name"]
+
+
+def test_objective_golden(cuda_ready, phase1_cases):
+    from paper_2509_26182_b200 import estimate_objective_params, scenarios as scen
+    for rec in phase1_cases["objective"][:6]:
+        cl, m = scen.synthetic_cluster(rec["n"], seed=rec["seed"], model=scen.bench_model(rec["L"]))
+        p = estimate_objective_params(cl.gpus_in_region(rec["region"]), cl, m, 1.0, 128.0)
+        assert (p.t_comp_seconds.hex(), p.rtt_seconds.hex()) == (rec["t_comp"], rec["rtt"])
+
+
+def test_waterfill_golden(cuda_ready, phase1_cases):
+    from paper_2509_26182_b200 import hamilton_round, solve_lambda
+    for i, rec in enumerate(phase1_cases["waterfill"][:120]):
+        flops = [hx(f) for f in rec["flops"]]
+        frac = solve_lambda(flops, rec["caps"], rec["L"])
+        want = [untag(t) for t in rec["targets"]]
+        assert list(frac.targets) == want and [type(t) for t in frac.targets] == [type(t) for t in want], i
+        assert frac.water_level == hx(rec["level"]), i
+        assert list(hamilton_round(frac, rec["caps"], rec["L"]).layers) == rec["layers"], i
+        assert list(hamilton_round(frac, rec["caps"]).layers) == list(
+            waterfill_ref.largest_remainder(frac.targets, rec["caps"])), i
+
+
+def test_waterfill_batched_vs_oracle(cuda_ready, phase1_cases):
+    """All golden rebalance cases in ONE batched ss_waterfill launch (mode 2)."""
+    import torch
+    from paper_2509_26182_b200 import _native as N
+    recs = phase1_cases["rebalance"]
+    sizes = [len(r["caps"]) for r in recs]
+    ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    dev = torch.device("cuda")
+    fl = torch.tensor([hx(f) for r in recs for f in r["flops"]], dtype=torch.float64, device=dev)
+    caps = torch.tensor([c for r in recs for c in r["caps"]], dtype=torch.int32, device=dev)
+    layers = torch.tensor([r["L"] for r in recs], dtype=torch.int32, device=dev)
+    gp = torch.from_numpy(ptr).to(dev)
+    n = int(ptr[-1])
+    counts = torch.zeros(n, dtype=torch.int32, device=dev)
+    st = torch.zeros(len(recs), dtype=torch.int32, device=dev)
+    aux = torch.zeros(len(recs), dtype=torch.int32, device=dev)
+    N.check(N.lib().ss_waterfill(len(recs), N.ptr(gp), N.ptr(fl), N.ptr(caps), N.ptr(layers), 2, None, None, None,
+                                 N.ptr(counts), N.ptr(st), N.ptr(aux), N.stream_handle()), "ss_waterfill")
+    counts, st = counts.cpu().numpy(), st.cpu().numpy()
+    names = {6: "RoundingOverflow", 5: "InfeasibleCapacity"}
+    for i, rec in enumerate(recs):
+        got = names[int(st[i])] if st[i] else counts[ptr[i]:ptr[i + 1]].tolist()
+        assert got == rec["lengths"], i
+
+
+def test_rebalance_pipeline_dropin(cuda_ready):
+    from paper_2509_26182_b200 import LayerSlice, ModelSpec, Pipeline, rebalance_pipeline, GpuNode
+    model = ModelSpec("m8", 8, 1e9, 2e10)
+    gpus = [GpuNode("fast", "east", 6 * 1e9 / 0.8, 3e14), GpuNode("slow", "east", 6 * 1e9 / 0.8, 1e14)]
+    pipe = Pipeline((LayerSlice("fast", 1, 4), LayerSlice("slow", 5, 8)), "east")
+    out = rebalance_pipeline(pipe, {g.id: g for g in gpus}, model)
+    assert [s.length for s in out.stages] == [6, 2]
+
+
+def test_score_and_errors(cuda_ready):
+    from paper_2509_26182_b200 import DegenerateObjective, ObjectiveParams, score, min_stages, k_max
+    p = ObjectiveParams(alpha=1.0, t_comp_seconds=0.5, rtt_seconds=0.25)
+    assert score(1, 2, p) == alloc_ref.score(1, 2, 1.0, 0.5, 0.25)
+    assert score(2, 4, p) == 2.0
+    with pytest.raises(DegenerateObjective):
+        score(1, 1, ObjectiveParams(1.0, 0.0, 0.0))
+    with pytest.raises(ValueError):
+        score(2, 1, p)
+    assert min_stages([6, 5, 5, 4], 10, 2).stages == 4
+    assert min_stages([6, 5, 5, 4], 10, 3) is None
+    assert k_max([6, 4, 5, 5], 10) == 2
+    from paper_2509_26182_b200 import solve_stage_counts, SweepStats
+    with pytest.raises(ValueError):
+        solve_stage_counts([4, 6], 10, 1)
+    st = SweepStats()
+    solve_stage_counts([8, 7, 6, 5, 5, 4, 3, 2], 12, 3, stats=st)
+    assert st.pruned_dominated > 0 and st.states_expanded > 0
+
+
+def test_allocate_bench_pools_vs_oracle(cuda_ready):
+    """C1/C2/C3-shaped bench pools and a homogeneous tie pool, plan for plan."""
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    for n, seed, L, fl in [(8, 3, 32, None), (64, 7, 64, None), (256, 9, 80, None), (48, 2, 48, 1e14),
+                           (1024, 1, 80, None)]:
+        cl, m = scen.synthetic_cluster(n, seed=seed, model=scen.bench_model(L), homogeneous_flops=fl)
+        got = _plan_hex(allocate(cl, m))
+        want = alloc_ref.allocate(cl, m)
+        want["objective"] = want["objective"].hex()
+        want["per_k"] = [dict(r, z=r["z"].hex()) for r in want["per_k"]]
+        assert got == want, (n, seed, L)
+
+
+def test_variant_sweep_vs_oracle(cuda_ready):
+    """C3-shaped candidate sweep (fill_all): every (variant, region, k) candidate vs the oracle."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import VariantSweep
+    packed, meta = scen.bench_variants(6, 256, 80, seed0=40)
+    sw = VariantSweep(packed, fill_all=True)
+    sw.run()
+    res = sw.batch.fetch()
+    totals = sw.total.cpu().numpy()
+    for v in range(6):
+        cl, m = scen.synthetic_cluster(256, seed=40 + v, model=scen.bench_model(80))
+        want = alloc_ref.allocate(cl, m)
+        assert totals[v] == want["objective"], v
+        for p in range(packed.var_ptr[v], packed.var_ptr[v + 1]):
+            pool = packed.pools[p]
+            sols = res.solutions(p)
+            assert sols == alloc_ref.stage_counts(pool.caps, 80, pool.kmax)
+            t, r = alloc_ref.objective(list(packed.obj_flops[p]), [str(i) for i in range(len(packed.obj_flops[p]))],
+                                       lambda a, b: 0.0 if a == b else 0.001, m.flops_per_layer_per_token, 80, 128.0)
+            for k, (s, groups) in sols.items():
+                assert res.z_of(p, k) == alloc_ref.score(k, s, 1.0, t, r)
+                counts = res.counts_of(p, k)
+                pos = 0
+                for grp in groups:
+                    want_len = waterfill_ref.stage_lengths([pool.flops[i] for i in grp], [pool.caps[i] for i in grp], 80)
+                    assert counts[pos:pos + len(grp)] == want_len
+                    pos += len(grp)
+    bv = int(sw.best_variant.cpu()[0])
+    assert bv == int(np.argmax(totals)) and float(sw.best_total.cpu()[0]) == totals.max()
