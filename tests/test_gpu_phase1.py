@@ -178,7 +178,8 @@ def test_variant_sweep_vs_oracle(cuda_ready):
             pool = packed.pools[p]
             sols = res.solutions(p)
             assert sols == alloc_ref.stage_counts(pool.caps, 80, pool.kmax)
-            t, r = alloc_ref.objective(list(packed.obj_flops[p]), [str(i) for i in range(len(packed.obj_flops[p]))],
+            t, r = alloc_ref.objective([float(x) for x in packed.obj_flops[p]],  # exact floats: CPython sum compensates only PyFloat
+                                        [str(i) for i in range(len(packed.obj_flops[p]))],
                                        lambda a, b: 0.0 if a == b else 0.001, m.flops_per_layer_per_token, 80, 128.0)
             for k, (s, groups) in sols.items():
                 assert res.z_of(p, k) == alloc_ref.score(k, s, 1.0, t, r)
