@@ -1,0 +1,396 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 scheduling hot path (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+Workload (BASELINE.json metric "Phase-2 chain selections/sec and Phase-1
+allocations/sec at 1/2/4/8 B200"):
+
+* Phase-2 (``value``): C4 -- a 64-layer model over a 256-GPU heterogeneous
+  bench pool (seed 0, placed by this package's device ``allocate``: k = 73
+  replicas), S scenario states per GPU (5% churn + per-pair RTT jitter, seeds
+  sharded s = rank + world * i, weak scaling), each replaying route /
+  release(i - 64) with on-device occupancy feedback.  One step = R requests
+  on every scenario of the rank.  Inputs are resident in HBM (3+ GB of edge
+  blocks per GPU, far larger than the 126 MB L2).
+* Phase-1 (``phase1``): C3 -- allocate() candidates of 256-GPU / 80-layer
+  bench pools (variants v = rank + world * i), every (variant, region, k)
+  stage-count + score + water-fill, then the per-variant objective fold and a
+  global argmax over ranks (NCCL all-gather over NVLink when N > 1).
+* ``e2e``: the same Phase-2 metric through ``ScenarioReplayer.run_from_host``:
+  pinned host scenario descriptors -> H2D -> device DAG build -> replay ->
+  D2H of per-request costs and chain hashes, all inside the timed region.
+* ``cpu_baseline`` / ``--impl reference``: the reference's CPU path (the
+  oracle port, pinned bit-exact to the reference) on this box's host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Phase-2 chain selections/sec and Phase-1 allocations/sec at 1/2/4/8 B200"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenarios-per-gpu", type=int, default=1184)
+    ap.add_argument("--requests-per-step", type=int, default=32)
+    ap.add_argument("--window", type=int, default=64)
+    ap.add_argument("--variants-per-gpu", type=int, default=227)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-phase1", action="store_true")
+    ap.add_argument("--cpu-sample-scenarios", type=int, default=32)
+    ap.add_argument("--cpu-sample-requests", type=int, default=40)
+    ap.add_argument("--cpu-sample-pools", type=int, default=160)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def timed(fn, steps, warmup, stream, barrier, reduce_max):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    return reduce_max(e0.elapsed_time(e1) / 1e3)
+
+
+def base_pool(device_allocate=True):
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+    plan = allocate(cl, model)
+    return cl, model, plan
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def reduce_max(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer, VariantSweep
+    stream = torch.cuda.Stream()
+    S, R, W = args.scenarios_per_gpu, args.requests_per_step, args.window
+
+    # ---- Phase-2 setup (outside the timed region) ----------------------------
+    with torch.cuda.stream(stream):
+        cl, model, plan = base_pool()
+        ss = scen.build_scenarios(cl, model, plan, S, seed0=0, churn=0.05, jitter=True)
+        ss.seeds = (rank + world * np.arange(S)).astype(np.int64)
+        # churn sets follow the sharded seeds
+        ids = ss.ids
+        pos = {g: i for i, g in enumerate(ids)}
+        slices = {pos[g]: (s.start_layer, s.end_layer) for g, s in plan.gpu_slices().items()}
+        ss.leave[:] = False
+        for i, sd in enumerate(ss.seeds):
+            ss.leave[i, scen.churn_set(int(sd), sorted(slices), slices, model.layer_count, 0.05)] = True
+        rp = ScenarioReplayer(ss, window=W, stream=stream)
+        rp.build()
+        out = rp.run(R)
+        torch.cuda.synchronize()
+        rp.raise_first_failure()
+        first_cost = out.cost.cpu().numpy().copy()
+    b2 = rp.bytes_per_selection()
+    sel_per_step_rank = S * R
+    hbm, peak_src = peaks()
+
+    def p2_step():
+        rp.run(R, out=out)
+
+    clocks = ClockSampler(local)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            p2_step()
+        torch.cuda.synchronize()
+        barrier()
+        clocks.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            p2_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        barrier()
+    t_rank = e0.elapsed_time(e1) / 1e3
+    t_max = reduce_max(t_rank)
+    total_sel = sel_per_step_rank * world * args.steps
+    value = total_sel / t_max
+    launch_s = t_rank / args.steps                      # one ss_replay launch per step
+    achieved = float(b2.mean()) * sel_per_step_rank / launch_s / 1e9
+
+    # ---- e2e: host descriptors in, host results out ---------------------------
+    leave_h = torch.from_numpy(ss.leave.astype(np.uint8)).pin_memory()
+    seeds_h = torch.from_numpy(ss.seeds.copy()).pin_memory()
+    cost_h = torch.empty((S, R), dtype=torch.float64).pin_memory()
+    hash_h = torch.empty((S, R), dtype=torch.int64).pin_memory()
+    rp2 = ScenarioReplayer(ss, window=W, stream=stream)
+    with torch.cuda.stream(stream):
+        def e2e_step():
+            rp2.run_from_host(leave_h, seeds_h, R, cost_h, hash_h)
+        t_e2e = timed(e2e_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
+    e2e_steps = max(2, args.steps // 2)
+    torch.cuda.synchronize()
+    # the e2e path routes the same first R requests of fresh scenarios: identical results
+    e2e_ok = bool(np.array_equal(cost_h.numpy(), first_cost))
+    e2e_value = S * R * world * e2e_steps / t_e2e
+
+    # ---- Phase-1 (C3) ---------------------------------------------------------
+    p1 = None
+    if not args.no_phase1:
+        V = args.variants_per_gpu
+        packed, meta = _variants_for_rank(scen, V, rank, world)
+        with torch.cuda.stream(stream):
+            sw = VariantSweep(packed, fill_all=True, stream=stream)
+            sw.run()
+            torch.cuda.synchronize()
+            gather = torch.zeros(2 * world, dtype=torch.float64, device="cuda")
+
+            def p1_step():
+                sw.run()
+                if dist:
+                    # global argmax over ranks: (best objective, variant id) all-gathered over NVLink
+                    mine = torch.stack([sw.best_total[0], sw.best_variant[0].to(torch.float64)])
+                    dist.all_gather_into_tensor(gather, mine)
+            t_p1 = timed(p1_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
+        p1_steps = max(2, args.steps // 2)
+        n_cand = packed.n_candidates
+        res = sw.batch.fetch()
+        bad = int((res.status[:len(packed.pools)] != 0).sum())
+        p1 = {"metric": "Phase-1 candidate allocations/sec", "value": n_cand * world * p1_steps / t_p1,
+              "unit": "candidates/s", "ms_per_step": 1e3 * t_p1 / p1_steps,
+              "config": {"workload": "C3: allocate() candidates of synthetic_cluster(256, seed=v), L=80, "
+                                     "every (variant, region, k) stage-count + score + water-fill, objective "
+                                     "fold per variant, global argmax (NCCL all-gather when N>1)",
+                         "variants_per_gpu": V, "candidates_per_gpu": n_cand, "pools_with_errors": bad},
+              "roofline": {"bound": "issue (integer/bitset DP)", "note": "not HBM-bound; see DESIGN.md"}}
+
+    # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, ss, packed if p1 else None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "selections/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4: L=64 model over a 256-GPU heterogeneous pool (k=%d replicas), %d "
+                                   "churn+jitter scenario states per GPU x %d requests per step, W=%d "
+                                   "route/release window, on-device load update" % (plan.replication_count, S, R, W),
+                       "scenarios_per_gpu": S, "requests_per_step": R, "window": W, "layers": 64, "pool_gpus": 256,
+                       "replicas": plan.replication_count, "parallelism": f"scenario-sharded x{world}",
+                       "l2": "inputs larger than L2: %.2f GB of edge blocks per GPU vs 126 MB L2"
+                             % (rp.edge_val.numel() * 8 / 1e9),
+                       "bytes_per_selection_B2": float(b2.mean())},
+            "e2e": {"value": e2e_value, "unit": "selections/s",
+                    "h2d_bytes_per_step": int(leave_h.numel() + seeds_h.numel() * 8),
+                    "d2h_bytes_per_step": int(cost_h.numel() * 8 + hash_h.numel() * 8),
+                    "path": "ScenarioReplayer.run_from_host: H2D descriptors, device DAG build, replay, D2H results",
+                    "matches_device_run": e2e_ok},
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": _traffic(), "peak_source": peak_src,
+                         "kernel": "chain_dp_kernel<3,true> (ss_replay)",
+                         "algorithmic_bytes_per_launch": float(b2.mean()) * sel_per_step_rank},
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "phase1": p1,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _variants_for_rank(scen, V, rank, world):
+    from paper_2509_26182_b200.batched import PackedVariants
+    parts = [scen.bench_variants(1, 256, 80, seed0=rank + world * i) for i in range(V)]
+    pools, of, orr, meta, var_ptr = [], [], [], [], [0]
+    for pk, mt in parts:
+        pools += pk.pools
+        of += pk.obj_flops
+        orr += pk.obj_rtt
+        meta += mt
+        var_ptr.append(len(pools))
+    p0 = parts[0][0]
+    return PackedVariants(pools, of, orr, np.array(var_ptr), p0.fpl, p0.layers, p0.tokens, p0.alpha), meta
+
+
+def _traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("replay_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(args, ss, packed):
+    from oracle import bench_cpu
+    n_s = min(args.cpu_sample_scenarios, ss.n_scenarios)
+    rate, cores, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), args.cpu_sample_requests, args.window)
+    out = {"value": rate, "unit": "selections/s", "cores": cores, "kind": "port",
+           "sample": f"C4 shape: {n_s} scenarios x {args.cpu_sample_requests} requests (W={args.window}), "
+                     f"{sel} selections in {wall:.1f} s wall on {cores} processes"}
+    if packed is not None:
+        r1, c1, cand, w1 = bench_cpu.phase1_rate(packed, args.cpu_sample_pools)
+        out["phase1"] = {"value": r1, "unit": "candidates/s", "cores": c1,
+                         "sample": f"C3 shape: first {args.cpu_sample_pools} pools, {cand} candidates in {w1:.1f} s"}
+    return out
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import alloc_ref, bench_cpu
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.plan import AllocationPlan, Pipeline
+    from paper_2509_26182_b200.topology import LayerSlice
+    cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+    d = alloc_ref.allocate(cl, model)
+    pipes = tuple(Pipeline(tuple(LayerSlice(s["gpu_id"], s["start_layer"], s["end_layer"]) for s in p["stages"]),
+                           p["region"]) for p in d["pipelines"])
+    plan = AllocationPlan(d["k"], pipes, sum(p.stage_count for p in pipes), d["objective"], ())
+    n_s = args.cpu_sample_scenarios
+    ss = scen.build_scenarios(cl, model, plan, n_s, seed0=0, churn=0.05, jitter=True)
+    rates, walls = [], []
+    for _ in range(args.warmup):
+        bench_cpu.phase2_rate(ss, list(range(min(8, n_s))), 4, args.window)
+    for _ in range(args.steps):
+        rate, cores, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), args.cpu_sample_requests // 4 or 1,
+                                                       args.window)
+        rates.append(rate)
+        walls.append(wall)
+    value = float(np.median(rates))
+    line = {"metric": METRIC, "value": value, "unit": "selections/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(walls)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C4 shape (L=64, 256-GPU pool, churn+jitter scenarios, W=%d) -- reference CPU "
+                                   "path (oracle port of router.py/perfmap.py, bit-exact to the reference)"
+                                   % args.window, "parallelism": f"{cores} host processes"},
+            "cpu_baseline": {"value": value, "unit": "selections/s", "cores": cores, "kind": "port",
+                             "sample": f"{n_s} scenarios x {args.cpu_sample_requests // 4 or 1} requests per step"},
+            "e2e": {"value": value, "unit": "selections/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

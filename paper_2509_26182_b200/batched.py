@@ -154,6 +154,27 @@ class ScenarioReplayer:
                                   N.stream_handle(self.stream)), "ss_replay")
         return out
 
+    def run_from_host(self, leave_h, seeds_h, n_req: int, cost_h, hash_h) -> ReplayResult:
+        """End-to-end call: host scenario descriptors in, host per-request results out.
+
+        leave_h [S, N] uint8 and seeds_h [S] int64 (pinned) are copied to the
+        device, the scenario DAGs are rebuilt (ss_scenario_columns +
+        ss_dag_edges), replay state is reset, n_req requests are routed per
+        scenario and the costs / chain hashes come back into pinned cost_h /
+        hash_h.  Stream-ordered; the caller synchronises.
+        """
+        self.leave.copy_(leave_h, non_blocking=True)
+        self.seeds.copy_(seeds_h, non_blocking=True)
+        self.occ.zero_()
+        self.ring.zero_()
+        self.next_req.zero_()
+        self.status.zero_()
+        self.build()
+        out = self.run(n_req)
+        cost_h.copy_(out.cost, non_blocking=True)
+        hash_h.copy_(out.chain_hash, non_blocking=True)
+        return out
+
     def raise_first_failure(self) -> None:
         st = self.status.cpu().numpy()
         bad = np.nonzero(st)[0]
