@@ -182,15 +182,8 @@ def run_ours(args):
     # ---- Phase-2 setup (outside the timed region) ----------------------------
     with torch.cuda.stream(stream):
         cl, model, plan = base_pool()
-        ss = scen.build_scenarios(cl, model, plan, S, seed0=0, churn=0.05, jitter=True)
-        ss.seeds = (rank + world * np.arange(S)).astype(np.int64)
-        # churn sets follow the sharded seeds
-        ids = ss.ids
-        pos = {g: i for i, g in enumerate(ids)}
-        slices = {pos[g]: (s.start_layer, s.end_layer) for g, s in plan.gpu_slices().items()}
-        ss.leave[:] = False
-        for i, sd in enumerate(ss.seeds):
-            ss.leave[i, scen.churn_set(int(sd), sorted(slices), slices, model.layer_count, 0.05)] = True
+        ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True,
+                                  seeds=rank + world * np.arange(S))     # scenario s -> rank s mod world
         rp = ScenarioReplayer(ss, window=W, stream=stream)
         rp.build()
         out = rp.run(R)

@@ -184,7 +184,7 @@ def base_rtt_matrix(cluster: ClusterSnapshot, ids: Sequence[str]) -> np.ndarray:
 
 
 def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenarios: int, *,
-                    seed0: int = 0, churn: float = 0.05, jitter: bool = True) -> ScenarioSet:
+                    seed0: int = 0, churn: float = 0.05, jitter: bool = True, seeds=None) -> ScenarioSet:
     """C4-style scenario batch over a placed pool."""
     ids = sorted(g.id for g in cluster.gpus)
     pos = {g: i for i, g in enumerate(ids)}
@@ -199,7 +199,8 @@ def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenario
         hi[pos[gid]] = sl.end_layer
         slices[pos[gid]] = (sl.start_layer, sl.end_layer)
     rtt = base_rtt_matrix(cluster, ids)
-    seeds = np.arange(seed0, seed0 + n_scenarios, dtype=np.int64)
+    seeds = (np.arange(seed0, seed0 + n_scenarios, dtype=np.int64) if seeds is None
+             else np.asarray(seeds, dtype=np.int64))
     leave = np.zeros((n_scenarios, n), dtype=bool)
     plan_gpus = sorted(slices)
     if churn > 0:
