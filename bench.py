@@ -48,18 +48,18 @@ HBM_FALLBACK_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scenarios-per-gpu", type=int, default=1184)
-    ap.add_argument("--requests-per-step", type=int, default=32)
+    ap.add_argument("--requests-per-step", type=int, default=64)
     ap.add_argument("--window", type=int, default=64)
     ap.add_argument("--variants-per-gpu", type=int, default=227)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase1", action="store_true")
-    ap.add_argument("--cpu-sample-scenarios", type=int, default=32)
-    ap.add_argument("--cpu-sample-requests", type=int, default=40)
-    ap.add_argument("--cpu-sample-pools", type=int, default=160)
+    ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
+    ap.add_argument("--cpu-sample-requests", type=int, default=64)
+    ap.add_argument("--cpu-sample-pools", type=int, default=400)
     return ap.parse_args()
 
 
@@ -176,6 +176,7 @@ def run_ours(args):
 
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer, VariantSweep
+    from paper_2509_26182_b200.distributed import global_argmax, shard
     stream = torch.cuda.Stream()
     S, R, W = args.scenarios_per_gpu, args.requests_per_step, args.window
 
@@ -183,7 +184,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         cl, model, plan = base_pool()
         ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True,
-                                  seeds=rank + world * np.arange(S))     # scenario s -> rank s mod world
+                                  seeds=shard(S, rank, world))           # scenario s -> rank s mod world
         rp = ScenarioReplayer(ss, window=W, stream=stream)
         rp.build()
         out = rp.run(R)
@@ -245,14 +246,13 @@ def run_ours(args):
             sw = VariantSweep(packed, fill_all=True, stream=stream)
             sw.run()
             torch.cuda.synchronize()
-            gather = torch.zeros(2 * world, dtype=torch.float64, device="cuda")
+            var_ids = torch.from_numpy(shard(V, rank, world)).to("cuda")
 
             def p1_step():
                 sw.run()
                 if dist:
                     # global argmax over ranks: (best objective, variant id) all-gathered over NVLink
-                    mine = torch.stack([sw.best_total[0], sw.best_variant[0].to(torch.float64)])
-                    dist.all_gather_into_tensor(gather, mine)
+                    global_argmax(sw.best_total[0], var_ids[sw.best_variant[0].clamp(min=0).long()])
             t_p1 = timed(p1_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
         p1_steps = max(2, args.steps // 2)
         n_cand = packed.n_candidates
@@ -306,7 +306,8 @@ def run_ours(args):
 
 def _variants_for_rank(scen, V, rank, world):
     from paper_2509_26182_b200.batched import PackedVariants
-    parts = [scen.bench_variants(1, 256, 80, seed0=rank + world * i) for i in range(V)]
+    from paper_2509_26182_b200.distributed import shard
+    parts = [scen.bench_variants(1, 256, 80, seed0=int(v)) for v in shard(V, rank, world)]
     pools, of, orr, meta, var_ptr = [], [], [], [], [0]
     for pk, mt in parts:
         pools += pk.pools
