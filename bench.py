@@ -291,7 +291,7 @@ def run_ours(args):
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": _traffic(), "peak_source": peak_src,
+                         "traffic": _traffic(sel_per_step_rank), "peak_source": peak_src,
                          "kernel": "chain_dp_kernel<3,true> (ss_replay)",
                          "algorithmic_bytes_per_launch": float(b2.mean()) * sel_per_step_rank},
             "clocks": clk,
@@ -319,11 +319,12 @@ def _variants_for_rank(scen, V, rank, world):
     return PackedVariants(pools, of, orr, np.array(var_ptr), p0.fpl, p0.layers, p0.tokens, p0.alpha), meta
 
 
-def _traffic():
+def _traffic(selections_per_launch):
+    """DRAM bytes per launch from the committed ncu capture (per selection x selections per launch)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get("replay_dram_bytes_per_launch")
+            return json.load(fh)["replay_dram_bytes_per_selection"] * selections_per_launch
     except Exception:
         return None
 

@@ -1,0 +1,24 @@
+#!/usr/bin/env python3
+"""Summarise an ncu report (raw page) into the metrics the bench/DESIGN cite.  Usage: summarize_ncu.py rep out.txt"""
+import csv, io, subprocess, sys
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_shared_mem", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
+        "launch__block_size", "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second"]
+rep, out = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+with open(out, "w") as fh:
+    for r in rows[2:]:
+        fh.write(f"kernel: {r[hdr.index('Kernel Name')]}\n")
+        for w in WANT:
+            if w in hdr:
+                i = hdr.index(w)
+                fh.write(f"  {w:62s} {r[i]:>18s} {units[i]}\n")
+print(open(out).read())
