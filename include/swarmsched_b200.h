@@ -220,6 +220,31 @@ int ss_hamilton(int32_t n_groups, const int32_t* grp_ptr, const double* targets,
 int ss_score(int32_t n, const int32_t* k, const int32_t* s_star, const double* kpow, const double* t_comp,
              const double* rtt, double* z, int32_t* status, void* stream);
 
+/* Slot-tile replay for interval-slice scenario sets (every GPU hosts one
+ * contiguous layer slice: allocate() plans and their churned states).  Each
+ * GPU gets one shared-memory slot for its whole frontier interval
+ * [max(lo-2,0), hi-1] (interval partitioning); the CTA keeps T[slot][slot] =
+ * rtt and streams only the rows/columns of GPUs entering the frontier.  The DP
+ * reads the same fp64 values as ss_replay -> bit-identical results with ~10x
+ * fewer HBM bytes per selection.
+ *   ss_slot_program: builds meta (meta_stride bytes per scenario, >=
+ *     ss_slot_meta_bytes) and row/column units (stream_stride doubles per
+ *     scenario, even) from slices + leave masks + the pool rtt matrix (x the
+ *     scenarios.py jitter when jitter_seed != NULL); s_used[s] = slots needed
+ *     (<= s_cap, a multiple of 32 <= 256), status[s] = SS_BAD_INPUT if not.
+ *   ss_replay_slots: same state / outputs / op script as ss_replay; dags
+ *     must be the matching ss_scenario_columns set; s_rows >= max s_used. */
+int64_t ss_slot_meta_bytes(int32_t layers, int32_t n_gpus, int32_t s_cap);
+int ss_slot_program(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo, const int32_t* slice_hi,
+                    const uint8_t* leave, const double* rtt, const int64_t* jitter_seed, int32_t s_cap,
+                    int64_t meta_stride, int64_t stream_stride, uint8_t* meta, double* stream, int32_t* s_used,
+                    int32_t* status, void* stream_h);
+int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_stride, const double* stream,
+                    int64_t stream_stride, int32_t s_cap, int32_t s_rows, const ss_replay_state* st,
+                    const double* occpow, int32_t occpow_len, int32_t window, int32_t n_req,
+                    const ss_replay_out* out, void* stream_h);
+int ss_set_slot_staging(int32_t stage_bytes, int32_t n_buffers);
+
 /* Kernel tuning knobs (0 = default); returns previous values via *_h. */
 int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
 

@@ -59,6 +59,14 @@ _SIGS = {
     "ss_replay": (C.c_int, [C.POINTER(DagSet), C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
                             C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
     "ss_set_tiling": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p]),
+    "ss_slot_meta_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "ss_slot_program": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]),
+    "ss_replay_slots": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+                                  C.c_int32, C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                  C.POINTER(ReplayOut), C.c_void_p]),
+    "ss_set_slot_staging": (C.c_int, [C.c_int32, C.c_int32]),
 }
 
 class PoolSet(C.Structure):

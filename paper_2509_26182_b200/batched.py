@@ -44,8 +44,15 @@ class ReplayResult:
 
 class ScenarioReplayer:
     def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
-                 max_requests: Optional[int] = None, stream=None):
+                 max_requests: Optional[int] = None, stream=None, mode: str = "slots"):
+        """mode "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
+        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay).  Bit-identical results."""
         import torch
+        if mode not in ("slots", "blocks"):
+            raise ValueError(f"mode must be 'slots' or 'blocks', got {mode!r}")
+        if scen.layer_count < 2:
+            mode = "blocks"                      # no boundaries: nothing to tile
+        self.mode = mode
         self.torch = torch
         self.scen = scen
         self.window = int(window)
@@ -83,7 +90,23 @@ class ScenarioReplayer:
         self.gpu_ptr = up(gpu_ptr, t32)
         self.col_len = torch.empty(S * L, dtype=t32, device=dev)
         self.node_gpu = torch.empty(S * cap_nodes, dtype=t32, device=dev)
-        self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
+        if mode == "blocks":
+            self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
+        else:
+            self.edge_val = None
+            # frontier |col_b U col_{b+1}| of the base plan bounds the slots (churn only removes hosts)
+            held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None])).sum(axis=1) \
+                if L > 1 else np.zeros(1, dtype=np.int64)
+            self.s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
+            n_plan = int(((hi >= lo) & (hi >= 1)).sum())
+            lib = N.load_library()
+            self.meta_stride = int(lib.ss_slot_meta_bytes(L, G, self.s_cap))
+            self.stream_stride = 2 * n_plan * self.s_cap
+            self.meta = torch.empty(S * self.meta_stride, dtype=torch.uint8, device=dev)
+            self.stream_buf = torch.empty(max(S * self.stream_stride, 2), dtype=f64, device=dev)
+            self.s_used = torch.zeros(S, dtype=t32, device=dev)
+            self.prog_status = torch.zeros(S, dtype=t32, device=dev)
+            self.s_rows = self.s_cap
         self.base_tau = up(np.tile(scen.base_tau, S), f64)
         self.slice_lo = up(lo, t32)
         self.slice_hi = up(hi, t32)
@@ -108,7 +131,7 @@ class ScenarioReplayer:
     def dag_set(self) -> N.DagSet:
         return N.DagSet(self.S, self.max_hosts, self.L, self.G, N.ptr(self.layer_ptr), N.ptr(self.col_off),
                         N.ptr(self.col_len), N.ptr(self.node_gpu), None, N.ptr(self.edge_off),
-                        N.ptr(self.edge_val))
+                        N.ptr(self.edge_val) if self.edge_val is not None else None)
 
     def build(self) -> None:
         """Scenario columns + jittered edge blocks, fully on device (ss_scenario_columns, ss_dag_edges)."""
@@ -118,7 +141,19 @@ class ScenarioReplayer:
                                         N.ptr(self.leave), N.ptr(self.col_off), N.ptr(self.col_len),
                                         N.ptr(self.node_gpu), N.ptr(self.status), N.ptr(self.aux), st),
                 "ss_scenario_columns")
-        if self.scen.jitter:
+        if self.mode == "slots":
+            N.check(lib.ss_slot_program(self.S, self.L, self.G, N.ptr(self.slice_lo), N.ptr(self.slice_hi),
+                                        N.ptr(self.leave), N.ptr(self.base_rtt),
+                                        N.ptr(self.seeds) if self.scen.jitter else None, self.s_cap, self.meta_stride,
+                                        self.stream_stride, N.ptr(self.meta), N.ptr(self.stream_buf),
+                                        N.ptr(self.s_used), N.ptr(self.prog_status), st), "ss_slot_program")
+            # one small D2H: the tile is sized by the slots actually used (two CTAs per SM at C4)
+            used = self.s_used.cpu().numpy()
+            bad = np.nonzero(self.prog_status.cpu().numpy())[0]
+            if bad.size:
+                raise ValueError(f"slot program failed for scenario {int(bad[0])} (slots > {self.s_cap})")
+            self.s_rows = int(max(1, used.max()))
+        elif self.scen.jitter:
             N.check(lib.ss_dag_edges(self.dag_set(), None, None, N.ptr(self.base_rtt), N.ptr(self.seeds), self.G,
                                      N.ptr(self.edge_val), st), "ss_dag_edges")
         else:
@@ -150,8 +185,14 @@ class ScenarioReplayer:
         st = N.ReplayState(N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self.occ), N.ptr(self.ring),
                            N.ptr(self.next_req), N.ptr(self.status), N.ptr(self.aux))
         ro = N.ReplayOut(N.ptr(out.cost), N.ptr(out.chain_hash), N.ptr(out.gpus))
-        N.check(N.lib().ss_replay(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window, n_req, ro,
-                                  N.stream_handle(self.stream)), "ss_replay")
+        if self.mode == "slots":
+            N.check(N.lib().ss_replay_slots(self.dag_set(), N.ptr(self.meta), self.meta_stride, N.ptr(self.stream_buf),
+                                            self.stream_stride, self.s_cap, self.s_rows, st, N.ptr(self.occpow),
+                                            self.occpow_len, self.window, n_req, ro, N.stream_handle(self.stream)),
+                    "ss_replay_slots")
+        else:
+            N.check(N.lib().ss_replay(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window, n_req,
+                                      ro, N.stream_handle(self.stream)), "ss_replay")
         return out
 
     def run_from_host(self, leave_h, seeds_h, n_req: int, cost_h, hash_h) -> ReplayResult:

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--budget", type=int, default=0)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--nojitter", action="store_true")
+    ap.add_argument("--mode", default="slots")
+    ap.add_argument("--stage", type=int, default=0)
+    ap.add_argument("--sbuf", type=int, default=0)
     args = ap.parse_args()
     import torch
     from paper_2509_26182_b200 import _native as N, scenarios as scen
@@ -44,7 +47,9 @@ def main():
     lib = N.lib()
     if args.nbuf or args.budget:
         lib.ss_set_tiling(args.budget * 1024, args.nbuf, None, None)
-    rp = ScenarioReplayer(ss, window=args.window)
+    if args.stage or args.sbuf:
+        lib.ss_set_slot_staging(args.stage * 1024, args.sbuf)
+    rp = ScenarioReplayer(ss, window=args.window, mode=args.mode)
     torch.cuda.synchronize()
     t1 = time.time()
     rp.build()
@@ -65,7 +70,7 @@ def main():
     t = float(np.median(times))
     sel = args.scen * args.req
     gbs = float(b2.mean()) * sel / t / 1e9
-    print(json.dumps({"scen": args.scen, "req": args.req, "L": args.L, "n": args.n, "k": plan.replication_count,
+    print(json.dumps({"mode": args.mode, "scen": args.scen, "req": args.req, "L": args.L, "n": args.n, "k": plan.replication_count,
                       "time_ms": t * 1e3, "sel_per_s": sel / t, "B2_mean": float(b2.mean()),
                       "algo_GBps": gbs, "frac_hbm": gbs / 6538.9, "times": times}))
 

@@ -87,7 +87,7 @@ def test_chain_router_golden(cuda_ready, router_replays, name, limit):
     assert router.stats.matrix_rebuilds == 1
 
 
-def _replayer_for_golden(rep, plan_dict, n_scen=1, seed0=None):
+def _replayer_for_golden(rep, plan_dict, n_scen=1, seed0=None, mode="slots"):
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer
     L = rep["L"]
@@ -99,15 +99,16 @@ def _replayer_for_golden(rep, plan_dict, n_scen=1, seed0=None):
     else:
         ss = scen.build_scenarios(cl, model, plan, n_scen, churn=0.0, jitter=False)
     W = rep["window"]
-    return ss, ScenarioReplayer(ss, window=-1 if W is None else W, max_requests=len(rep["routes"]) + 4)
+    return ss, ScenarioReplayer(ss, window=-1 if W is None else W, max_requests=len(rep["routes"]) + 4, mode=mode)
 
 
+@pytest.mark.parametrize("mode", ["slots", "blocks"])
 @pytest.mark.parametrize("name", ["c1", "c1_tie", "n32_tie", "rt16", "c2", "c4_s11", "c4_s12"])
-def test_replay_kernel_golden(cuda_ready, router_replays, name):
-    """ss_replay (on-device load update) == reference ChainRouter op script, bit-exact."""
+def test_replay_kernel_golden(cuda_ready, router_replays, name, mode):
+    """ss_replay / ss_replay_slots (on-device load update) == reference ChainRouter op script, bit-exact."""
     rep = router_replays[name]
     plan = rep.get("plan", router_replays.get("c4_plan"))
-    ss, rp = _replayer_for_golden(rep, plan)
+    ss, rp = _replayer_for_golden(rep, plan, mode=mode)
     if "leave" in rep:
         assert sorted(np.nonzero(ss.leave[0])[0].tolist()) == rep["leave"]
     n = len(rep["routes"])
@@ -132,8 +133,9 @@ def _hash(gpus_row):
     return sum(splitmix64((l << 32) | int(g)) for l, g in enumerate(gpus_row)) & M
 
 
+@pytest.mark.parametrize("mode", ["slots", "blocks"])
 @pytest.mark.parametrize("window", [64, 0, -1, 1, 7])
-def test_replay_many_scenarios_vs_oracle(cuda_ready, window):
+def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
     """C4-shaped batch (L64/N256 pool, churn + jitter) vs the oracle, every scenario."""
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer
@@ -143,7 +145,7 @@ def test_replay_many_scenarios_vs_oracle(cuda_ready, window):
     cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
     S, n_req = 12, 40
     ss = scen.build_scenarios(cl, model, plan, S, seed0=1000 + window, churn=0.05, jitter=True)
-    rp = ScenarioReplayer(ss, window=window, max_requests=n_req + 4)
+    rp = ScenarioReplayer(ss, window=window, max_requests=n_req + 4, mode=mode)
     out = rp.run(n_req, gpus=True)
     rp.raise_first_failure()
     gpus, cost, hashes = out.gpus.cpu().numpy(), out.cost.cpu().numpy(), out.chain_hash.cpu().numpy()
@@ -159,7 +161,8 @@ def test_replay_many_scenarios_vs_oracle(cuda_ready, window):
             assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
 
 
-def test_replay_tie_pool_vs_oracle(cuda_ready):
+@pytest.mark.parametrize("mode", ["slots", "blocks"])
+def test_replay_tie_pool_vs_oracle(cuda_ready, mode):
     """Homogeneous flops => many exact ties (13-23% of columns): first-index rule must hold."""
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer
@@ -168,7 +171,7 @@ def test_replay_tie_pool_vs_oracle(cuda_ready):
     cl, model = scen.synthetic_cluster(64, seed=5, model=scen.bench_model(48), homogeneous_flops=1e14)
     plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
     ss = scen.build_scenarios(cl, model, plan, 4, seed0=77, churn=0.05, jitter=False)
-    rp = ScenarioReplayer(ss, window=16, max_requests=64)
+    rp = ScenarioReplayer(ss, window=16, max_requests=64, mode=mode)
     out = rp.run(60, gpus=True)
     rp.raise_first_failure()
     for s in range(4):
@@ -185,7 +188,8 @@ def _plan_dict(d):
     return d
 
 
-def test_uncovered_scenario_reports_status(cuda_ready):
+@pytest.mark.parametrize("mode", ["slots", "blocks"])
+def test_uncovered_scenario_reports_status(cuda_ready, mode):
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer
     from paper_2509_26182_b200.errors import UncoveredLayer
@@ -196,7 +200,7 @@ def test_uncovered_scenario_reports_status(cuda_ready):
     first_gpu = min(g for g in range(ss.n_gpus) if ss.slice_lo[g] == 1)
     ss.leave[1, :] = False
     ss.leave[1, [g for g in range(ss.n_gpus) if ss.slice_lo[g] <= 1 <= ss.slice_hi[g]]] = True
-    rp = ScenarioReplayer(ss, window=4, max_requests=16)
+    rp = ScenarioReplayer(ss, window=4, max_requests=16, mode=mode)
     rp.run(5)
     st = rp.status.cpu().numpy()
     assert st[0] == 0 and st[2] == 0 and st[1] == 1 and int(rp.aux.cpu()[1]) == 1
