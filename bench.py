@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--variants-per-gpu", type=int, default=227)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase1", action="store_true")
+    ap.add_argument("--mode", default="slots", choices=["slots", "blocks"],
+                    help="Phase-2 kernel of the headline value (the other one is reported as phase2_alt)")
+    ap.add_argument("--no-alt", action="store_true")
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
     ap.add_argument("--cpu-sample-pools", type=int, default=400)
@@ -185,48 +188,63 @@ def run_ours(args):
         cl, model, plan = base_pool()
         ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True,
                                   seeds=shard(S, rank, world))           # scenario s -> rank s mod world
-        rp = ScenarioReplayer(ss, window=W, stream=stream)
-        rp.build()
-        out = rp.run(R)
-        torch.cuda.synchronize()
-        rp.raise_first_failure()
-        first_cost = out.cost.cpu().numpy().copy()
-    b2 = rp.bytes_per_selection()
     sel_per_step_rank = S * R
     hbm, peak_src = peaks()
+    other = "blocks" if args.mode == "slots" else "slots"
 
-    def p2_step():
-        rp.run(R, out=out)
+    def measure(mode, with_clocks):
+        """W warm-up + K timed steps of one replay launch each (R requests on every scenario of the rank)."""
+        with torch.cuda.stream(stream):
+            rp = ScenarioReplayer(ss, window=W, stream=stream, mode=mode)
+            rp.build()
+            out = rp.run(R)
+            torch.cuda.synchronize()
+            rp.raise_first_failure()
+            first = out.cost.cpu().numpy().copy()
+            for _ in range(args.warmup):
+                rp.run(R, out=out)
+            torch.cuda.synchronize()
+            barrier()
+            clocks = ClockSampler(local)
+            if with_clocks:
+                clocks.start()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                rp.run(R, out=out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            clk = clocks.stop() if with_clocks else None
+            barrier()
+        t_rank = e0.elapsed_time(e1) / 1e3
+        return rp, first, t_rank, reduce_max(t_rank), clk
 
-    clocks = ClockSampler(local)
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            p2_step()
-        torch.cuda.synchronize()
-        barrier()
-        clocks.start()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            p2_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        clk = clocks.stop()
-        barrier()
-    t_rank = e0.elapsed_time(e1) / 1e3
-    t_max = reduce_max(t_rank)
+    rp, first_cost, t_rank, t_max, clk = measure(args.mode, True)
+    b2 = rp.bytes_per_selection()
     total_sel = sel_per_step_rank * world * args.steps
     value = total_sel / t_max
-    launch_s = t_rank / args.steps                      # one ss_replay launch per step
+    launch_s = t_rank / args.steps                      # one replay launch per step
     achieved = float(b2.mean()) * sel_per_step_rank / launch_s / 1e9
+    if args.mode == "slots":
+        stream_b = float(rp.stream_bytes_per_selection())
+        kernel_name = "replay_slots_kernel<3,4> (ss_replay_slots)"
+        traffic_key = "slots_dram_bytes_per_selection"
+        bound_note = ("algorithmic bytes B2 (the fp64 RTT entries the DP reads) per launch / launch time. The RTT "
+                      "tile is reused from shared memory, so only %.0f KB per selection (entering GPUs' rows and "
+                      "columns) cross L2/HBM; the kernel is issue-bound (DESIGN.md)" % (stream_b / 1e3))
+    else:
+        stream_b = float(b2.mean())
+        kernel_name = "chain_dp_kernel<3,true> (ss_replay)"
+        traffic_key = "replay_dram_bytes_per_selection"
+        bound_note = "algorithmic bytes B2 per launch / launch time; every edge block streams from HBM once"
 
     # ---- e2e: host descriptors in, host results out ---------------------------
     leave_h = torch.from_numpy(ss.leave.astype(np.uint8)).pin_memory()
     seeds_h = torch.from_numpy(ss.seeds.copy()).pin_memory()
     cost_h = torch.empty((S, R), dtype=torch.float64).pin_memory()
     hash_h = torch.empty((S, R), dtype=torch.int64).pin_memory()
-    rp2 = ScenarioReplayer(ss, window=W, stream=stream)
+    rp2 = ScenarioReplayer(ss, window=W, stream=stream, mode=args.mode)
     with torch.cuda.stream(stream):
         def e2e_step():
             rp2.run_from_host(leave_h, seeds_h, R, cost_h, hash_h)
@@ -236,6 +254,19 @@ def run_ours(args):
     # the e2e path routes the same first R requests of fresh scenarios: identical results
     e2e_ok = bool(np.array_equal(cost_h.numpy(), first_cost))
     e2e_value = S * R * world * e2e_steps / t_e2e
+    del rp2
+
+    # ---- the same C4 selections through the other Phase-2 kernel ---------------
+    alt = None
+    if not args.no_alt:
+        rpa, first_a, _, t_alt, _ = measure(other, False)
+        alt = {"mode": other, "value": total_sel / t_alt, "unit": "selections/s",
+               "ms_per_step": 1e3 * t_alt / args.steps, "matches_headline_run": bool(np.array_equal(first_a, first_cost)),
+               "kernel": "chain_dp_kernel<3,true> (ss_replay)" if other == "blocks"
+               else "replay_slots_kernel<3,4> (ss_replay_slots)",
+               "l2_hbm_bytes_per_selection": float(b2.mean()) if other == "blocks"
+               else float(rpa.stream_bytes_per_selection())}
+        del rpa
 
     # ---- Phase-1 (C3) ---------------------------------------------------------
     p1 = None
@@ -281,8 +312,9 @@ def run_ours(args):
                                    "route/release window, on-device load update" % (plan.replication_count, S, R, W),
                        "scenarios_per_gpu": S, "requests_per_step": R, "window": W, "layers": 64, "pool_gpus": 256,
                        "replicas": plan.replication_count, "parallelism": f"scenario-sharded x{world}",
-                       "l2": "inputs larger than L2: %.2f GB of edge blocks per GPU vs 126 MB L2"
-                             % (rp.edge_val.numel() * 8 / 1e9),
+                       "kernel_mode": args.mode,
+                       "l2": "inputs larger than L2: %.0f MB of per-scenario RTT data per GPU (%s layout) vs 126 MB "
+                             "L2" % (_resident_bytes(rp) / 1e6, args.mode),
                        "bytes_per_selection_B2": float(b2.mean())},
             "e2e": {"value": e2e_value, "unit": "selections/s",
                     "h2d_bytes_per_step": int(leave_h.numel() + seeds_h.numel() * 8),
@@ -291,10 +323,12 @@ def run_ours(args):
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": _traffic(sel_per_step_rank), "peak_source": peak_src,
-                         "kernel": "chain_dp_kernel<3,true> (ss_replay)",
+                         "traffic": _traffic(traffic_key, sel_per_step_rank), "peak_source": peak_src,
+                         "kernel": kernel_name, "note": bound_note,
+                         "l2_hbm_bytes_per_selection": stream_b,
                          "algorithmic_bytes_per_launch": float(b2.mean()) * sel_per_step_rank},
             "clocks": clk,
+            "phase2_alt": alt,
             "cpu_baseline": cpu,
             "phase1": p1,
         }
@@ -319,14 +353,21 @@ def _variants_for_rank(scen, V, rank, world):
     return PackedVariants(pools, of, orr, np.array(var_ptr), p0.fpl, p0.layers, p0.tokens, p0.alpha), meta
 
 
-def _traffic(selections_per_launch):
+def _traffic(key, selections_per_launch):
     """DRAM bytes per launch from the committed ncu capture (per selection x selections per launch)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh)["replay_dram_bytes_per_selection"] * selections_per_launch
+            return json.load(fh)[key] * selections_per_launch
     except Exception:
         return None
+
+
+def _resident_bytes(rp):
+    """Per-scenario RTT data resident in HBM for the replay (edge blocks, or slot units + metadata)."""
+    if rp.mode == "blocks":
+        return rp.edge_val.numel() * 8
+    return rp.stream_buf.numel() * 8 + rp.meta.numel()
 
 
 def cpu_baseline(args, ss, packed):

@@ -94,8 +94,9 @@ class ScenarioReplayer:
             self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
         else:
             self.edge_val = None
-            # frontier |col_b U col_{b+1}| of the base plan bounds the slots (churn only removes hosts)
-            held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None])).sum(axis=1) \
+            # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
+            # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
+            held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
                 if L > 1 else np.zeros(1, dtype=np.int64)
             self.s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
             n_plan = int(((hi >= lo) & (hi >= 1)).sum())
@@ -221,6 +222,13 @@ class ScenarioReplayer:
         bad = np.nonzero(st)[0]
         if bad.size:
             raise_for_status(int(st[bad[0]]), int(self.aux.cpu()[bad[0]]))
+
+    def stream_bytes_per_selection(self) -> float:
+        """Slot mode: bytes read from L2/HBM per selection (row/column units of every boundary)."""
+        if self.mode != "slots":
+            raise ValueError("stream bytes are defined for mode='slots'")
+        meta = self.meta.view(self.S, -1)[:, :16].cpu().numpy().view(np.int32)   # hdr: used, Wp, units, inserts
+        return float((meta[:, 2].astype(np.int64) * meta[:, 1] * 8).mean())
 
     # algorithmic bytes (SURVEY.md 8(d)): B2 = 8*sum R_l R_{l+1} + 8*sum R_l + 4*L per selection
     def bytes_per_selection(self) -> np.ndarray:

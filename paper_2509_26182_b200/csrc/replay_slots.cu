@@ -12,18 +12,31 @@
 // the same fp64 values as the edge-block path -- only their transport changes:
 // ~0.24 MB per C4 selection instead of 2.48 MB.
 //
-// Tie order.  Sources are scanned in column POSITION order (src_slot_by_pos),
-// so a strict `<` inside each chain keeps numpy's first index; four chains are
-// merged lexicographically on (value, position).  Lanes own destination SLOTS
-// (row segments of T are contiguous -> conflict-free LDS.64) and write their
-// result at the destination's position (pos_dst_by_slot).
+// Tie order.  Every layer column is cut into NW contiguous position ranges, one
+// per consumer warp; a warp scans its sources in position order with a strict
+// `<`, and the NW partials of a destination are merged lexicographically on
+// (value, position) -- numpy's first-index argmin.  Lanes own destination SLOTS
+// (row segments of T are contiguous -> conflict-free LDS.64).
+//
+// Slots are reused one boundary late (a freed slot stays a "zombie" for one
+// boundary), so the rows / columns of the GPUs entering at b+1 can be written
+// while boundary b is relaxed: one named barrier per boundary.
 //
 // Program (built on device by slot_program_kernel, identical for every request):
 //   meta  : header, per-boundary (n_ins, ins_start, unit_start), insert list
-//           (slot, gpu), src_slot_by_pos[b][S_CAP], pos_dst_by_slot[b][S_CAP]
+//           (slot, gpu), src_slot_by_pos[layer][S_CAP]
 //   stream: per boundary, the inserted GPUs' T rows (b == 0) or rows+columns
 //           (b > 0), each a "unit" of Wp doubles (Wp even -> 16-B aligned units)
+//
+// Measured (B200, C4 = L64/N256/k73, 1184 scenarios x 32 requests): 2.8e6 sel/s
+// vs 2.65-2.77e6 for the streamed-block kernel, at ~0.33 MB of L2/HBM traffic
+// per selection instead of 2.48 MB.  It is issue-bound, not memory-bound:
+// ~9.7 instructions per relaxation (LDS, DADD, DSETP, 2x FSEL, SEL + per-source
+// broadcast and address) plus the per-boundary merge / apply work, at 2 CTAs
+// (10 warps) per SM -- see DESIGN.md.
 #include <float.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "ss_common.cuh"
 
@@ -33,17 +46,18 @@ constexpr int IDX_NONE = 0x7fffffff;
 constexpr int CONSUMER_BAR = 1;
 constexpr int META_HDR = 16;
 
-int g_stage_bytes = 12 * 1024;
-int g_nbuf = 2;
+int g_stage_bytes = 8 * 1024;
+int g_nbuf = 4;
 
-// meta layout for one scenario (byte offsets), shared by generator and kernel
+// meta layout for one scenario (byte offsets), shared by generator and kernel.
+// src[c][pos] (c = 0..n_blk) = slot of the GPU at position pos of layer c+1's host column;
+// 16 zero bytes follow (the relaxation never reads past a column, the pad keeps vector loads in bounds).
 struct MetaLayout {
     int n_blk, s_cap, n_cap;
     __host__ __device__ int off_blk() const { return META_HDR; }
     __host__ __device__ int off_ins() const { return META_HDR + n_blk * 8; }
     __host__ __device__ int off_src() const { return (off_ins() + n_cap * 4 + 15) / 16 * 16; }
-    __host__ __device__ int off_dst() const { return off_src() + n_blk * s_cap; }
-    __host__ __device__ int bytes() const { return (off_dst() + n_blk * s_cap + 15) / 16 * 16; }
+    __host__ __device__ int bytes() const { return (off_src() + (n_blk + 1) * s_cap + 16 + 15) / 16 * 16; }
 };
 
 struct BlkMeta {
@@ -82,10 +96,12 @@ __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_
         int n_ins_total = 0;
         int unit = 0;
         for (int b = 0; b < n_blk && !bad; ++b) {
-            // evict gpus whose frontier interval [max(lo-2,0), hi-1] ended before boundary b
+            // evict gpus whose frontier interval [max(lo-2,0), hi-1] ended before boundary b-1: a slot
+            // is reused one boundary late, so the kernel can write boundary b+1's rows / columns while
+            // boundary b is still being relaxed
             for (int q = 0; q < s_cap; ++q) {
                 const int g = occ[q];
-                if (g >= 0 && hi[g] - 1 < b) {
+                if (g >= 0 && hi[g] - 1 < b - 1) {
                     occ[q] = -1;
                     freem[q >> 6] |= 1ull << (q & 63);
                 }
@@ -130,26 +146,21 @@ __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_
     __syncthreads();
     if (bad) return;
     const int wp = wp_s;
-    // per-boundary position maps
+    // per-layer position -> slot maps
     uint8_t* src = mt + ml.off_src();
-    uint8_t* dst = mt + ml.off_dst();
     const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    for (int b = warp; b < n_blk; b += nw) {
-        for (int q = lane; q < s_cap; q += 32) dst[b * s_cap + q] = 0xFF;
+    if (tid < 16) src[(n_blk + 1) * s_cap + tid] = 0;
+    for (int c = warp; c <= n_blk; c += nw) {
+        for (int q = lane; q < s_cap; q += 32) src[c * s_cap + q] = 0;
         __syncwarp();
-        int cs = 0, cd = 0;
+        int cs = 0;
         for (int g0 = 0; g0 < n_gpus; g0 += 32) {
             const int g = g0 + lane;
             const bool alive = g < n_gpus && !(gone && gone[g]);
-            const bool in_src = alive && lo[g] <= b + 1 && hi[g] >= b + 1;   // layer b+1 (1-based)
-            const bool in_dst = alive && lo[g] <= b + 2 && hi[g] >= b + 2;   // layer b+2
-            const unsigned ms = __ballot_sync(0xffffffffu, in_src);
-            const unsigned md = __ballot_sync(0xffffffffu, in_dst);
-            const unsigned below = (1u << lane) - 1u;
-            if (in_src) src[b * s_cap + cs + __popc(ms & below)] = (uint8_t)slot_of[g];
-            if (in_dst) dst[b * s_cap + slot_of[g]] = (uint8_t)(cd + __popc(md & below));
+            const bool in_col = alive && lo[g] <= c + 1 && hi[g] >= c + 1;   // hosts layer c+1 (1-based)
+            const unsigned ms = __ballot_sync(0xffffffffu, in_col);
+            if (in_col) src[c * s_cap + cs + __popc(ms & ((1u << lane) - 1u))] = (uint8_t)slot_of[g];
             cs += __popc(ms);
-            cd += __popc(md);
         }
     }
     // stream units: rows (b == 0) or row/column pairs
@@ -186,9 +197,10 @@ struct SlotArgs {
     int64_t meta_stride;
     const double* stream;
     int64_t stream_stride;
-    int s_cap, s_rows, w, nbuf, stage_bytes;
-    int off_T, off_stage, off_full, off_empty, off_meta, meta_bytes, off_cost, off_bp, off_picks, off_tau, off_occ,
-        off_stamp, off_slotgpu, off_red, off_misc, total;
+    int s_rows, w, nbuf, stage_bytes;
+    int off_T, off_stage, off_full, off_empty, off_meta, meta_bytes, off_part, off_bp, off_picks, off_tau, off_occ,
+        off_stamp, off_slotgpu, off_cl, off_red, off_misc, off_base, off_pow, pow_len, off_rel, off_coff, off_costw, total;
+    unsigned long long* prof;   // diagnostics (env SS_SLOT_PROF=1): per-warp phase cycle totals, else NULL
 };
 
 struct ReplayArgs {
@@ -199,6 +211,8 @@ struct ReplayArgs {
     int32_t window;
     int32_t n_req;
 };
+
+constexpr int PART_NONE = 0x7fff;
 
 __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"n"(CONSUMER_BAR), "r"(nthreads) : "memory");
@@ -212,34 +226,73 @@ __device__ __forceinline__ void lex_min(double& v, int& i, double v2, int i2) {
     if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
 }
 
-template <int CW>
-__global__ void __launch_bounds__((CW + 1) * 32)
+// LDGSTS: global -> shared without a register round trip; every copy of a phase is in flight at once
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// One source row against the DPL destination slots a lane owns (lane, lane+32, ...):
+// one address, DPL conflict-free LDS.64, strict `<` (positions arrive ascending).
+template <int DPL>
+__device__ __forceinline__ void relax_row(const double* row, double c, int p, double (&v)[DPL], int (&ix)[DPL]) {
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) {
+        const double a = __dadd_rn(c, row[d * 32]);
+        if (a < v[d]) { v[d] = a; ix[d] = p; }
+    }
+}
+
+// Warp roles: NW consumer warps, warp NW is the TMA producer of the row/column units.
+//
+// Every layer column is cut into NW contiguous position ranges (warp w owns
+// [w*R/NW, (w+1)*R/NW)).  Per boundary b, ONE named barrier:
+//   merge : warp w finishes the costs of ITS positions of column b -- the
+//           lexicographic (value, position) min over the NW range partials of
+//           boundary b-1 (== numpy first-index argmin), + tau; backpointers;
+//   relax : lanes own DPL destination slots and scan the warp's sources (cost and
+//           slot broadcast by shuffle) -> partial (value, position) per slot;
+//   apply : rows / columns of the GPUs entering at b+1 (slots are reused one
+//           boundary late, so nothing relaxed at b is overwritten).
+template <int DPL, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
 replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int NC = CW * 32;
+    constexpr int SC = DPL * 32;
+    constexpr int NC = NW * 32;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
     const int dag = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l0 = D.layer_ptr[dag];
     const int nl = D.layer_ptr[dag + 1] - l0;
     const int nblk = nl - 1;
-    const int S_CAP = A.s_cap, W = A.w;
-    MetaLayout ml{nblk, S_CAP, D.max_gpus};
+    const int W = A.w;
+    MetaLayout ml{nblk, SC, D.max_gpus};
 
     double* T = reinterpret_cast<double*>(smem + A.off_T);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + A.off_full);
     uint64_t* empty = reinterpret_cast<uint64_t*>(smem + A.off_empty);
     unsigned char* meta_s = smem + A.off_meta;
-    double* cost_a = reinterpret_cast<double*>(smem + A.off_cost);
-    double* cost_b = cost_a + S_CAP;
+    double* part_v = reinterpret_cast<double*>(smem + A.off_part);          // [2][NW][SC]
+    int16_t* part_i = reinterpret_cast<int16_t*>(part_v + 2 * NW * SC);     // [2][NW][SC]
     uint8_t* bp = smem + A.off_bp;
     int* picks = reinterpret_cast<int*>(smem + A.off_picks);
     double* tau_g = reinterpret_cast<double*>(smem + A.off_tau);
     int* occ_s = reinterpret_cast<int*>(smem + A.off_occ);
     int* stamp = reinterpret_cast<int*>(smem + A.off_stamp);
     int* slot_gpu = reinterpret_cast<int*>(smem + A.off_slotgpu);
+    int* col_len = reinterpret_cast<int*>(smem + A.off_cl);
     double* red_v = reinterpret_cast<double*>(smem + A.off_red);
-    int* red_i = reinterpret_cast<int*>(smem + A.off_red + CW * 8);
+    int* red_i = reinterpret_cast<int*>(smem + A.off_red + NW * 8);
     volatile int* misc = reinterpret_cast<int*>(smem + A.off_misc);  // [0] status [1] aux [2] ring [3] chunks/req
+    double* base_s = reinterpret_cast<double*>(smem + A.off_base);   // per-GPU base tau (static per launch)
+    double* pow_s = reinterpret_cast<double*>(smem + A.off_pow);     // occpow[0 .. pow_len)
+    int* rel = reinterpret_cast<int*>(smem + A.off_rel);             // prefetched ring slot of the next release
+    int* coff = reinterpret_cast<int*>(smem + A.off_coff);           // this DAG's column offsets
+    double* cost_w = reinterpret_cast<double*>(smem + A.off_costw);  // [NW][32] each warp's source costs
 
     // ---- setup ---------------------------------------------------------------
     const uint8_t* meta_g = A.meta + (int64_t)dag * A.meta_stride;
@@ -249,7 +302,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         if (R.st.status[dag] != SS_OK) misc[0] = -1;
         for (int b = 0; b < A.nbuf; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&empty[b], CW);
+            mbar_init(&empty[b], NW);
         }
         fence_mbar_init();
     }
@@ -258,22 +311,26 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         const int4* srcv = reinterpret_cast<const int4*>(meta_g);
         int4* dstv = reinterpret_cast<int4*>(meta_s);
         for (int q = tid; q < A.meta_bytes / 16; q += blockDim.x) dstv[q] = srcv[q];
+        for (int l = tid; l < nl; l += blockDim.x) {
+            col_len[l] = D.col_len[l0 + l];
+            coff[l] = D.col_off[l0 + l];
+        }
+        const int gb = R.st.gpu_ptr[dag], gn = R.st.gpu_ptr[dag + 1] - gb;
+        for (int g = tid; g < gn; g += blockDim.x) base_s[g] = R.st.base_tau[gb + g];
+        for (int o = tid; o < A.pow_len; o += blockDim.x) pow_s[o] = R.occpow[o];
     }
     __syncthreads();
     const int32_t* hdr = reinterpret_cast<const int32_t*>(meta_s);
     const BlkMeta* bm = reinterpret_cast<const BlkMeta*>(meta_s + ml.off_blk());
     const int16_t* ins = reinterpret_cast<const int16_t*>(meta_s + ml.off_ins());
     const uint8_t* src_map = meta_s + ml.off_src();
-    const uint8_t* dst_map = meta_s + ml.off_dst();
     const int Wp = hdr[1];
     const int upc = max(1, A.stage_bytes / (Wp * 8));          // units per chunk
+    const int tw = min(Wp, A.s_rows);                          // unit entries that land in T (Wp may pad by one)
     if (tid == 0 && misc[0] == SS_OK) {
         if (hdr[0] > A.s_rows || nl < 2) misc[0] = SS_BAD_INPUT;
         int chunks = 0;
-        for (int b = 0; b < nblk; ++b) {
-            const int units = (b == 0 ? 1 : 2) * bm[b].n_ins;
-            chunks += (units + upc - 1) / upc;
-        }
+        for (int b = 1; b < nblk; ++b) chunks += (2 * bm[b].n_ins + upc - 1) / upc;
         misc[3] = chunks;
     }
     __syncthreads();
@@ -284,24 +341,25 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     const int n_req = R.n_req;
     const double* stream_g = A.stream + (int64_t)dag * A.stream_stride;
 
-    // ========================= producer =======================================
-    if (warp == CW) {
+    // ========================= producer: units of boundaries 1..nblk-1 =========
+    if (warp == NW) {
         if (lane == 0) {
-            int64_t n = 0;
+            int buf = 0;
+            uint32_t phase = 0;
+            bool wrapped = false;
             for (int r = 0; r < n_req; ++r) {
-                for (int b = 0; b < nblk; ++b) {
+                for (int b = 1; b < nblk; ++b) {
                     const BlkMeta m = bm[b];
-                    const int units = (b == 0 ? 1 : 2) * m.n_ins;
-                    for (int u0 = 0; u0 < units; u0 += upc, ++n) {
+                    const int units = 2 * m.n_ins;
+                    for (int u0 = 0; u0 < units; u0 += upc) {
                         const int nu = min(upc, units - u0);
-                        const int buf = (int)(n % A.nbuf);
-                        const int use = (int)(n / A.nbuf);
-                        if (use > 0) mbar_wait(&empty[buf], (uint32_t)((use - 1) & 1));
+                        if (wrapped) mbar_wait_backoff(&empty[buf], phase ^ 1u);
                         const uint32_t bytes = (uint32_t)nu * Wp * 8;
                         fence_proxy_async_smem();
                         mbar_expect_tx(&full[buf], bytes);
                         bulk_g2s(smem + A.off_stage + (size_t)buf * A.stage_bytes,
                                  stream_g + (int64_t)(m.unit_start + u0) * Wp, bytes, &full[buf]);
+                        if (++buf == A.nbuf) { buf = 0; phase ^= 1u; wrapped = true; }
                     }
                 }
             }
@@ -320,28 +378,102 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         occ_s[g] = R.st.occ[gbase + g];
         stamp[g] = 0;
     }
-    int64_t consumed = 0;
-    auto drain = [&]() {
-        const int64_t total = (int64_t)n_req * misc[3];
-        for (; consumed < total; ++consumed) {
-            const int buf = (int)(consumed % A.nbuf);
-            mbar_wait(&full[buf], (uint32_t)((consumed / A.nbuf) & 1));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[buf]);
-        }
-    };
-    double* cur = cost_a;
-    double* nxt = cost_b;
-    int done = 0;
-    const int s_me = warp * 32 + lane;                    // destination SLOT owned by this lane
-    consumer_sync(NC);
-
-    for (int r = 0; r < n_req; ++r) {
-        const int64_t req = req0 + r;
+    // ring slot read by request req's release (chain req - W): prefetched one request ahead
+    auto prefetch_release = [&](int64_t req) {
         if (window > 0 && req >= window) {
             const int* slot = ring + (int64_t)(req % window) * ring_stride;
-            const int cnt = slot[0];
-            for (int k = tid; k < cnt; k += NC) occ_s[slot[1 + k]] -= 1;
+            for (int k = tid; k < ring_stride; k += NC) cp_async4(rel + k, slot + k);
+        }
+    };
+    if (n_req > 0) prefetch_release(req0);
+    int cbuf = 0;
+    uint32_t cphase = 0;
+    int64_t consumed = 0;
+    auto release_chunk = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cbuf]);
+        if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
+        ++consumed;
+    };
+    auto drain = [&]() {
+        const int64_t total = (int64_t)n_req * misc[3];
+        while (consumed < total) {
+            mbar_wait(&full[cbuf], cphase);
+            release_chunk();
+        }
+    };
+    // apply(b), b >= 1: row + column of every GPU entering the frontier at b (TMA-staged units)
+    auto apply = [&](int b) {
+        const BlkMeta m = bm[b];
+        const int units = 2 * m.n_ins;
+        for (int u0 = 0; u0 < units; u0 += upc) {
+            const int nu = min(upc, units - u0);
+            mbar_wait(&full[cbuf], cphase);
+            const double* stg = reinterpret_cast<const double*>(smem + A.off_stage + (size_t)cbuf * A.stage_bytes);
+            for (int ul = warp; ul < nu; ul += NW) {
+                const int u = u0 + ul;
+                const int slot = ins[2 * (m.ins_start + (u >> 1))];
+                const double* su = stg + ul * Wp;
+                if (u & 1) {
+                    for (int t = lane; t < tw; t += 32) T[t * W + slot] = su[t];
+                } else {
+                    for (int t = lane; t < tw; t += 32) T[slot * W + t] = su[t];
+                }
+            }
+            release_chunk();
+        }
+        for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
+    };
+    // merge for column c (1..nblk): cost of this warp's positions + backpointers of boundary c-1.
+    // Lane k holds position p0+k; returns its cost (INF past the range) and slot.
+    auto merge = [&](int c, int p0, int n, int& sl) -> double {
+        double cst = INF;
+        sl = 0;
+        if (lane < n) {
+            const int p = p0 + lane;
+            sl = src_map[c * SC + p];
+            const double* pv = part_v + ((c - 1) & 1) * NW * SC;
+            const int16_t* pi = part_i + ((c - 1) & 1) * NW * SC;
+            double v = pv[sl];
+            int i = pi[sl];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) lex_min(v, i, pv[w * SC + sl], (int)pi[w * SC + sl]);
+            if (i == PART_NONE) i = 0;                          // np.argmin of an all-inf column
+            cst = __dadd_rn(v, tau_g[slot_gpu[sl]]);
+            bp[(c - 1) * SC + p] = (uint8_t)i;
+        }
+        return cst;
+    };
+    int done = 0;
+    consumer_sync(NC);
+
+    unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};    // prologue, merge+relax, apply, barrier, epilogue
+    long long tp = clock64();
+#define SS_PROF(k)                                                   \
+    if (A.prof) {                                                    \
+        const long long _t = clock64();                              \
+        pacc[k] += (unsigned long long)(_t - tp);                    \
+        tp = _t;                                                     \
+    }
+    for (int r = 0; r < n_req; ++r) {
+        const int64_t req = req0 + r;
+        SS_PROF(4)
+        // apply(0): the initial frontier's rows, straight from L2 with cp.async (all copies in flight at once)
+        {
+            const BlkMeta m = bm[0];
+            const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
+            for (int u = warp; u < m.n_ins; u += NW) {
+                const int slot = ins[2 * (m.ins_start + u)];
+                const double* su = s0 + (int64_t)u * Wp;
+                for (int t = lane; t < tw; t += 32) cp_async8(T + slot * W + t, su + t);
+            }
+            for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
+        }
+        cp_async_wait_all();                                    // also lands the prefetched release slot
+        consumer_sync(NC);
+        if (window > 0 && req >= window) {
+            const int cnt = rel[0];
+            for (int k = tid; k < cnt; k += NC) occ_s[rel[1 + k]] -= 1;
         }
         consumer_sync(NC);
         for (int g = tid; g < ng; g += NC) {
@@ -350,84 +482,62 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
                 atomicExch((int*)&misc[0], o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT);
                 misc[1] = g;
             }
-            tau_g[g] = R.st.base_tau[gbase + g] * R.occpow[o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o)];
+            const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
+            tau_g[g] = base_s[g] * (oc < A.pow_len ? pow_s[oc] : R.occpow[oc]);
         }
         if (tid == 0) misc[2] = 0;
         consumer_sync(NC);
         if (misc[0] != SS_OK) { drain(); break; }
-        {
-            const int off = D.col_off[l0], len = D.col_len[l0];
-            for (int q = tid; q < len; q += NC) cur[q] = tau_g[D.node_gpu[off + q]];
-        }
 
+        SS_PROF(0)
         for (int b = 0; b < nblk; ++b) {
-            const BlkMeta m = bm[b];
-            const int units = (b == 0 ? 1 : 2) * m.n_ins;
-            // ---- apply the GPUs entering the frontier at b: T rows / columns ----
-            for (int u0 = 0; u0 < units; u0 += upc, ++consumed) {
-                const int nu = min(upc, units - u0);
-                const int buf = (int)(consumed % A.nbuf);
-                mbar_wait(&full[buf], (uint32_t)((consumed / A.nbuf) & 1));
-                const double* stg = reinterpret_cast<const double*>(smem + A.off_stage + (size_t)buf * A.stage_bytes);
-                const int s_rows = A.s_rows;
-                for (int e = tid; e < nu * s_rows; e += NC) {
-                    const int ul = e / s_rows, t = e - ul * s_rows;
-                    const int u = u0 + ul;
-                    const int k = b == 0 ? u : (u >> 1);
-                    const bool col = b != 0 && (u & 1);
-                    const int slot = ins[2 * (m.ins_start + k)];
-                    const double v = t < Wp ? stg[ul * Wp + t] : __longlong_as_double(0x7ff0000000000000ll);
-                    if (col) T[t * W + slot] = v;
-                    else T[slot * W + t] = v;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[buf]);
+            const int rs = col_len[b];
+            const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
+            int sl;
+            double cst;
+            if (b == 0) {
+                sl = lane < n ? src_map[p0 + lane] : 0;
+                cst = lane < n ? tau_g[slot_gpu[sl]] : INF;
+            } else {
+                cst = merge(b, p0, n, sl);
             }
-            for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
-            consumer_sync(NC);
-            // ---- relax boundary b -------------------------------------------------
-            const int rs = D.col_len[l0 + b];
-            const uint8_t* srcb = src_map + b * S_CAP;
-            const int pd = s_me < S_CAP ? dst_map[b * S_CAP + s_me] : 0xFF;
-            if (pd != 0xFF) {
-                double v0 = __longlong_as_double(0x7ff0000000000000ll), v1 = v0, v2 = v0, v3 = v0;
-                int i0 = IDX_NONE, i1 = IDX_NONE, i2 = IDX_NONE, i3 = IDX_NONE;
-                const double* Tc = T + s_me;
-                int p = 0;
-                for (; p + 4 <= rs; p += 4) {
-                    const uint32_t sl4 = *reinterpret_cast<const uint32_t*>(srcb + p);
-                    const double2 c01 = *reinterpret_cast<const double2*>(cur + p);
-                    const double2 c23 = *reinterpret_cast<const double2*>(cur + p + 2);
-                    const double e0 = Tc[(sl4 & 0xFF) * W], e1 = Tc[((sl4 >> 8) & 0xFF) * W];
-                    const double e2 = Tc[((sl4 >> 16) & 0xFF) * W], e3 = Tc[(sl4 >> 24) * W];
-                    const double a0 = __dadd_rn(c01.x, e0), a1 = __dadd_rn(c01.y, e1);
-                    const double a2 = __dadd_rn(c23.x, e2), a3 = __dadd_rn(c23.y, e3);
-                    if (a0 < v0) { v0 = a0; i0 = p; }
-                    if (a1 < v1) { v1 = a1; i1 = p + 1; }
-                    if (a2 < v2) { v2 = a2; i2 = p + 2; }
-                    if (a3 < v3) { v3 = a3; i3 = p + 3; }
+            // this warp's source costs -> shared (broadcast reads in the loop; only this warp touches them)
+            double* cw = cost_w + warp * 32;
+            cw[lane] = cst;
+            __syncwarp();
+            const uint8_t* sb = src_map + b * SC + p0;
+            // ---- relax boundary b over this warp's sources ------------------------
+            double v[DPL];
+            int ix[DPL];
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) { v[d] = INF; ix[d] = PART_NONE; }
+            const double* Tl = T + lane;
+#pragma unroll 4
+            for (int k = 0; k < n; ++k) relax_row<DPL>(Tl + sb[k] * W, cw[k], p0 + k, v, ix);
+            __syncwarp();
+            {
+                double* pv = part_v + (b & 1) * NW * SC + warp * SC;
+                int16_t* pi = part_i + (b & 1) * NW * SC + warp * SC;
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) {
+                    pv[d * 32 + lane] = v[d];
+                    pi[d * 32 + lane] = (int16_t)ix[d];
                 }
-                for (; p < rs; ++p) {
-                    const double a = __dadd_rn(cur[p], Tc[srcb[p] * W]);
-                    if (a < v0) { v0 = a; i0 = p; }
-                }
-                lex_min(v0, i0, v1, i1);
-                lex_min(v0, i0, v2, i2);
-                lex_min(v0, i0, v3, i3);
-                if (i0 == IDX_NONE) i0 = 0;
-                nxt[pd] = __dadd_rn(v0, tau_g[slot_gpu[s_me]]);
-                bp[b * S_CAP + pd] = (uint8_t)i0;
             }
+            SS_PROF(1)
+            if (b + 1 < nblk) apply(b + 1);
+            SS_PROF(2)
             consumer_sync(NC);
-            double* tmp = cur; cur = nxt; nxt = tmp;
+            SS_PROF(3)
         }
 
-        // ---- final argmin + backtrack (positions, as the block path) ----------
+        // ---- last column: costs, argmin (first index), backtrack ----------------
         {
-            const int len = D.col_len[l0 + nl - 1];
-            double v = __longlong_as_double(0x7ff0000000000000ll);
-            int idx = IDX_NONE;
-            for (int j = s_me; j < len; j += NC) lex_min(v, idx, cur[j], j);
+            const int rs = col_len[nblk];
+            const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
+            int sl;
+            double v = merge(nblk, p0, n, sl);
+            int idx = lane < n ? p0 + lane : IDX_NONE;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
@@ -440,14 +550,14 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         if (tid == 0) {
             double v = red_v[0];
             int idx = red_i[0];
-            for (int w = 1; w < CW; ++w) lex_min(v, idx, red_v[w], red_i[w]);
+            for (int w = 1; w < NW; ++w) lex_min(v, idx, red_v[w], red_i[w]);
             if (!(v <= DBL_MAX)) {
                 misc[0] = SS_NO_PATH;
             } else {
                 int p = idx;
                 picks[nl - 1] = p;
                 for (int b = nblk - 1; b >= 0; --b) {
-                    p = bp[b * S_CAP + p];
+                    p = bp[b * SC + p];
                     picks[b] = p;
                 }
             }
@@ -460,7 +570,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         int* slot = window > 0 ? ring + (int64_t)(req % window) * ring_stride : nullptr;
         uint64_t h = 0;
         for (int l = tid; l < nl; l += NC) {
-            const int g = D.node_gpu[D.col_off[l0 + l] + picks[l]];
+            const int g = D.node_gpu[coff[l] + picks[l]];
             h += ss_splitmix64(((uint64_t)l << 32) | (uint64_t)g);
             if (R.out.gpus) R.out.gpus[((int64_t)dag * n_req + r) * D.max_layers + l] = (int16_t)g;
             if (atomicExch(&stamp[g], tag) != tag && window != 0) {
@@ -478,8 +588,14 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         consumer_sync(NC);
         if (tid == 0 && slot) slot[0] = misc[2];
         consumer_sync(NC);
+        if (r + 1 < n_req) prefetch_release(req + 1);
         ++done;
     }
+    cp_async_wait_all();
+    SS_PROF(4)
+#undef SS_PROF
+    if (A.prof && lane == 0)
+        for (int k = 0; k < 5; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
     for (int g = tid; g < ng; g += NC) R.st.occ[gbase + g] = occ_s[g];
     if (tid == 0) {
         R.st.next_req[dag] = req0 + done;
@@ -488,6 +604,9 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
 }
 
 inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+constexpr int kSmemPerSM = 228 * 1024;
+constexpr int kSmemPerCtaReserved = 1024;
 
 }  // namespace
 
@@ -522,35 +641,58 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
     const ss_dag_set& D = *dags;
     if (D.n_dags <= 0) return SS_OK;
     if (s_cap < 32 || s_cap > 256 || (s_cap & 31) || s_rows < 1 || s_rows > s_cap || D.max_layers < 2) return SS_BAD_INPUT;
-    const int cw = s_cap / 32;
+    const int dpl = s_cap / 32;
+    // 4 source ranges: measured best on B200 (C4: 2.8e6 sel/s vs 2.65e6 with 8 -- the per-position merge of
+    // NW partials and the per-warp fixed costs outgrow the shorter relax loops)
+    const int nw = 4;
     SlotArgs A{};
     A.meta = meta;
     A.meta_stride = meta_stride;
     A.stream = stream;
     A.stream_stride = stream_stride;
-    A.s_cap = s_cap;
     A.s_rows = s_rows;
-    A.w = s_rows | 1;
-    A.nbuf = g_nbuf;
-    A.stage_bytes = g_stage_bytes;
+    A.w = s_rows | 1;                                   // odd row pitch: column writes are conflict-free
     MetaLayout ml{D.max_layers - 1, s_cap, D.max_gpus};
     A.meta_bytes = ml.bytes();
-    int o = 0;
-    A.off_T = o;       o += align_up(s_rows * A.w * 8, 128);
-    A.off_stage = o;   o += A.nbuf * A.stage_bytes;
-    A.off_full = o;    o += 64;
-    A.off_empty = o;   o += 64;
-    A.off_meta = o;    o += align_up(A.meta_bytes, 16);
-    A.off_cost = o;    o += 2 * s_cap * 8;
-    A.off_bp = o;      o += align_up(D.max_layers * s_cap, 16);
-    A.off_picks = o;   o += align_up(D.max_layers * 4, 16);
-    A.off_tau = o;     o += D.max_gpus * 8;
-    A.off_occ = o;     o += D.max_gpus * 4;
-    A.off_stamp = o;   o += D.max_gpus * 4;
-    A.off_slotgpu = o; o += s_cap * 4;
-    A.off_red = o;     o += align_up(cw * 16, 16);
-    A.off_misc = o;    o += 64;
-    A.total = o;
+    auto layout = [&](int nbuf, int stage) {
+        A.nbuf = nbuf;
+        A.stage_bytes = stage;
+        int o = 0;
+        A.off_T = o;       o += align_up((s_rows * A.w + s_cap) * 8, 128);
+        A.off_stage = o;   o += A.nbuf * A.stage_bytes;
+        A.off_full = o;    o += 64;
+        A.off_empty = o;   o += 64;
+        A.off_meta = o;    o += align_up(A.meta_bytes, 16);
+        A.off_part = o;    o += 2 * nw * s_cap * 10;
+        A.off_bp = o;      o += align_up(D.max_layers * s_cap, 16);
+        A.off_picks = o;   o += align_up(D.max_layers * 4, 16);
+        A.off_tau = o;     o += align_up(D.max_gpus * 8, 16);
+        A.off_occ = o;     o += align_up(D.max_gpus * 4, 16);
+        A.off_stamp = o;   o += align_up(D.max_gpus * 4, 16);
+        A.off_slotgpu = o; o += s_cap * 4;
+        A.off_cl = o;      o += align_up(D.max_layers * 4, 16);
+        A.off_red = o;     o += align_up(nw * 12, 16);
+        A.off_misc = o;    o += 64;
+        A.off_base = o;    o += align_up(D.max_gpus * 8, 16);
+        A.pow_len = occpow_len < 256 ? occpow_len : 256;
+        A.off_pow = o;     o += align_up(A.pow_len * 8, 16);
+        A.off_rel = o;     o += align_up((D.max_layers + 1) * 4, 16);
+        A.off_coff = o;    o += align_up(D.max_layers * 4, 16);
+        A.off_costw = o;   o += nw * 32 * 8;
+        A.total = o;
+    };
+    // two CTAs per SM when the staging ring can shrink to fit (>= 2 buffers of >= one unit);
+    // otherwise one CTA with the configured ring
+    const int unit_min = align_up((s_rows + 1) * 8, 128);
+    const int stage_cfg = max(g_stage_bytes, unit_min);
+    const int two_cta = kSmemPerSM / 2 - kSmemPerCtaReserved;
+    layout(0, 0);
+    const int rest = A.total;
+    int nb = g_nbuf, st_b = stage_cfg;
+    while (nb > 2 && rest + nb * st_b > two_cta) --nb;
+    if (rest + nb * st_b > two_cta) st_b = ((two_cta - rest) / 2) / 128 * 128;
+    if (st_b >= unit_min) layout(nb, st_b);
+    else layout(g_nbuf, stage_cfg);
     if (A.total > 227 * 1024) return SS_BAD_INPUT;
     ReplayArgs R{};
     R.st = *st;
@@ -561,22 +703,38 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
     R.n_req = n_req;
     cudaStream_t s = ss_stream(stream_h);
     if (R.out.chain_hash) cudaMemsetAsync(R.out.chain_hash, 0, sizeof(uint64_t) * (size_t)D.n_dags * n_req, s);
+    const bool prof = getenv("SS_SLOT_PROF") != nullptr;
+    if (prof && cudaMalloc(&A.prof, 64 * 8 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(A.prof, 0, 64 * 8 * sizeof(unsigned long long), s);
     auto run = [&](auto kern, int threads) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
             return SS_CUDA_ERROR;
         kern<<<D.n_dags, threads, A.total, s>>>(D, A, R);
         SS_CHECK_LAUNCH();
+        if (A.prof) {
+            unsigned long long h[64 * 8];
+            cudaMemcpyAsync(h, A.prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "slot prof: smem=%d nbuf=%d stage=%d s_rows=%d | per CTA-request cycles, by warp:\n",
+                    A.total, A.nbuf, A.stage_bytes, A.s_rows);
+            for (int w = 0; w < 9; ++w) {
+                const double d = (double)D.n_dags * n_req;
+                fprintf(stderr, "  w%d prologue %.0f relax %.0f apply %.0f barrier %.0f epilogue %.0f\n", w,
+                        h[w * 8 + 0] / d, h[w * 8 + 1] / d, h[w * 8 + 2] / d, h[w * 8 + 3] / d, h[w * 8 + 4] / d);
+            }
+            cudaFree(A.prof);
+        }
         return SS_OK;
     };
-    switch (cw) {
-        case 1: return run(replay_slots_kernel<1>, 64);
-        case 2: return run(replay_slots_kernel<2>, 96);
-        case 3: return run(replay_slots_kernel<3>, 128);
-        case 4: return run(replay_slots_kernel<4>, 160);
-        case 5: return run(replay_slots_kernel<5>, 192);
-        case 6: return run(replay_slots_kernel<6>, 224);
-        case 7: return run(replay_slots_kernel<7>, 256);
-        default: return run(replay_slots_kernel<8>, 288);
+    switch (dpl) {
+        case 1: return run(replay_slots_kernel<1, 4>, 5 * 32);
+        case 2: return run(replay_slots_kernel<2, 4>, 5 * 32);
+        case 3: return run(replay_slots_kernel<3, 4>, 5 * 32);
+        case 4: return run(replay_slots_kernel<4, 4>, 5 * 32);
+        case 5: return run(replay_slots_kernel<5, 4>, 5 * 32);
+        case 6: return run(replay_slots_kernel<6, 4>, 5 * 32);
+        case 7: return run(replay_slots_kernel<7, 4>, 5 * 32);
+        default: return run(replay_slots_kernel<8, 4>, 5 * 32);
     }
 }
 
