@@ -292,7 +292,9 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     double* pow_s = reinterpret_cast<double*>(smem + A.off_pow);     // occpow[0 .. pow_len)
     int* rel = reinterpret_cast<int*>(smem + A.off_rel);             // prefetched ring slot of the next release
     int* coff = reinterpret_cast<int*>(smem + A.off_coff);           // this DAG's column offsets
-    double* cost_w = reinterpret_cast<double*>(smem + A.off_costw);  // [NW][32] each warp's source costs
+    constexpr int CW_LEN = SC / NW + 8;                               // >= ceil(SC / NW) + 3, multiple of 4
+    double* cost_w = reinterpret_cast<double*>(smem + A.off_costw);  // [NW][CW_LEN] each warp's source costs
+    int* row_w = reinterpret_cast<int*>(cost_w + NW * CW_LEN);        // [NW][CW_LEN] their T row byte offsets
 
     // ---- setup ---------------------------------------------------------------
     const uint8_t* meta_g = A.meta + (int64_t)dag * A.meta_stride;
@@ -424,25 +426,36 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         }
         for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
     };
-    // merge for column c (1..nblk): cost of this warp's positions + backpointers of boundary c-1.
-    // Lane k holds position p0+k; returns its cost (INF past the range) and slot.
-    auto merge = [&](int c, int p0, int n, int& sl) -> double {
-        double cst = INF;
-        sl = 0;
-        if (lane < n) {
-            const int p = p0 + lane;
-            sl = src_map[c * SC + p];
-            const double* pv = part_v + ((c - 1) & 1) * NW * SC;
-            const int16_t* pi = part_i + ((c - 1) & 1) * NW * SC;
-            double v = pv[sl];
-            int i = pi[sl];
+    // Costs of this warp's positions [p0, p0+n) of column c into cw[], their T row byte offsets into rw[]
+    // (padded with +inf / row 0 to a multiple of 4).  c == 0: tau of the first layer's hosts; c >= 1: the
+    // lexicographic (value, position) min over the NW range partials of boundary c-1 (== numpy first-index
+    // argmin) + tau, recording the backpointers of boundary c-1.
+    auto stage_sources = [&](int c, int p0, int n, double* cw, int* rw) {
+        const int n4 = (n + 3) & ~3;
+        for (int q = lane; q < n4; q += 32) {
+            double cst = INF;
+            int sl = 0;
+            if (q < n) {
+                const int p = p0 + q;
+                sl = src_map[c * SC + p];
+                if (c == 0) {
+                    cst = tau_g[slot_gpu[sl]];
+                } else {
+                    const double* pv = part_v + ((c - 1) & 1) * NW * SC;
+                    const int16_t* pi = part_i + ((c - 1) & 1) * NW * SC;
+                    double v = pv[sl];
+                    int i = pi[sl];
 #pragma unroll
-            for (int w = 1; w < NW; ++w) lex_min(v, i, pv[w * SC + sl], (int)pi[w * SC + sl]);
-            if (i == PART_NONE) i = 0;                          // np.argmin of an all-inf column
-            cst = __dadd_rn(v, tau_g[slot_gpu[sl]]);
-            bp[(c - 1) * SC + p] = (uint8_t)i;
+                    for (int w = 1; w < NW; ++w) lex_min(v, i, pv[w * SC + sl], (int)pi[w * SC + sl]);
+                    if (i == PART_NONE) i = 0;                  // np.argmin of an all-inf column
+                    cst = __dadd_rn(v, tau_g[slot_gpu[sl]]);
+                    bp[(c - 1) * SC + p] = (uint8_t)i;
+                }
+            }
+            cw[q] = cst;
+            rw[q] = sl * W * 8;
         }
-        return cst;
+        __syncwarp();
     };
     int done = 0;
     consumer_sync(NC);
@@ -490,30 +503,28 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         if (misc[0] != SS_OK) { drain(); break; }
 
         SS_PROF(0)
+        double* cw = cost_w + warp * CW_LEN;
+        int* rw = row_w + warp * CW_LEN;
         for (int b = 0; b < nblk; ++b) {
             const int rs = col_len[b];
             const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
-            int sl;
-            double cst;
-            if (b == 0) {
-                sl = lane < n ? src_map[p0 + lane] : 0;
-                cst = lane < n ? tau_g[slot_gpu[sl]] : INF;
-            } else {
-                cst = merge(b, p0, n, sl);
-            }
-            // this warp's source costs -> shared (broadcast reads in the loop; only this warp touches them)
-            double* cw = cost_w + warp * 32;
-            cw[lane] = cst;
-            __syncwarp();
-            const uint8_t* sb = src_map + b * SC + p0;
-            // ---- relax boundary b over this warp's sources ------------------------
+            stage_sources(b, p0, n, cw, rw);
+            // ---- relax boundary b over this warp's sources (4 per step: 2x LDS.128 cost, 1x LDS.128 rows) --
             double v[DPL];
             int ix[DPL];
 #pragma unroll
             for (int d = 0; d < DPL; ++d) { v[d] = INF; ix[d] = PART_NONE; }
-            const double* Tl = T + lane;
-#pragma unroll 4
-            for (int k = 0; k < n; ++k) relax_row<DPL>(Tl + sb[k] * W, cw[k], p0 + k, v, ix);
+            const char* Tb = reinterpret_cast<const char*>(T + lane);
+#pragma unroll 2
+            for (int k = 0; k < n; k += 4) {
+                const double2 c01 = *reinterpret_cast<const double2*>(cw + k);
+                const double2 c23 = *reinterpret_cast<const double2*>(cw + k + 2);
+                const int4 r4 = *reinterpret_cast<const int4*>(rw + k);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.x), c01.x, p0 + k, v, ix);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.y), c01.y, p0 + k + 1, v, ix);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.z), c23.x, p0 + k + 2, v, ix);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.w), c23.y, p0 + k + 3, v, ix);
+            }
             __syncwarp();
             {
                 double* pv = part_v + (b & 1) * NW * SC + warp * SC;
@@ -535,9 +546,10 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         {
             const int rs = col_len[nblk];
             const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
-            int sl;
-            double v = merge(nblk, p0, n, sl);
-            int idx = lane < n ? p0 + lane : IDX_NONE;
+            stage_sources(nblk, p0, n, cw, rw);
+            double v = INF;
+            int idx = IDX_NONE;
+            for (int q = lane; q < n; q += 32) lex_min(v, idx, cw[q], p0 + q);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
@@ -678,7 +690,7 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
         A.off_pow = o;     o += align_up(A.pow_len * 8, 16);
         A.off_rel = o;     o += align_up((D.max_layers + 1) * 4, 16);
         A.off_coff = o;    o += align_up(D.max_layers * 4, 16);
-        A.off_costw = o;   o += nw * 32 * 8;
+        A.off_costw = o;   o += nw * (s_cap / nw + 8) * 12;
         A.total = o;
     };
     // two CTAs per SM when the staging ring can shrink to fit (>= 2 buffers of >= one unit);
