@@ -44,15 +44,13 @@ class ReplayResult:
 
 class ScenarioReplayer:
     def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
-                 max_requests: Optional[int] = None, stream=None, mode: str = "slots"):
+                 max_requests: Optional[int] = None, stream=None, mode: str = "auto"):
         """mode "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
-        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay).  Bit-identical results."""
+        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "auto": slots while the tile
+        leaves room for two CTAs per SM (<= 96 slots), else blocks.  All modes give bit-identical results."""
         import torch
-        if mode not in ("slots", "blocks"):
-            raise ValueError(f"mode must be 'slots' or 'blocks', got {mode!r}")
-        if scen.layer_count < 2:
-            mode = "blocks"                      # no boundaries: nothing to tile
-        self.mode = mode
+        if mode not in ("slots", "blocks", "auto"):
+            raise ValueError(f"mode must be 'slots', 'blocks' or 'auto', got {mode!r}")
         self.torch = torch
         self.scen = scen
         self.window = int(window)
@@ -63,6 +61,16 @@ class ScenarioReplayer:
         self.S, self.G, self.L = S, G, L
         lo, hi = scen.slice_lo.astype(np.int64), scen.slice_hi.astype(np.int64)
         layers = np.arange(1, L + 1)
+        # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
+        # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
+        held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
+            if L > 1 else np.zeros(1, dtype=np.int64)
+        s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
+        if mode == "auto":
+            mode = "slots" if s_cap <= 96 else "blocks"
+        if L < 2:
+            mode = "blocks"                      # no boundaries: nothing to tile
+        self.mode = mode
         cap = ((lo[None, :] <= layers[:, None]) & (hi[None, :] >= layers[:, None])).sum(axis=1)
         if (cap == 0).any():
             raise ValueError("base plan leaves a layer uncovered")
@@ -94,11 +102,9 @@ class ScenarioReplayer:
             self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
         else:
             self.edge_val = None
-            # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
-            # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
-            held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
-                if L > 1 else np.zeros(1, dtype=np.int64)
-            self.s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
+            if s_cap > 256:
+                raise ValueError(f"slot mode supports <= 256 frontier slots, this plan needs {int(held.max())}")
+            self.s_cap = s_cap
             n_plan = int(((hi >= lo) & (hi >= 1)).sum())
             lib = N.load_library()
             self.meta_stride = int(lib.ss_slot_meta_bytes(L, G, self.s_cap))

@@ -207,3 +207,39 @@ def test_uncovered_scenario_reports_status(cuda_ready, mode):
     with pytest.raises(UncoveredLayer):
         rp.raise_first_failure()
     assert first_gpu >= 0
+
+
+@pytest.mark.parametrize("mode", ["slots", "blocks"])
+def test_replay_wide_columns_vs_oracle(cuda_ready, mode):
+    """k = 129 hosts per layer: every slot-replay warp owns > 32 source positions (multi-pass staging)."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from oracle import alloc_ref
+    cl, model = scen.synthetic_cluster(144, seed=0, model=scen.bench_model(10))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    assert plan.replication_count == 129
+    ss = scen.build_scenarios(cl, model, plan, 3, seed0=404, churn=0.05, jitter=True)
+    rp = ScenarioReplayer(ss, window=8, max_requests=32, mode=mode)
+    assert rp.mode == mode
+    out = rp.run(24, gpus=True)
+    rp.raise_first_failure()
+    for s in range(3):
+        want_g, want_c, want_occ, _ = chain_ref.replay(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), 24, 8,
+                                                       chain_ref.occ_power_table(32))
+        assert out.gpus.cpu().numpy()[s].tolist() == want_g, s
+        assert out.cost.cpu().numpy()[s].tolist() == want_c, s
+        assert rp.occ.view(3, -1)[s].cpu().numpy().tolist() == want_occ.tolist(), s
+
+
+def test_replay_auto_mode_picks_blocks_for_wide_frontiers(cuda_ready):
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from oracle import alloc_ref
+    cl, model = scen.synthetic_cluster(144, seed=0, model=scen.bench_model(10))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
+    assert ScenarioReplayer(ss, window=8).mode == "blocks"
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
+    assert ScenarioReplayer(ss, window=8).mode == "slots"
