@@ -129,6 +129,17 @@ typedef struct ss_replay_out {
 int ss_replay(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
               int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
 
+/* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
+ * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring
+ * and state staged in shared memory once per launch; no CTA barriers on the
+ * request path.  Same state / outputs / op script as ss_replay (ring entries
+ * of a chain are stored in layer order).  ss_replay_warp_smem returns the
+ * dynamic shared memory one scenario needs, or -1 when the DAG set does not
+ * qualify (hosts > 32, or edges + ring exceed 227 KB). */
+int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len);
+int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
+                   int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Phase-1                                      */
 /* ------------------------------------------------------------------------ */

@@ -42,15 +42,48 @@ class ReplayResult:
     status: object                # torch int32 [S]
 
 
+def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int], mode: str):
+    """(kernel mode, hosts per layer of the base plan, slot capacity, occpow table length)."""
+    L = scen.layer_count
+    lo, hi = scen.slice_lo.astype(np.int64), scen.slice_hi.astype(np.int64)
+    layers = np.arange(1, L + 1)
+    cap = ((lo[None, :] <= layers[:, None]) & (hi[None, :] >= layers[:, None])).sum(axis=1)
+    if (cap == 0).any():
+        raise ValueError("base plan leaves a layer uncovered")
+    # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
+    # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
+    held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
+        if L > 1 else np.zeros(1, dtype=np.int64)
+    s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
+    occ_len = window + 2 if window > 0 else (max_requests or 1 << 16) + 2
+    probe = N.DagSet(scen.n_scenarios, int(cap.max()), L, scen.n_gpus, None, None, None, None, None, None, None)
+    warp_ok = int(cap.max()) <= 32 and int(N.load_library().ss_replay_warp_smem(probe, window, occ_len)) > 0
+    if mode == "auto":
+        mode = "warp" if warp_ok else ("slots" if s_cap <= 96 else "blocks")
+    if mode == "warp" and not warp_ok:
+        raise ValueError("warp mode needs <= 32 hosts per layer and edges + ring within 227 KB of shared memory")
+    if L < 2 and mode == "slots":
+        mode = "blocks"                      # no boundaries: nothing to tile
+    return mode, cap, s_cap, occ_len
+
+
+def replay_mode(scen: ScenarioSet, *, window: int = 64, max_requests: Optional[int] = None,
+                mode: str = "auto") -> str:
+    """The replay kernel ScenarioReplayer would use for these scenarios (no GPU needed)."""
+    return _replay_geometry(scen, int(window), max_requests, mode)[0]
+
+
 class ScenarioReplayer:
     def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
                  max_requests: Optional[int] = None, stream=None, mode: str = "auto"):
         """mode "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
-        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "auto": slots while the tile
-        leaves room for two CTAs per SM (<= 96 slots), else blocks.  All modes give bit-identical results."""
+        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "warp": one warp per scenario
+        with its edge blocks resident in shared memory (ss_replay_warp; columns <= 32 hosts); "auto":
+        warp when it qualifies, else slots while the tile leaves room for two CTAs per SM (<= 96 slots),
+        else blocks.  All modes give bit-identical results."""
         import torch
-        if mode not in ("slots", "blocks", "auto"):
-            raise ValueError(f"mode must be 'slots', 'blocks' or 'auto', got {mode!r}")
+        if mode not in ("slots", "blocks", "warp", "auto"):
+            raise ValueError(f"mode must be 'slots', 'blocks', 'warp' or 'auto', got {mode!r}")
         self.torch = torch
         self.scen = scen
         self.window = int(window)
@@ -61,19 +94,8 @@ class ScenarioReplayer:
         self.S, self.G, self.L = S, G, L
         lo, hi = scen.slice_lo.astype(np.int64), scen.slice_hi.astype(np.int64)
         layers = np.arange(1, L + 1)
-        # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
-        # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
-        held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
-            if L > 1 else np.zeros(1, dtype=np.int64)
-        s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
-        if mode == "auto":
-            mode = "slots" if s_cap <= 96 else "blocks"
-        if L < 2:
-            mode = "blocks"                      # no boundaries: nothing to tile
+        mode, cap, s_cap, occ_len = _replay_geometry(scen, self.window, max_requests, mode)
         self.mode = mode
-        cap = ((lo[None, :] <= layers[:, None]) & (hi[None, :] >= layers[:, None])).sum(axis=1)
-        if (cap == 0).any():
-            raise ValueError("base plan leaves a layer uncovered")
         self.cap = cap
         cap_nodes = int(cap.sum())
         node_pre = np.concatenate([[0], np.cumsum(cap)[:-1]])
@@ -98,12 +120,12 @@ class ScenarioReplayer:
         self.gpu_ptr = up(gpu_ptr, t32)
         self.col_len = torch.empty(S * L, dtype=t32, device=dev)
         self.node_gpu = torch.empty(S * cap_nodes, dtype=t32, device=dev)
-        if mode == "blocks":
+        if mode in ("blocks", "warp"):
             self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
         else:
             self.edge_val = None
             if s_cap > 256:
-                raise ValueError(f"slot mode supports <= 256 frontier slots, this plan needs {int(held.max())}")
+                raise ValueError(f"slot mode supports <= 256 frontier slots, this plan needs {s_cap}")
             self.s_cap = s_cap
             n_plan = int(((hi >= lo) & (hi >= 1)).sum())
             lib = N.load_library()
@@ -125,10 +147,7 @@ class ScenarioReplayer:
         self.next_req = torch.zeros(S, dtype=t64, device=dev)
         self.status = torch.zeros(S, dtype=t32, device=dev)
         self.aux = torch.zeros(S, dtype=t32, device=dev)
-        if self.window > 0:
-            size = self.window + 2
-        else:
-            size = (max_requests or 1 << 16) + 2
+        size = occ_len
         self.occpow_len = size
         self.occpow = up(occ_power_table(size, exponent), f64)
         self.max_hosts = int(cap.max())
@@ -197,6 +216,9 @@ class ScenarioReplayer:
                                             self.stream_stride, self.s_cap, self.s_rows, st, N.ptr(self.occpow),
                                             self.occpow_len, self.window, n_req, ro, N.stream_handle(self.stream)),
                     "ss_replay_slots")
+        elif self.mode == "warp":
+            N.check(N.lib().ss_replay_warp(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window,
+                                           n_req, ro, N.stream_handle(self.stream)), "ss_replay_warp")
         else:
             N.check(N.lib().ss_replay(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window, n_req,
                                       ro, N.stream_handle(self.stream)), "ss_replay")

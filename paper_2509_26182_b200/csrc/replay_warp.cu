@@ -1,0 +1,344 @@
+// Warp-resident replay: Phase-2 route / release(i - W) for DAGs whose layer
+// columns hold <= 32 hosts (C1 / C2 shapes).
+//
+// One warp owns one scenario for the whole launch.  Its edge blocks, host
+// columns, occupancy, release ring and backpointers are copied into shared
+// memory once; every request then runs without a single CTA barrier:
+//   * boundary b: lane j forms the candidates c_i + E_b[i][j] eight sources at a
+//     time (column costs broadcast from shared memory, independent loads and
+//     DADDs), then a tournament whose left operand always holds the lower source
+//     index and loses only to a strictly smaller right value == numpy first-index argmin
+//     (router.py:171); cost = (c_i + r_ij) + tau_j exactly (router.py:170-174);
+//   * load update as perfmap.py:353-382 with tau = base(g) * (1 + occ)^e
+//     (sim.py:182-183) and the distinct GPUs of each chain kept in the ring.
+// Latency per boundary: ceil(R_b / 8) groups of (loads, DADDs, 3-level tournament).
+#include <float.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "ss_common.cuh"
+
+namespace {
+
+constexpr int NONE = 0x7fffffff;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct WarpLayout {
+    int e_cap, ring_len, pow_len;
+    int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
+        off_ring, off_pow, off_cost, total;
+};
+
+struct WarpReplay {
+    ss_replay_state st;
+    ss_replay_out out;
+    const double* occpow;
+    int32_t occpow_len;
+    int32_t window;
+    int32_t n_req;
+    unsigned long long* prof;   // diagnostics (env SS_WARP_PROF=1): cycles per phase, else NULL
+};
+
+__device__ __forceinline__ void lexmin(double& v, int& i, double v2, int i2) {
+    if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+
+__global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int dag = blockIdx.x;
+    const int lane = threadIdx.x;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    if (R.st.status[dag] != SS_OK) return;                      // sticky failure: skip
+    const int l0 = D.layer_ptr[dag];
+    const int nl = D.layer_ptr[dag + 1] - l0;
+    const int nblk = nl - 1;
+    double* E = reinterpret_cast<double*>(smem + A.off_E);
+    int* node = reinterpret_cast<int*>(smem + A.off_node);
+    int* cl = reinterpret_cast<int*>(smem + A.off_cl);
+    int* noff = reinterpret_cast<int*>(smem + A.off_noff);
+    int* eoff = reinterpret_cast<int*>(smem + A.off_eoff);
+    uint8_t* bp = smem + A.off_bp;
+    int* picks = reinterpret_cast<int*>(smem + A.off_picks);
+    double* tau = reinterpret_cast<double*>(smem + A.off_tau);
+    double* base = reinterpret_cast<double*>(smem + A.off_base);
+    int* occ = reinterpret_cast<int*>(smem + A.off_occ);
+    int* stamp = reinterpret_cast<int*>(smem + A.off_stamp);
+    int* ring = reinterpret_cast<int*>(smem + A.off_ring);
+    double* pw = reinterpret_cast<double*>(smem + A.off_pow);
+    double* costs = reinterpret_cast<double*>(smem + A.off_cost);   // [2][40] column costs (32 hosts + 8 pad)
+
+    // ---- one-time staging: columns, edges, per-GPU state, ring --------------
+    for (int l = lane; l < nl; l += 32) cl[l] = D.col_len[l0 + l];
+    __syncwarp();
+    if (lane == 0) {
+        int n = 0, e = 0, bad = 0;
+        for (int l = 0; l < nl; ++l) {
+            if (cl[l] > 32) bad = 1;
+            noff[l] = n;
+            n += cl[l];
+            if (l < nblk) {
+                eoff[l] = e;
+                e += cl[l] * cl[l + 1];
+            }
+        }
+        if (e > A.e_cap) bad = 1;
+        cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
+    }
+    __syncwarp();
+    if (cl[nl]) {
+        if (lane == 0) R.st.status[dag] = SS_BAD_INPUT;
+        return;
+    }
+    for (int l = 0; l < nl; ++l) {
+        const int len = cl[l];
+        if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
+        if (l < nblk) {
+            const double* src = D.edge_val + D.edge_off[l0 + l];
+            const int cnt = len * cl[l + 1];
+            for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
+        }
+    }
+    const int gbase = R.st.gpu_ptr[dag];
+    const int ng = R.st.gpu_ptr[dag + 1] - gbase;
+    const int window = R.window;
+    const int ring_stride = D.max_layers + 1;
+    int* ring_g = R.st.ring + (int64_t)dag * (window > 0 ? window : 1) * ring_stride;
+    for (int g = lane; g < ng; g += 32) {
+        occ[g] = R.st.occ[gbase + g];
+        base[g] = R.st.base_tau[gbase + g];
+        stamp[g] = 0;
+    }
+    for (int o = lane; o < A.pow_len; o += 32) pw[o] = R.occpow[o];
+    for (int q = lane; q < A.ring_len; q += 32) ring[q] = ring_g[q];
+    if (lane < 8) { costs[32 + lane] = INF; costs[72 + lane] = INF; }
+    __syncwarp();
+
+    const int n_req = R.n_req;
+    const int64_t req0 = R.st.next_req[dag];
+    int status = SS_OK, aux = 0, done = 0;
+    unsigned long long pacc[3] = {0, 0, 0};
+    long long tp = clock64();
+    auto mark = [&](int k) {
+        if (R.prof) {
+            const long long t = clock64();
+            pacc[k] += (unsigned long long)(t - tp);
+            tp = t;
+        }
+    };
+    for (int r = 0; r < n_req; ++r) {
+        const int64_t req = req0 + r;
+        mark(2);
+        // ---- release chain req - W, refresh tau(g) ----------------------------
+        if (window > 0 && req >= window) {
+            const int* slot = ring + (int)(req % window) * ring_stride;
+            const int cnt = slot[0];
+            for (int k = lane; k < cnt; k += 32) occ[slot[1 + k]] -= 1;   // distinct GPUs: no collisions
+        }
+        __syncwarp();
+        int err = 0, errg = 0;
+        for (int g = lane; g < ng; g += 32) {
+            const int o = occ[g];
+            if (o < 0 || o >= R.occpow_len) {
+                err = o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT;
+                errg = g;
+            }
+            const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
+            tau[g] = base[g] * (oc < A.pow_len ? pw[oc] : R.occpow[oc]);
+        }
+        const unsigned em = __ballot_sync(FULL, err != 0);
+        if (em) {
+            const int src = __ffs(em) - 1;
+            status = __shfl_sync(FULL, err, src);
+            aux = __shfl_sync(FULL, errg, src);
+            break;
+        }
+        __syncwarp();
+        mark(0);
+        // ---- DP over the layer columns -------------------------------------------
+        double* cur = costs;
+        double* nxt = costs + 40;
+        cur[lane] = lane < cl[0] ? tau[node[lane]] : INF;
+        __syncwarp();
+        double c = cur[lane];
+        for (int b = 0; b < nblk; ++b) {
+            const int rs = cl[b], rd = cl[b + 1];
+            const bool act = lane < rd;
+            const double tdst = act ? tau[node[noff[b + 1] + lane]] : 0.0;
+            const double* ep = E + eoff[b] + lane;
+            // groups of 8 sources: independent loads / DADDs and a first-index tournament per group (left
+            // operand = lower positions, loses only to a strictly smaller right value); groups merged in
+            // ascending order with the same strict rule
+            double best = INF;
+            int bi = 0;                                          // +inf everywhere -> 0 == np.argmin
+            for (int g0 = 0; g0 < rs; g0 += 8) {
+                double a[8];
+                int ix[8];
+#pragma unroll
+                for (int q = 0; q < 8; q += 2) {
+                    const double2 c2 = *reinterpret_cast<const double2*>(cur + g0 + q);
+                    const double e0 = (act && g0 + q < rs) ? ep[q * rd] : INF;
+                    const double e1 = (act && g0 + q + 1 < rs) ? ep[(q + 1) * rd] : INF;
+                    a[q] = __dadd_rn(c2.x, e0);
+                    a[q + 1] = __dadd_rn(c2.y, e1);
+                    ix[q] = g0 + q;
+                    ix[q + 1] = g0 + q + 1;
+                }
+#pragma unroll
+                for (int st = 1; st < 8; st *= 2) {
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2 * st) {
+                        if (a[q + st] < a[q]) { a[q] = a[q + st]; ix[q] = ix[q + st]; }
+                    }
+                }
+                if (a[0] < best) { best = a[0]; bi = ix[0]; }
+                ep += 8 * rd;
+            }
+            if (act) bp[b * 32 + lane] = (uint8_t)bi;
+            c = act ? __dadd_rn(best, tdst) : INF;
+            nxt[lane] = c;
+            __syncwarp();
+            double* t = cur; cur = nxt; nxt = t;
+        }
+        mark(1);
+        // ---- final argmin (first index) + backtrack --------------------------------
+        double v = c;
+        int idx = lane < cl[nblk] ? lane : NONE;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(FULL, v, o);
+            const int i2 = __shfl_xor_sync(FULL, idx, o);
+            lexmin(v, idx, v2, i2);
+        }
+        if (lane == 0) {
+            if (R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
+            if (v <= DBL_MAX) {
+                int p = idx;
+                picks[nblk] = p;
+                for (int b = nblk - 1; b >= 0; --b) {
+                    p = bp[b * 32 + p];
+                    picks[b] = p;
+                }
+            }
+        }
+        if (!(v <= DBL_MAX)) {
+            status = SS_NO_PATH;
+            break;
+        }
+        __syncwarp();
+        // ---- load update: +1 per distinct GPU of the chain, ring, outputs ---------
+        const int tag = (int)(req & 0x3fffffff) + 1;
+        int* slot = window > 0 ? ring + (int)(req % window) * ring_stride : nullptr;
+        uint64_t h = 0;
+        int cnt = 0;
+        for (int l0c = 0; l0c < nl; l0c += 32) {
+            const int l = l0c + lane;
+            int g = 0;
+            bool first = false;
+            if (l < nl) {
+                g = node[noff[l] + picks[l]];
+                h += ss_splitmix64(((uint64_t)l << 32) | (uint64_t)g);
+                if (R.out.gpus) R.out.gpus[((int64_t)dag * n_req + r) * D.max_layers + l] = (int16_t)g;
+                first = atomicExch(&stamp[g], tag) != tag && window != 0;
+            }
+            const unsigned m = __ballot_sync(FULL, first);
+            if (first) {
+                occ[g] += 1;
+                if (slot) slot[1 + cnt + __popc(m & ((1u << lane) - 1u))] = g;
+            }
+            cnt += __popc(m);
+        }
+        if (R.out.chain_hash) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(FULL, h, o);
+            if (lane == 0) R.out.chain_hash[(int64_t)dag * n_req + r] = h;
+        }
+        if (lane == 0 && slot) slot[0] = cnt;
+        __syncwarp();
+        ++done;
+    }
+    __syncwarp();
+    mark(2);
+    if (R.prof && lane == 0)
+        for (int k = 0; k < 3; ++k) atomicAdd(&R.prof[k], pacc[k]);
+    for (int g = lane; g < ng; g += 32) R.st.occ[gbase + g] = occ[g];
+    for (int q = lane; q < A.ring_len; q += 32) ring_g[q] = ring[q];
+    if (lane == 0) {
+        R.st.next_req[dag] = req0 + done;
+        if (status != SS_OK) { R.st.status[dag] = status; R.st.aux[dag] = aux; }
+    }
+}
+
+inline int align16(int x) { return (x + 15) / 16 * 16; }
+
+bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A) {
+    if (D.max_hosts > 32 || D.max_layers < 1) return false;
+    const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * D.max_hosts * D.max_hosts;
+    const int64_t ring_len = window > 0 ? (int64_t)window * (D.max_layers + 1) : 0;
+    if (e_cap > (1 << 20) || ring_len > (1 << 20)) return false;
+    A.e_cap = (int)e_cap;
+    A.ring_len = (int)ring_len;
+    A.pow_len = occpow_len < 256 ? occpow_len : 256;
+    int o = 0;
+    A.off_E = o;      o += align16(A.e_cap * 8);
+    A.off_node = o;   o += align16(D.max_layers * D.max_hosts * 4);
+    A.off_cl = o;     o += align16((D.max_layers + 1) * 4);
+    A.off_noff = o;   o += align16(D.max_layers * 4);
+    A.off_eoff = o;   o += align16(D.max_layers * 4);
+    A.off_bp = o;     o += align16(D.max_layers * 32);
+    A.off_picks = o;  o += align16(D.max_layers * 4);
+    A.off_tau = o;    o += align16(D.max_gpus * 8);
+    A.off_base = o;   o += align16(D.max_gpus * 8);
+    A.off_occ = o;    o += align16(D.max_gpus * 4);
+    A.off_stamp = o;  o += align16(D.max_gpus * 4);
+    A.off_ring = o;   o += align16(A.ring_len * 4);
+    A.off_pow = o;    o += align16(A.pow_len * 8);
+    A.off_cost = o;   o += 2 * 40 * 8;
+    A.total = o;
+    return A.total <= 227 * 1024;
+}
+
+}  // namespace
+
+extern "C" int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len) {
+    if (!dags) return -1;
+    WarpLayout A{};
+    return warp_layout(*dags, window, occpow_len < 1 ? 1 : occpow_len, A) ? A.total : -1;
+}
+
+extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow,
+                              int32_t occpow_len, int32_t window, int32_t n_req, const ss_replay_out* out,
+                              void* stream_h) {
+    if (!dags || !st || !occpow || occpow_len < 1 || n_req < 1) return SS_BAD_INPUT;
+    const ss_dag_set& D = *dags;
+    if (D.n_dags <= 0) return SS_OK;
+    if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
+    WarpLayout A{};
+    if (!warp_layout(D, window, occpow_len, A)) return SS_BAD_INPUT;
+    WarpReplay R{};
+    R.st = *st;
+    if (out) R.out = *out;
+    R.occpow = occpow;
+    R.occpow_len = occpow_len;
+    R.window = window;
+    R.n_req = n_req;
+    cudaStream_t s = ss_stream(stream_h);
+    if (getenv("SS_WARP_PROF") && cudaMalloc(&R.prof, 4 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(R.prof, 0, 4 * sizeof(unsigned long long), s);
+    // One warp per scenario.  Splitting a column's sources over 2-4 warps (one barrier per boundary, each warp
+    // merging its own next positions) measured slower at C2 (27e3 vs 33e3 sel/s): at <= 32 hosts the per-warp
+    // fixed work (partial merge, shuffles, the 8-wide tournament) outweighs the shorter source ranges.
+    if (cudaFuncSetAttribute(replay_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
+        return SS_CUDA_ERROR;
+    replay_warp_kernel<<<D.n_dags, 32, A.total, s>>>(D, A, R);
+    SS_CHECK_LAUNCH();
+    if (R.prof) {
+        unsigned long long h[4];
+        cudaMemcpyAsync(h, R.prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const double d = (double)D.n_dags * n_req;
+        fprintf(stderr, "warp prof: cycles per request: release+tau %.0f  DP %.0f  argmin+update %.0f\n", h[0] / d,
+                h[1] / d, h[2] / d);
+        cudaFree(R.prof);
+    }
+    return SS_OK;
+}

@@ -62,3 +62,33 @@ def test_jitter_vectorised_equals_scalar():
         for j in range(40):
             if i != j:
                 assert m[i, j] == scen.jitter_factor(12345, i, j)
+
+
+def test_replay_mode_selection():
+    """Kernel choice is a pure function of the plan geometry (no GPU needed)."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers_golden import plan_from_golden
+    from oracle import alloc_ref
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import replay_mode
+
+    def plan_for(n, L):
+        cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
+        d = alloc_ref.allocate(cl, model)
+        d["objective"] = d["objective"].hex()
+        d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+        return cl, model, plan_from_golden(d)
+
+    cl, model, plan = plan_for(64, 64)                  # C2: k = 17
+    ss = scen.build_scenarios(cl, model, plan, 2, churn=0.0, jitter=False)
+    assert replay_mode(ss, window=64) == "warp"
+    assert replay_mode(ss, window=64, mode="blocks") == "blocks"
+    cl, model, plan = plan_for(256, 64)                 # C4: k = 73
+    ss = scen.build_scenarios(cl, model, plan, 2, churn=0.0, jitter=False)
+    assert replay_mode(ss, window=64) == "slots"
+    with pytest.raises(ValueError):
+        replay_mode(ss, window=64, mode="warp")
+    cl, model, plan = plan_for(144, 10)                 # k = 129: tile too wide for 2 CTAs/SM
+    ss = scen.build_scenarios(cl, model, plan, 2, churn=0.0, jitter=False)
+    assert replay_mode(ss, window=64) == "blocks"

@@ -99,10 +99,15 @@ def _replayer_for_golden(rep, plan_dict, n_scen=1, seed0=None, mode="slots"):
     else:
         ss = scen.build_scenarios(cl, model, plan, n_scen, churn=0.0, jitter=False)
     W = rep["window"]
+    if mode == "warp" and int(ss.slice_hi.max()) > 0:
+        layers = np.arange(1, L + 1)
+        hosts = ((ss.slice_lo[None, :] <= layers[:, None]) & (ss.slice_hi[None, :] >= layers[:, None])).sum(axis=1)
+        if hosts.max() > 32:
+            pytest.skip("warp replay needs <= 32 hosts per layer")
     return ss, ScenarioReplayer(ss, window=-1 if W is None else W, max_requests=len(rep["routes"]) + 4, mode=mode)
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks"])
+@pytest.mark.parametrize("mode", ["slots", "blocks", "warp"])
 @pytest.mark.parametrize("name", ["c1", "c1_tie", "n32_tie", "rt16", "c2", "c4_s11", "c4_s12"])
 def test_replay_kernel_golden(cuda_ready, router_replays, name, mode):
     """ss_replay / ss_replay_slots (on-device load update) == reference ChainRouter op script, bit-exact."""
@@ -161,7 +166,7 @@ def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
             assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks"])
+@pytest.mark.parametrize("mode", ["slots", "blocks", "warp"])
 def test_replay_tie_pool_vs_oracle(cuda_ready, mode):
     """Homogeneous flops => many exact ties (13-23% of columns): first-index rule must hold."""
     from paper_2509_26182_b200 import scenarios as scen
@@ -188,7 +193,7 @@ def _plan_dict(d):
     return d
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks"])
+@pytest.mark.parametrize("mode", ["slots", "blocks", "warp"])
 def test_uncovered_scenario_reports_status(cuda_ready, mode):
     from paper_2509_26182_b200 import scenarios as scen
     from paper_2509_26182_b200.batched import ScenarioReplayer
@@ -242,4 +247,33 @@ def test_replay_auto_mode_picks_blocks_for_wide_frontiers(cuda_ready):
     cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
     plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
     ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
-    assert ScenarioReplayer(ss, window=8).mode == "slots"
+    assert ScenarioReplayer(ss, window=8).mode == "warp"
+
+
+@pytest.mark.parametrize("window", [64, 0, -1, 1, 7])
+def test_warp_replay_c2_shape_vs_oracle(cuda_ready, window):
+    """Warp-resident replay on C2-shaped scenarios (L64/N64 pool, k=17, churn + jitter) vs the oracle."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from oracle import alloc_ref
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    S, n_req = 6, 40
+    ss = scen.build_scenarios(cl, model, plan, S, seed0=300 + window, churn=0.05, jitter=True)
+    rp = ScenarioReplayer(ss, window=window, max_requests=n_req + 4)
+    assert rp.mode == "warp"
+    a = rp.run(n_req // 2, gpus=True)
+    b = rp.run(n_req - n_req // 2, gpus=True)
+    rp.raise_first_failure()
+    gpus = np.concatenate([a.gpus.cpu().numpy(), b.gpus.cpu().numpy()], axis=1)
+    cost = np.concatenate([a.cost.cpu().numpy(), b.cost.cpu().numpy()], axis=1)
+    hashes = np.concatenate([a.chain_hash.cpu().numpy(), b.chain_hash.cpu().numpy()], axis=1)
+    W = None if window < 0 else window
+    for s in range(S):
+        want_g, want_c, want_occ, _ = chain_ref.replay(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), n_req, W,
+                                                       chain_ref.occ_power_table(n_req + 4))
+        assert gpus[s].tolist() == want_g, s
+        assert cost[s].tolist() == want_c, s
+        assert rp.occ.view(S, -1)[s].cpu().numpy().tolist() == want_occ.tolist(), s
+        for r in range(n_req):
+            assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
