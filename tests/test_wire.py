@@ -1,0 +1,70 @@
+"""Wire formats against the reference's own JSON text (tests/golden/wire_cases.json).
+
+CPU: plan JSON round trip (load -> save reproduces the reference text byte for byte).
+GPU: device allocate -> save_plan text, and device replay -> chains_from_replay -> chains_to_json, equal to the
+reference's ``swarmsched route --json`` output for the same pool.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def wire_cases():
+    with open(os.path.join(HERE, "golden", "wire_cases.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_plan_json_round_trip(tmp_path, wire_cases, name):
+    from paper_2509_26182_b200.wire import load_plan, save_plan
+    src = tmp_path / "ref.json"
+    src.write_text(wire_cases[name]["plan_json"])
+    plan = load_plan(str(src))
+    dst = tmp_path / "ours.json"
+    save_plan(plan, str(dst))
+    assert dst.read_text() == wire_cases[name]["plan_json"]
+
+
+def test_load_plan_rejects_malformed(tmp_path):
+    from paper_2509_26182_b200.wire import load_plan
+    p = tmp_path / "bad.json"
+    p.write_text('{"k": 1}')
+    with pytest.raises(ValueError, match="not a valid plan file"):
+        load_plan(str(p))
+
+
+def test_chains_from_replay_merges_hops():
+    from paper_2509_26182_b200.wire import chains_from_replay, chains_to_json
+    ids = ["a", "b", "c"]
+    chains = chains_from_replay(ids, np.array([[0, 0, 1, 1, 0], [2, 2, 2, 2, 2]]), np.array([1.5, 0.25]))
+    assert [(h.gpu_id, h.start_layer, h.end_layer) for h in chains[0].hops] == [("a", 1, 2), ("b", 3, 4), ("a", 5, 5)]
+    assert [(h.gpu_id, h.start_layer, h.end_layer) for h in chains[1].hops] == [("c", 1, 5)]
+    payload = json.loads(chains_to_json(chains))
+    assert payload["chains"][0]["cost_s"] == 1.5 and payload["chains"][1]["hops"][0]["gpu_id"] == "c"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_device_path_reproduces_reference_json(cuda_ready, tmp_path, wire_cases, name):
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.wire import chains_from_replay, chains_to_json, save_plan
+    c = wire_cases[name]
+    cl, model = scen.synthetic_cluster(c["n"], seed=c["seed"], model=scen.bench_model(c["L"]))
+    plan = allocate(cl, model)
+    out = tmp_path / "plan.json"
+    save_plan(plan, str(out))
+    assert out.read_text() == c["plan_json"]
+    ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
+    for mode in ("warp", "slots", "blocks"):
+        rp = ScenarioReplayer(ss, window=-1, max_requests=c["requests"] + 4, mode=mode)
+        res = rp.run(c["requests"], gpus=True)
+        rp.raise_first_failure()
+        chains = chains_from_replay(ss.ids, res.gpus.cpu().numpy()[0], res.cost.cpu().numpy()[0])
+        assert chains_to_json(chains) + "\n" == c["route_json"], mode
