@@ -85,3 +85,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) __nanosleep(64);
 }
+
+// ---------------------------------------------------------------------------
+// CPython 3.12 sum() over int / float items, start = 0
+// ---------------------------------------------------------------------------
+struct PySum {   // SURVEY.md hazard H2; modelled by oracle/waterfill_ref.py:cpython_sum_model
+    bool is_int;
+    long long iacc;
+    double f, c;
+    __device__ void init() { is_int = true; iacc = 0; f = 0.0; c = 0.0; }
+    __device__ void add_int(long long v) {
+        if (is_int) iacc += v;
+        else f = __dadd_rn(f, (double)v);
+    }
+    __device__ void add_float(double x) {
+        if (is_int) {           // int accumulator meets its first float: plain add, compensation starts
+            f = __dadd_rn((double)iacc, x);
+            c = 0.0;
+            is_int = false;
+            return;
+        }
+        const double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        f = t;
+    }
+    __device__ double value() const {
+        if (is_int) return (double)iacc;
+        double r = f;
+        if (c != 0.0 && isfinite(c)) r = __dadd_rn(r, c);
+        return r;
+    }
+};
+
+

@@ -130,6 +130,60 @@ def churn_set(seed: int, plan_gpus: Sequence[int], slices: Dict[int, Tuple[int, 
     return sorted(out)
 
 
+LEAVE_SALT = 0xC4 << 40
+JOIN_SALT = 0x4A << 40
+
+
+def join_order(seed: int, candidates: Sequence[int]) -> List[int]:
+    """Seeded order in which absent pool GPUs join (ascending splitmix64 key, then index)."""
+    return sorted(candidates, key=lambda g: (splitmix64((splitmix64(seed) ^ JOIN_SALT ^ g) & MASK64), g))
+
+
+def membership_events(seed: int, lo: np.ndarray, hi: np.ndarray, present: np.ndarray, token_cap: np.ndarray,
+                      layer_cap: np.ndarray, layer_count: int, fraction: float, n_join: int):
+    """One scenario's membership history, in the reference's semantics.
+
+    1. ``on_leave`` (membership.py:340-357) of the seeded churn set of the plan GPUs that are present
+       (:func:`churn_set`: never uncovers a layer).
+    2. ``on_join`` (membership.py:317-338) of the first ``n_join`` absent pool GPUs in :func:`join_order`:
+       the GPU starts at ``bottleneck_layer()`` (membership.py:303-315: the layer with the least summed
+       ``ram_token_capacity`` over its current hosts, first such layer; holes count as 0) and takes
+       ``min(start + layer_capacity - 1, L)``; a GPU below one layer joins without a slice (ZeroCapacityGpu).
+
+    Returns (absent[N] bool, lo_s[N], hi_s[N], left, joined, bottlenecks) -- slices 0/-1 when none.
+    """
+    n = lo.shape[0]
+    lo_s, hi_s = lo.astype(np.int32).copy(), hi.astype(np.int32).copy()
+    absent = ~present.astype(bool)
+    lo_s[absent] = 0
+    hi_s[absent] = -1
+    plan = [g for g in range(n) if not absent[g] and lo_s[g] <= hi_s[g]]
+    slices = {g: (int(lo_s[g]), int(hi_s[g])) for g in plan}
+    want = int(len(plan) * fraction)
+    left = churn_set(seed, plan, slices, layer_count, fraction) if want > 0 else []
+    for g in left:
+        absent[g] = True
+        lo_s[g], hi_s[g] = 0, -1
+    tot = np.zeros(layer_count + 2, dtype=np.int64)
+    for g in range(n):
+        if not absent[g] and lo_s[g] <= hi_s[g]:
+            tot[lo_s[g]:hi_s[g] + 1] += int(token_cap[g])
+    joined, bottlenecks = [], []
+    candidates = [g for g in range(n) if not present[g]]
+    for g in join_order(seed, candidates)[:n_join]:
+        start = int(np.argmin(tot[1:layer_count + 1])) + 1          # first least-capacity layer
+        bottlenecks.append(start)
+        absent[g] = False
+        joined.append(g)
+        cap = int(layer_cap[g])
+        if cap < 1:
+            continue                                                   # registered, serves nothing
+        end = min(start + cap - 1, layer_count)
+        lo_s[g], hi_s[g] = start, end
+        tot[start:end + 1] += int(token_cap[g])
+    return absent, lo_s, hi_s, left, joined, bottlenecks
+
+
 # ---------------------------------------------------------------------------
 # scenario description (what the replay consumes)
 # ---------------------------------------------------------------------------
@@ -140,9 +194,12 @@ class ScenarioSet:
 
     base_rtt[N, N]   ground-truth rtt_s over all pool GPUs (diag 0)
     base_tau[N]      flops_per_layer_per_token / flops
-    slice_lo/hi[N]   1-based inclusive layer range per GPU, 0/-1 when not serving
+    slice_lo/hi[N]   1-based inclusive layer range per GPU in the base plan, 0/-1 when not serving
     seeds[S]         per-scenario jitter / churn seed
-    leave[S, N]      bool, GPU departed in scenario s
+    leave[S, N]      bool, GPU absent in scenario s (departed, or a join-pool GPU that did not join)
+    present0[N]      bool, GPU in the pool before the scenario's events (False: join pool)
+    slice_lo_s/hi_s  [S, N] per-scenario slices when the scenarios have joins, else None
+    churn/joins      the event counts the device generator reproduces (ss_scenario_membership)
     """
 
     layer_count: int
@@ -154,6 +211,13 @@ class ScenarioSet:
     seeds: np.ndarray
     leave: np.ndarray
     jitter: bool = True
+    present0: Optional[np.ndarray] = None
+    slice_lo_s: Optional[np.ndarray] = None
+    slice_hi_s: Optional[np.ndarray] = None
+    churn: float = 0.0
+    joins: int = 0
+    token_cap: Optional[np.ndarray] = None
+    layer_cap: Optional[np.ndarray] = None
 
     @property
     def n_scenarios(self) -> int:
@@ -168,10 +232,15 @@ class ScenarioSet:
             return self.base_rtt.copy()
         return self.base_rtt * jitter_factor_matrix(int(self.seeds[s]), self.n_gpus)
 
+    def slices(self, s: int) -> Tuple[np.ndarray, np.ndarray]:
+        if self.slice_lo_s is not None:
+            return self.slice_lo_s[s], self.slice_hi_s[s]
+        return self.slice_lo, self.slice_hi
+
     def columns(self, s: int) -> List[np.ndarray]:
         alive = ~self.leave[s]
-        return [np.nonzero(alive & (self.slice_lo <= l) & (self.slice_hi >= l))[0]
-                for l in range(1, self.layer_count + 1)]
+        lo, hi = self.slices(s)
+        return [np.nonzero(alive & (lo <= l) & (hi >= l))[0] for l in range(1, self.layer_count + 1)]
 
 
 def base_rtt_matrix(cluster: ClusterSnapshot, ids: Sequence[str]) -> np.ndarray:
@@ -184,8 +253,16 @@ def base_rtt_matrix(cluster: ClusterSnapshot, ids: Sequence[str]) -> np.ndarray:
 
 
 def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenarios: int, *,
-                    seed0: int = 0, churn: float = 0.05, jitter: bool = True, seeds=None) -> ScenarioSet:
-    """C4-style scenario batch over a placed pool."""
+                    seed0: int = 0, churn: float = 0.05, jitter: bool = True, seeds=None,
+                    join_pool: Sequence[str] = (), joins: int = 0, host_events: bool = True) -> ScenarioSet:
+    """C4-style scenario batch over a placed pool.
+
+    ``cluster`` holds every GPU a scenario can see; ``join_pool`` names the ones absent at the start
+    (not in the plan's pool), ``joins`` of which join each scenario after its leaves
+    (:func:`membership_events`).  With ``host_events=False`` the events are left to the device generator
+    (``ss_scenario_membership``, run by ScenarioReplayer.build) and ``leave`` / per-scenario slices stay
+    unset on the host.
+    """
     ids = sorted(g.id for g in cluster.gpus)
     pos = {g: i for i, g in enumerate(ids)}
     n = len(ids)
@@ -203,10 +280,34 @@ def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenario
              else np.asarray(seeds, dtype=np.int64))
     leave = np.zeros((n_scenarios, n), dtype=bool)
     plan_gpus = sorted(slices)
-    if churn > 0:
+    pool_absent = set(join_pool)
+    present0 = np.array([g not in pool_absent for g in ids], dtype=bool)
+    token_cap = np.array([by_id[g].ram_token_capacity for g in ids], dtype=np.int64)
+    from .topology import layer_capacity
+    layer_cap = np.array([layer_capacity(by_id[g], model) for g in ids], dtype=np.int32)
+    if joins and not pool_absent:
+        raise ValueError("joins need a join_pool of absent GPUs")
+    lo_s = hi_s = None
+    if not host_events:
+        leave[:, ~present0] = True
+        if joins:
+            lo_s = np.zeros((n_scenarios, n), dtype=np.int32)
+            hi_s = np.full((n_scenarios, n), -1, dtype=np.int32)
+    elif joins:
+        lo_s = np.zeros((n_scenarios, n), dtype=np.int32)
+        hi_s = np.full((n_scenarios, n), -1, dtype=np.int32)
         for s in range(n_scenarios):
-            leave[s, churn_set(int(seeds[s]), plan_gpus, slices, model.layer_count, churn)] = True
-    return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter)
+            absent, l_s, h_s, _, _, _ = membership_events(int(seeds[s]), lo, hi, present0, token_cap, layer_cap,
+                                                          model.layer_count, churn, joins)
+            leave[s], lo_s[s], hi_s[s] = absent, l_s, h_s
+    else:
+        leave[:, ~present0] = True
+        if churn > 0:
+            plan_now = [g for g in plan_gpus if present0[g]]
+            for s in range(n_scenarios):
+                leave[s, churn_set(int(seeds[s]), plan_now, slices, model.layer_count, churn)] = True
+    return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter, present0, lo_s, hi_s,
+                       churn, joins, token_cap, layer_cap)
 
 
 # ---------------------------------------------------------------------------
