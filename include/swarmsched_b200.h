@@ -87,9 +87,10 @@ int ss_dag_columns(int32_t n_dags, const int32_t* layer_ptr, const int32_t* gpu_
 
 /* Scenario columns (C4/C5 replay states): host set of layer l in scenario s =
  * gpus g (pool order) with !leave[s][g] and slice_lo[g] <= l <= slice_hi[g];
- * the base pool is shared, scenario s owns flat layers [s*L, (s+1)*L). */
+ * scenario s owns flat layers [s*L, (s+1)*L).  slice_stride = 0: one shared
+ * plan; = n_gpus: per-scenario slices (after joins, ss_scenario_membership). */
 int ss_scenario_columns(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
-                        const int32_t* slice_hi, const uint8_t* leave, const int32_t* col_off,
+                        const int32_t* slice_hi, int64_t slice_stride, const uint8_t* leave, const int32_t* col_off,
                         int32_t* col_len, int32_t* node_gpu, int32_t* status, int32_t* aux, void* stream);
 
 /* Edge blocks E_l = RTT[col_l, col_{l+1}] (router.py:169 gather).  RTT source:
@@ -128,6 +129,43 @@ typedef struct ss_replay_out {
 
 int ss_replay(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
               int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
+
+/* Membership churn on device (membership.py:303-357).
+ * One CTA per scenario replays the scenario's events on the base placement:
+ *   1. on_leave of want_leave plan GPUs present at the start, visited in
+ *      ascending splitmix64(splitmix64(seed) ^ 0xC4<<40 ^ g) order, each taken
+ *      only if every layer of its slice keeps another host (never uncovers);
+ *   2. on_join of the first n_join absent GPUs (present0 == 0) in ascending
+ *      splitmix64(splitmix64(seed) ^ 0x4A<<40 ^ g) order: slice starts at
+ *      bottleneck_layer() (least summed token_cap over current hosts, first
+ *      such layer, holes = 0) and spans min(layer_cap, L - start + 1) layers;
+ *      layer_cap < 1 joins without a slice (ZeroCapacityGpu).
+ * Outputs per scenario row (stride n_gpus): absent (left or never joined),
+ * lo_s / hi_s (0 / -1 when no slice), joined[s * n_join + j] (-1 past the
+ * pool), status SS_UNCOVERED_LAYER + aux = first hole.  Bit-identical to
+ * scenarios.membership_events (pinned to the reference MembershipManager). */
+int ss_scenario_membership(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
+                           const int32_t* slice_hi, const uint8_t* present0, const int64_t* token_cap,
+                           const int32_t* layer_cap, const int64_t* seeds, int32_t want_leave, int32_t n_join,
+                           uint8_t* absent, int32_t* lo_s, int32_t* hi_s, int32_t* joined, int32_t* status,
+                           int32_t* aux, void* stream);
+
+/* evaluate_triggers per scenario (membership.py:359-396, perfmap.py:86-114),
+ * bit-identical under CPython 3.12 semantics: total memory / flops and the CoV
+ * mean / variance are compensated sum()s; per-layer kv / compute are plain
+ * folds in slices order.  gpu_order lists the base pool in _gpus (cluster)
+ * order, slice_order the plan GPUs in plan.gpu_slices() order; joined GPUs
+ * (joined[s * n_join + j], -1 = none) are appended to both.  State rows
+ * (kv_reserved int64, occ int32; either may be NULL = 0) use state_stride.
+ * decision: 0 local/balanced, 1 global/uncovered_layers, 2 global/load_cov_exceeded;
+ * first_uncovered = 0 when covered; loads may be NULL. */
+int ss_membership_triggers(int32_t n_scen, int32_t layers, int32_t n_gpus, const uint8_t* absent,
+                           const int32_t* lo_s, const int32_t* hi_s, int64_t slice_stride, const int32_t* gpu_order,
+                           int32_t n_order, const int32_t* slice_order, int32_t n_slice_order, const int32_t* joined,
+                           int32_t n_join, const double* vram, const double* reserve, const double* flops,
+                           const int64_t* token_cap, const int64_t* kv_reserved, const int32_t* occ,
+                           int64_t state_stride, double mix_alpha, double cov_threshold, double* loads, double* cov,
+                           int32_t* decision, int32_t* first_uncovered, void* stream);
 
 /* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
  * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring
@@ -247,7 +285,7 @@ int ss_score(int32_t n, const int32_t* k, const int32_t* s_star, const double* k
  *     must be the matching ss_scenario_columns set; s_rows >= max s_used. */
 int64_t ss_slot_meta_bytes(int32_t layers, int32_t n_gpus, int32_t s_cap);
 int ss_slot_program(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo, const int32_t* slice_hi,
-                    const uint8_t* leave, const double* rtt, const int64_t* jitter_seed, int32_t s_cap,
+                    int64_t slice_stride, const uint8_t* leave, const double* rtt, const int64_t* jitter_seed, int32_t s_cap,
                     int64_t meta_stride, int64_t stream_stride, uint8_t* meta, double* stream, int32_t* s_used,
                     int32_t* status, void* stream_h);
 int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_stride, const double* stream,

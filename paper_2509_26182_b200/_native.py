@@ -51,8 +51,9 @@ _SIGS = {
     "ss_dag_columns": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),
-    "ss_scenario_columns": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
-                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_scenario_columns": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]),
     "ss_dag_edges": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                C.c_void_p, C.c_void_p]),
     "ss_select": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -60,14 +61,22 @@ _SIGS = {
                             C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
     "ss_set_tiling": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p]),
     "ss_slot_meta_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
-    "ss_slot_program": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                  C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+    "ss_slot_program": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p]),
     "ss_replay_slots": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_int32, C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(ReplayOut), C.c_void_p]),
     "ss_set_slot_staging": (C.c_int, [C.c_int32, C.c_int32]),
     "ss_replay_warp_smem": (C.c_int64, [C.POINTER(DagSet), C.c_int32, C.c_int32]),
+    "ss_scenario_membership": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_membership_triggers": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                         C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_replay_warp": (C.c_int, [C.POINTER(DagSet), C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
 }

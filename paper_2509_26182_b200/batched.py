@@ -51,9 +51,12 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
     if (cap == 0).any():
         raise ValueError("base plan leaves a layer uncovered")
     # frontier |col_b U col_{b+1}| of the base plan, plus the slots held one boundary longer
-    # (delayed reuse, replay_slots.cu), bounds the slots; churn only removes hosts
+    # (delayed reuse, replay_slots.cu), bounds the slots; departures only remove hosts, each join adds
+    # at most one host per layer and one slot per boundary
     held = ((lo[None, :] <= layers[:-1, None] + 1) & (hi[None, :] >= layers[:-1, None] - 1)).sum(axis=1) \
         if L > 1 else np.zeros(1, dtype=np.int64)
+    cap = cap + scen.joins
+    held = held + scen.joins
     s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
     occ_len = window + 2 if window > 0 else (max_requests or 1 << 16) + 2
     probe = N.DagSet(scen.n_scenarios, int(cap.max()), L, scen.n_gpus, None, None, None, None, None, None, None)
@@ -140,6 +143,19 @@ class ScenarioReplayer:
         self.slice_lo = up(lo, t32)
         self.slice_hi = up(hi, t32)
         self.leave = up(scen.leave.astype(np.uint8), torch.uint8)
+        # per-scenario slices (joins): host-made, or written by ss_scenario_membership in build()
+        self.per_scenario = scen.joins > 0 or scen.device_events
+        if self.per_scenario:
+            if scen.slice_lo_s is not None and not scen.device_events:
+                self.lo_s, self.hi_s = up(scen.slice_lo_s, t32), up(scen.slice_hi_s, t32)
+            else:
+                self.lo_s = torch.zeros(S * G, dtype=t32, device=dev)
+                self.hi_s = torch.zeros(S * G, dtype=t32, device=dev)
+            self.joined = torch.full((S * max(scen.joins, 1),), -1, dtype=t32, device=dev)
+        if scen.device_events:
+            self.present0 = up(scen.present0.astype(np.uint8), torch.uint8)
+            self.token_cap = up(scen.token_cap, t64)
+            self.layer_cap = up(scen.layer_cap, t32)
         self.seeds = up(scen.seeds.astype(np.int64), t64)
         self.base_rtt = up(scen.base_rtt.reshape(-1), f64)
         self.occ = torch.zeros(S * G, dtype=t32, device=dev)
@@ -163,12 +179,22 @@ class ScenarioReplayer:
         """Scenario columns + jittered edge blocks, fully on device (ss_scenario_columns, ss_dag_edges)."""
         lib = N.lib()
         st = N.stream_handle(self.stream)
-        N.check(lib.ss_scenario_columns(self.S, self.L, self.G, N.ptr(self.slice_lo), N.ptr(self.slice_hi),
+        if self.scen.device_events:
+            # membership churn on device: leaves + joins from the scenario seeds (no host prep)
+            N.check(lib.ss_scenario_membership(self.S, self.L, self.G, N.ptr(self.slice_lo), N.ptr(self.slice_hi),
+                                               N.ptr(self.present0), N.ptr(self.token_cap), N.ptr(self.layer_cap),
+                                               N.ptr(self.seeds), self.scen.want_leave, self.scen.joins,
+                                               N.ptr(self.leave), N.ptr(self.lo_s), N.ptr(self.hi_s),
+                                               N.ptr(self.joined), N.ptr(self.status), N.ptr(self.aux), st),
+                    "ss_scenario_membership")
+        lo_p, hi_p, stride = ((self.lo_s, self.hi_s, self.G) if self.per_scenario
+                              else (self.slice_lo, self.slice_hi, 0))
+        N.check(lib.ss_scenario_columns(self.S, self.L, self.G, N.ptr(lo_p), N.ptr(hi_p), stride,
                                         N.ptr(self.leave), N.ptr(self.col_off), N.ptr(self.col_len),
                                         N.ptr(self.node_gpu), N.ptr(self.status), N.ptr(self.aux), st),
                 "ss_scenario_columns")
         if self.mode == "slots":
-            N.check(lib.ss_slot_program(self.S, self.L, self.G, N.ptr(self.slice_lo), N.ptr(self.slice_hi),
+            N.check(lib.ss_slot_program(self.S, self.L, self.G, N.ptr(lo_p), N.ptr(hi_p), stride,
                                         N.ptr(self.leave), N.ptr(self.base_rtt),
                                         N.ptr(self.seeds) if self.scen.jitter else None, self.s_cap, self.meta_stride,
                                         self.stream_stride, N.ptr(self.meta), N.ptr(self.stream_buf),
@@ -227,13 +253,15 @@ class ScenarioReplayer:
     def run_from_host(self, leave_h, seeds_h, n_req: int, cost_h, hash_h) -> ReplayResult:
         """End-to-end call: host scenario descriptors in, host per-request results out.
 
-        leave_h [S, N] uint8 and seeds_h [S] int64 (pinned) are copied to the
-        device, the scenario DAGs are rebuilt (ss_scenario_columns +
-        ss_dag_edges), replay state is reset, n_req requests are routed per
+        leave_h [S, N] uint8 (None when the scenario events are generated on
+        the device) and seeds_h [S] int64 (pinned) are copied to the device,
+        the scenario DAGs are rebuilt (membership events, columns, edge blocks
+        or slot program), replay state is reset, n_req requests are routed per
         scenario and the costs / chain hashes come back into pinned cost_h /
         hash_h.  Stream-ordered; the caller synchronises.
         """
-        self.leave.copy_(leave_h, non_blocking=True)
+        if leave_h is not None:
+            self.leave.copy_(leave_h, non_blocking=True)
         self.seeds.copy_(seeds_h, non_blocking=True)
         self.occ.zero_()
         self.ring.zero_()
@@ -244,6 +272,39 @@ class ScenarioReplayer:
         cost_h.copy_(out.cost, non_blocking=True)
         hash_h.copy_(out.chain_hash, non_blocking=True)
         return out
+
+    def triggers(self, *, cov_threshold: float = 0.5, mix_alpha: float = 0.5, kv_reserved=None):
+        """evaluate_triggers of every scenario on the current occupancy (membership.py:389-396).
+
+        Returns (decision int32 [S]: 0 local, 1 global/uncovered_layers, 2 global/load_cov_exceeded;
+        cov float64 [S]; first uncovered layer int32 [S]; loads float64 [S, L]) as device tensors.
+        """
+        torch = self.torch
+        sc = self.scen
+        if not hasattr(self, "_trig"):
+            up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=self.dev, dtype=dt)
+            self._trig = dict(order=up(sc.cluster_order, torch.int32), sorder=up(sc.plan_order, torch.int32),
+                              vram=up(sc.vram, torch.float64), reserve=up(sc.reserve, torch.float64),
+                              flops=up(sc.flops, torch.float64), token=up(sc.token_cap, torch.int64))
+            if not self.per_scenario:
+                self._trig["lo"] = self.slice_lo
+                self._trig["hi"] = self.slice_hi
+        t = self._trig
+        lo, hi, stride = ((self.lo_s, self.hi_s, self.G) if self.per_scenario else (t["lo"], t["hi"], 0))
+        S, L = self.S, self.L
+        dec = torch.empty(S, dtype=torch.int32, device=self.dev)
+        cov = torch.empty(S, dtype=torch.float64, device=self.dev)
+        hole = torch.empty(S, dtype=torch.int32, device=self.dev)
+        loads = torch.empty((S, L), dtype=torch.float64, device=self.dev)
+        n_join = self.scen.joins if self.per_scenario else 0
+        N.check(N.lib().ss_membership_triggers(
+            S, L, self.G, N.ptr(self.leave), N.ptr(lo), N.ptr(hi), stride, N.ptr(t["order"]), len(sc.cluster_order),
+            N.ptr(t["sorder"]), len(sc.plan_order), N.ptr(self.joined) if n_join else None, n_join,
+            N.ptr(t["vram"]), N.ptr(t["reserve"]), N.ptr(t["flops"]), N.ptr(t["token"]),
+            N.ptr(kv_reserved) if kv_reserved is not None else None, N.ptr(self.occ), self.G, float(mix_alpha),
+            float(cov_threshold), N.ptr(loads), N.ptr(cov), N.ptr(dec), N.ptr(hole), N.stream_handle(self.stream)),
+            "ss_membership_triggers")
+        return dec, cov, hole, loads
 
     def raise_first_failure(self) -> None:
         st = self.status.cpu().numpy()

@@ -85,9 +85,11 @@ __global__ void dag_columns_kernel(const int32_t* layer_ptr, const int32_t* gpu_
 }
 
 __global__ void scenario_columns_kernel(int32_t layers, int32_t n_gpus, const int32_t* lo, const int32_t* hi,
-                                        const uint8_t* leave, const int32_t* col_off, int32_t* col_len,
-                                        int32_t* node_gpu, int32_t* status, int32_t* aux) {
+                                        int64_t slice_stride, const uint8_t* leave, const int32_t* col_off,
+                                        int32_t* col_len, int32_t* node_gpu, int32_t* status, int32_t* aux) {
     const int s = blockIdx.x;
+    lo += s * slice_stride;                               // per-scenario slices (joins) or the shared plan
+    hi += s * slice_stride;
     const uint8_t* gone = leave ? leave + (int64_t)s * n_gpus : nullptr;
     __shared__ int first_empty;
     if (threadIdx.x == 0) first_empty = 0x7fffffff;
@@ -176,13 +178,13 @@ extern "C" int ss_dag_columns(int32_t n_dags, const int32_t* layer_ptr, const in
 }
 
 extern "C" int ss_scenario_columns(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
-                                   const int32_t* slice_hi, const uint8_t* leave, const int32_t* col_off,
-                                   int32_t* col_len, int32_t* node_gpu, int32_t* status, int32_t* aux,
-                                   void* stream) {
+                                   const int32_t* slice_hi, int64_t slice_stride, const uint8_t* leave,
+                                   const int32_t* col_off, int32_t* col_len, int32_t* node_gpu, int32_t* status,
+                                   int32_t* aux, void* stream) {
     if (n_scen <= 0) return SS_OK;
-    if (layers < 1 || n_gpus < 1) return SS_BAD_INPUT;
-    scenario_columns_kernel<<<n_scen, 256, 0, ss_stream(stream)>>>(layers, n_gpus, slice_lo, slice_hi, leave,
-                                                                   col_off, col_len, node_gpu, status, aux);
+    if (layers < 1 || n_gpus < 1 || slice_stride < 0) return SS_BAD_INPUT;
+    scenario_columns_kernel<<<n_scen, 256, 0, ss_stream(stream)>>>(layers, n_gpus, slice_lo, slice_hi, slice_stride,
+                                                                   leave, col_off, col_len, node_gpu, status, aux);
     SS_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -69,13 +69,15 @@ struct BlkMeta {
 // program generation: one CTA per scenario
 // ---------------------------------------------------------------------------
 __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_t* lo, const int32_t* hi,
-                                    const uint8_t* leave, const double* rtt, const int64_t* jitter_seed,
+                                    int64_t slice_stride, const uint8_t* leave, const double* rtt, const int64_t* jitter_seed,
                                     int32_t s_cap, int64_t meta_stride, int64_t stream_stride, uint8_t* meta,
                                     double* stream, int32_t* s_used_out, int32_t* status) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int s = blockIdx.x;
     const int n_blk = layers - 1;
     const uint8_t* gone = leave ? leave + (int64_t)s * n_gpus : nullptr;
+    lo += s * slice_stride;                               // per-scenario slices (joins) or the shared plan
+    hi += s * slice_stride;
     MetaLayout ml{n_blk, s_cap, n_gpus};
     uint8_t* mt = meta + (int64_t)s * meta_stride;
     double* st = stream + (int64_t)s * stream_stride;
@@ -628,7 +630,7 @@ extern "C" int64_t ss_slot_meta_bytes(int32_t layers, int32_t n_gpus, int32_t s_
 }
 
 extern "C" int ss_slot_program(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
-                               const int32_t* slice_hi, const uint8_t* leave, const double* rtt,
+                               const int32_t* slice_hi, int64_t slice_stride, const uint8_t* leave, const double* rtt,
                                const int64_t* jitter_seed, int32_t s_cap, int64_t meta_stride, int64_t stream_stride,
                                uint8_t* meta, double* stream, int32_t* s_used, int32_t* status, void* stream_h) {
     if (n_scen <= 0) return SS_OK;
@@ -638,7 +640,8 @@ extern "C" int ss_slot_program(int32_t n_scen, int32_t layers, int32_t n_gpus, c
     if (smem > 200 * 1024) return SS_BAD_INPUT;
     if (cudaFuncSetAttribute(slot_program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SS_CUDA_ERROR;
-    slot_program_kernel<<<n_scen, 256, smem, ss_stream(stream_h)>>>(layers, n_gpus, slice_lo, slice_hi, leave, rtt,
+    slot_program_kernel<<<n_scen, 256, smem, ss_stream(stream_h)>>>(layers, n_gpus, slice_lo, slice_hi, slice_stride,
+                                                                    leave, rtt,
                                                                     jitter_seed, s_cap, meta_stride, stream_stride,
                                                                     meta, stream, s_used, status);
     SS_CHECK_LAUNCH();

@@ -218,6 +218,13 @@ class ScenarioSet:
     joins: int = 0
     token_cap: Optional[np.ndarray] = None
     layer_cap: Optional[np.ndarray] = None
+    device_events: bool = False        # leave / slices are generated by ss_scenario_membership
+    want_leave: int = 0
+    cluster_order: Optional[np.ndarray] = None   # base pool GPUs in cluster (MembershipManager._gpus) order
+    plan_order: Optional[np.ndarray] = None      # plan GPUs in plan.gpu_slices() order
+    vram: Optional[np.ndarray] = None
+    reserve: Optional[np.ndarray] = None
+    flops: Optional[np.ndarray] = None
 
     @property
     def n_scenarios(self) -> int:
@@ -306,8 +313,15 @@ def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenario
             plan_now = [g for g in plan_gpus if present0[g]]
             for s in range(n_scenarios):
                 leave[s, churn_set(int(seeds[s]), plan_now, slices, model.layer_count, churn)] = True
+    want = int(len([g for g in plan_gpus if present0[g]]) * churn) if churn > 0 else 0
+    cluster_order = np.array([pos[g.id] for g in cluster.gpus if present0[pos[g.id]]], dtype=np.int32)
+    plan_order = np.array([pos[g] for g in plan.gpu_slices()], dtype=np.int32)
+    vram = np.array([by_id[g].vram_bytes for g in ids], dtype=np.float64)
+    reserve = np.array([by_id[g].reserve_fraction for g in ids], dtype=np.float64)
+    flops = np.array([by_id[g].flops for g in ids], dtype=np.float64)
     return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter, present0, lo_s, hi_s,
-                       churn, joins, token_cap, layer_cap)
+                       churn, joins, token_cap, layer_cap, not host_events, want, cluster_order, plan_order, vram,
+                       reserve, flops)
 
 
 # ---------------------------------------------------------------------------
