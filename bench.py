@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--mode", default="slots", choices=["slots", "blocks"],
                     help="Phase-2 kernel of the headline value (the other one is reported as phase2_alt)")
     ap.add_argument("--no-alt", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-scenarios", type=int, default=4096, help="C5 scenarios per sub-pool (whole job)")
+    ap.add_argument("--c5-steps", type=int, default=8)
+    ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--c2-requests", type=int, default=20000)
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
     ap.add_argument("--cpu-sample-pools", type=int, default=400)
@@ -297,6 +302,9 @@ def run_ours(args):
                          "variants_per_gpu": V, "candidates_per_gpu": n_cand, "pools_with_errors": bad},
               "roofline": {"bound": "issue (integer/bitset DP)", "note": "not HBM-bound; see DESIGN.md"}}
 
+    c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
+    c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
+
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -331,11 +339,96 @@ def run_ours(args):
             "phase2_alt": alt,
             "cpu_baseline": cpu,
             "phase1": p1,
+            "c5": c5,
+            "c2": c2,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_c5(args, rank, world, stream, barrier, reduce_max):
+    """C5: 1,024-GPU mixed pool (8B/32B/70B sub-pools, 8 regions, explicit cross-region link
+    matrix), full two-phase schedule: device allocate() per sub-pool, device-generated churn + jitter scenario
+    states (sharded s -> rank s mod world), then route/release replay with on-device load update."""
+    import torch
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    R, W = args.requests_per_step, args.window
+    pools = scen.c5_pools(0)
+    seeds = shard(args.c5_scenarios, rank, world)
+    with torch.cuda.stream(stream):
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        plans = [allocate(cl, model) for _, cl, model in pools]              # Phase-1 on device
+        torch.cuda.synchronize()
+        t_p1 = reduce_max(time.perf_counter() - t0)
+        t1 = time.perf_counter()
+        reps, outs = [], []
+        for (name, cl, model), plan in zip(pools, plans):
+            ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.05, jitter=True,
+                                      host_events=False)                      # events generated on device
+            rp = ScenarioReplayer(ss, window=W, stream=stream)
+            rp.build()
+            reps.append(rp)
+            outs.append(rp.run(R))
+        torch.cuda.synchronize()
+        t_build = reduce_max(time.perf_counter() - t1)
+        for rp in reps:
+            rp.raise_first_failure()
+
+        def step():
+            for rp, out in zip(reps, outs):
+                rp.run(R, out=out)
+        t = timed(step, args.c5_steps, args.warmup, stream, barrier, reduce_max)
+    sel = len(seeds) * R * len(reps) * world * args.c5_steps
+    res = {"metric": "C5 two-phase schedule: Phase-2 chain selections/sec (whole job)", "value": sel / t,
+           "unit": "selections/s", "ms_per_step": 1e3 * t / args.c5_steps,
+           "phase1_ms": 1e3 * t_p1, "scenario_build_ms": 1e3 * t_build,
+           "config": {"workload": "C5: 1,024 GPUs in 8 regions (explicit region RTT matrix, intra 1 ms, inter "
+                                  "U(5,80) ms) split 256/384/384 into 8B (L=32) / 32B (L=64) / 70B (L=80) "
+                                  "sub-pools; device allocate() per sub-pool; %d churn+jitter scenarios per "
+                                  "sub-pool (device-generated membership events) x %d requests per step, W=%d"
+                                  % (args.c5_scenarios, R, W),
+                      "sub_pools": [{"name": name, "gpus": len(cl.gpus), "layers": model.layer_count,
+                                     "k": plan.replication_count, "kernel": rp.mode}
+                                    for (name, cl, model), plan, rp in zip(pools, plans, reps)],
+                      "scenarios_per_sub_pool": args.c5_scenarios, "parallelism": f"scenario-sharded x{world}"}}
+    del reps, outs
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_c2(args, stream):
+    """C2: one 64-layer scenario over 64 GPUs (k = 17), a long serial request stream with
+    on-device load update (W=64): the latency-bound path (one warp owns the scenario)."""
+    import torch
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = allocate(cl, model)
+    ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
+    rp = ScenarioReplayer(ss, window=args.window, stream=stream)
+    n = args.c2_requests
+    with torch.cuda.stream(stream):
+        rp.run(64)
+        torch.cuda.synchronize()
+        rp.reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rp.run(n)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    rp.raise_first_failure()
+    t = e0.elapsed_time(e1) / 1e3
+    return {"metric": "C2 serial chain selections/sec (one scenario)", "value": n / t, "unit": "selections/s",
+            "us_per_selection": 1e6 * t / n, "kernel": rp.mode,
+            "config": {"workload": "C2: L=64 over 64 GPUs (k=%d), %d consecutive requests of one scenario, W=%d "
+                                   "(the 1M-request stream at this rate takes %.0f s)"
+                                   % (plan.replication_count, n, args.window, 1e6 * t / n)}}
 
 
 def _variants_for_rank(scen, V, rank, world):

@@ -67,6 +67,45 @@ def synthetic_cluster(gpu_count: int, *, seed: int = 0, region_count: Optional[i
     return ClusterSnapshot(gpus=tuple(nodes), links=links), model
 
 
+C5_SPLIT = ((256, 32, "8b"), (384, 64, "32b"), (384, 80, "70b"))
+
+
+def region_rtt_matrix(region_count: int, seed: int, intra: float = INTRA_REGION_RTT_S,
+                      inter: Tuple[float, float] = (0.005, 0.080)) -> np.ndarray:
+    """Seeded symmetric region x region one-way RTT matrix: intra 1 ms, inter U(5, 80) ms."""
+    rng = random.Random(seed)
+    m = np.full((region_count, region_count), intra)
+    for a in range(region_count):
+        for b in range(a + 1, region_count):
+            m[a, b] = m[b, a] = rng.uniform(*inter)
+    return m
+
+
+def c5_pools(seed: int = 0, region_count: int = 8):
+    """C5: 1,024 bench-drawn GPUs in 8 regions with an explicit all-pairs link table from a
+    seeded region RTT matrix, split 256 / 384 / 384 into 8B (L=32) / 32B (L=64) / 70B (L=80) sub-pools.
+    Returns [(name, ClusterSnapshot, ModelSpec)], one per sub-pool (its GPUs and their links only)."""
+    total = sum(n for n, _, _ in C5_SPLIT)
+    rng = random.Random(seed)
+    names = [f"region-{chr(ord('a') + i)}" for i in range(region_count)]
+    reg = region_rtt_matrix(region_count, seed ^ 0x5EED)
+    draws = [(rng.randint(*CAPACITY_RANGE), rng.uniform(*FLOPS_RANGE)) for _ in range(total)]
+    out, start = [], 0
+    for n, layers, name in C5_SPLIT:
+        model = bench_model(layers, f"c5-{name}")
+        nodes = tuple(GpuNode(id=f"gpu-{i:04d}", region=names[i % region_count],
+                              vram_bytes=draws[i][0] * model.bytes_per_layer / 0.8, flops=draws[i][1],
+                              reserve_fraction=0.2) for i in range(start, start + n))
+        links = {}
+        for a in range(n):
+            ra = (start + a) % region_count
+            for b in range(a + 1, n):
+                links[(nodes[a].id, nodes[b].id)] = float(reg[ra, (start + b) % region_count])
+        out.append((name, ClusterSnapshot(gpus=nodes, links=links), model))
+        start += n
+    return out
+
+
 # ---------------------------------------------------------------------------
 # deterministic hashing shared with the device generator
 # ---------------------------------------------------------------------------
