@@ -81,44 +81,56 @@ __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_
     MetaLayout ml{n_blk, s_cap, n_gpus};
     uint8_t* mt = meta + (int64_t)s * meta_stride;
     double* st = stream + (int64_t)s * stream_stride;
-    // smem: slot_of[n_gpus] int16, occ_tl[n_blk][s_cap] int16, misc
+    // smem: slot_of[n_gpus] int16, occ_tl[n_blk][s_cap] int16, bucket lists (insert / free boundary)
     int16_t* slot_of = reinterpret_cast<int16_t*>(sm);
     int16_t* occ_tl = slot_of + ((n_gpus + 7) / 8) * 8;
+    int* ins_head = reinterpret_cast<int*>(occ_tl + ((n_blk * s_cap + 7) / 8) * 8);   // [n_blk + 2]
+    int* free_head = ins_head + n_blk + 2;                                             // [n_blk + 2]
+    int* ins_next = free_head + n_blk + 2;                                             // [n_gpus]
+    int* free_next = ins_next + n_gpus;                                                // [n_gpus]
     __shared__ int s_used, bad, wp_s;
     const int tid = threadIdx.x;
+    for (int i = tid; i < n_blk * s_cap; i += blockDim.x) occ_tl[i] = -1;
+    for (int g = tid; g < n_gpus; g += blockDim.x) slot_of[g] = -1;
+    for (int b = tid; b < n_blk + 2; b += blockDim.x) { ins_head[b] = -1; free_head[b] = -1; }
+    __syncthreads();
     if (tid == 0) {
+        // bucket the GPUs by first frontier boundary max(lo-2, 0) and by the boundary hi+1 at which their slot
+        // becomes reusable (interval [max(lo-2,0), hi-1] plus one zombie boundary); pushing front while
+        // walking g downwards keeps every bucket in ascending GPU order
+        for (int g = n_gpus - 1; g >= 0; --g) {
+            if (hi[g] < lo[g] || hi[g] < 1 || (gone && gone[g])) continue;
+            const int sb = lo[g] - 2 < 0 ? 0 : lo[g] - 2;
+            if (sb >= n_blk) continue;
+            ins_next[g] = ins_head[sb];
+            ins_head[sb] = g;
+            const int fb = hi[g] + 1;
+            if (fb < n_blk) {
+                free_next[g] = free_head[fb];
+                free_head[fb] = g;
+            }
+        }
         bad = 0;
         int used = 0;
         uint64_t freem[4] = {~0ull, ~0ull, ~0ull, ~0ull};      // s_cap <= 256
-        int16_t occ[256];
-        for (int q = 0; q < s_cap; ++q) occ[q] = -1;
-        for (int g = 0; g < n_gpus; ++g) slot_of[g] = -1;
         BlkMeta* bm = reinterpret_cast<BlkMeta*>(mt + ml.off_blk());
         int16_t* ins = reinterpret_cast<int16_t*>(mt + ml.off_ins());
         int n_ins_total = 0;
         int unit = 0;
         for (int b = 0; b < n_blk && !bad; ++b) {
-            // evict gpus whose frontier interval [max(lo-2,0), hi-1] ended before boundary b-1: a slot
-            // is reused one boundary late, so the kernel can write boundary b+1's rows / columns while
+            // slots are reused one boundary late, so the kernel can write boundary b+1's rows / columns while
             // boundary b is still being relaxed
-            for (int q = 0; q < s_cap; ++q) {
-                const int g = occ[q];
-                if (g >= 0 && hi[g] - 1 < b - 1) {
-                    occ[q] = -1;
-                    freem[q >> 6] |= 1ull << (q & 63);
-                }
+            for (int g = free_head[b]; g >= 0; g = free_next[g]) {
+                const int q = slot_of[g];
+                if (q >= 0) freem[q >> 6] |= 1ull << (q & 63);
             }
             const int start = n_ins_total;
-            for (int g = 0; g < n_gpus; ++g) {
-                if (hi[g] < lo[g] || (gone && gone[g])) continue;
-                const int sb = lo[g] - 2 < 0 ? 0 : lo[g] - 2;
-                if (sb != b || hi[g] < 1) continue;
+            for (int g = ins_head[b]; g >= 0; g = ins_next[g]) {
                 int q = -1;
                 for (int w = 0; w < 4 && q < 0; ++w)
                     if (freem[w]) q = w * 64 + __ffsll((long long)freem[w]) - 1;
                 if (q < 0 || q >= s_cap) { bad = 1; break; }
                 freem[q >> 6] &= ~(1ull << (q & 63));
-                occ[q] = (int16_t)g;
                 slot_of[g] = (int16_t)q;
                 if (q + 1 > used) used = q + 1;
                 ins[2 * n_ins_total] = (int16_t)q;
@@ -131,7 +143,6 @@ __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_
             m.unit_start = unit;
             bm[b] = m;
             unit += (b == 0 ? 1 : 2) * (n_ins_total - start);
-            for (int q = 0; q < s_cap; ++q) occ_tl[b * s_cap + q] = occ[q];
         }
         s_used = used;
         const int wp = (used + 1) & ~1;
@@ -144,6 +155,15 @@ __global__ void slot_program_kernel(int32_t layers, int32_t n_gpus, const int32_
         if ((int64_t)unit * wp > stream_stride) bad = 2;
         status[s] = bad ? SS_BAD_INPUT : SS_OK;
         s_used_out[s] = bad ? 0 : used;
+    }
+    __syncthreads();
+    // occupancy timeline: GPU g holds its slot for boundaries [max(lo-2,0), hi] (interval + zombie boundary)
+    for (int g = tid; g < n_gpus; g += blockDim.x) {
+        const int q = slot_of[g];
+        if (q < 0) continue;
+        const int sb = lo[g] - 2 < 0 ? 0 : lo[g] - 2;
+        const int eb = hi[g] < n_blk - 1 ? hi[g] : n_blk - 1;
+        for (int b = sb; b <= eb; ++b) occ_tl[b * s_cap + q] = (int16_t)g;
     }
     __syncthreads();
     if (bad) return;
@@ -636,7 +656,8 @@ extern "C" int ss_slot_program(int32_t n_scen, int32_t layers, int32_t n_gpus, c
     if (n_scen <= 0) return SS_OK;
     if (layers < 2 || n_gpus < 1 || s_cap < 32 || s_cap > 256 || (s_cap & 31)) return SS_BAD_INPUT;
     if (meta_stride < ss_slot_meta_bytes(layers, n_gpus, s_cap) || (meta_stride & 15)) return SS_BAD_INPUT;
-    const int smem = ((n_gpus + 7) / 8) * 8 * 2 + (layers - 1) * s_cap * 2 + 64;
+    const int smem = ((n_gpus + 7) / 8) * 8 * 2 + (((layers - 1) * s_cap + 7) / 8) * 8 * 2 + (layers + 1) * 8 +
+                     n_gpus * 8 + 64;
     if (smem > 200 * 1024) return SS_BAD_INPUT;
     if (cudaFuncSetAttribute(slot_program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SS_CUDA_ERROR;
