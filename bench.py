@@ -191,8 +191,10 @@ def run_ours(args):
     # ---- Phase-2 setup (outside the timed region) ----------------------------
     with torch.cuda.stream(stream):
         cl, model, plan = base_pool()
-        ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True,
-                                  seeds=shard(S, rank, world))           # scenario s -> rank s mod world
+        # scenario s -> rank s mod world; the departures (on_leave of up to 5% of the plan GPUs) are
+        # generated on the device from the seeds (ss_scenario_membership) -- no host preparation
+        ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=shard(S, rank, world),
+                                  host_events=False)
     sel_per_step_rank = S * R
     hbm, peak_src = peaks()
     other = "blocks" if args.mode == "slots" else "slots"
@@ -245,14 +247,13 @@ def run_ours(args):
         bound_note = "algorithmic bytes B2 per launch / launch time; every edge block streams from HBM once"
 
     # ---- e2e: host descriptors in, host results out ---------------------------
-    leave_h = torch.from_numpy(ss.leave.astype(np.uint8)).pin_memory()
     seeds_h = torch.from_numpy(ss.seeds.copy()).pin_memory()
     cost_h = torch.empty((S, R), dtype=torch.float64).pin_memory()
     hash_h = torch.empty((S, R), dtype=torch.int64).pin_memory()
     rp2 = ScenarioReplayer(ss, window=W, stream=stream, mode=args.mode)
     with torch.cuda.stream(stream):
         def e2e_step():
-            rp2.run_from_host(leave_h, seeds_h, R, cost_h, hash_h)
+            rp2.run_from_host(None, seeds_h, R, cost_h, hash_h)
         t_e2e = timed(e2e_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
     e2e_steps = max(2, args.steps // 2)
     torch.cuda.synchronize()
@@ -325,9 +326,10 @@ def run_ours(args):
                              "L2" % (_resident_bytes(rp) / 1e6, args.mode),
                        "bytes_per_selection_B2": float(b2.mean())},
             "e2e": {"value": e2e_value, "unit": "selections/s",
-                    "h2d_bytes_per_step": int(leave_h.numel() + seeds_h.numel() * 8),
+                    "h2d_bytes_per_step": int(seeds_h.numel() * 8),
                     "d2h_bytes_per_step": int(cost_h.numel() * 8 + hash_h.numel() * 8),
-                    "path": "ScenarioReplayer.run_from_host: H2D descriptors, device DAG build, replay, D2H results",
+                    "path": "ScenarioReplayer.run_from_host: H2D scenario seeds, device membership events + DAG "
+                            "build, replay, D2H results",
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -463,9 +465,13 @@ def _resident_bytes(rp):
     return rp.stream_buf.numel() * 8 + rp.meta.numel()
 
 
-def cpu_baseline(args, ss, packed):
+def cpu_baseline(args, ss_dev, packed):
     from oracle import bench_cpu
-    n_s = min(args.cpu_sample_scenarios, ss.n_scenarios)
+    from paper_2509_26182_b200 import scenarios as scen
+    n_s = min(args.cpu_sample_scenarios, ss_dev.n_scenarios)
+    cl, model, plan = base_pool()
+    # the sampled scenarios' departures drawn on the host (the same events the device generated)
+    ss = scen.build_scenarios(cl, model, plan, n_s, seeds=ss_dev.seeds[:n_s], churn=0.05, jitter=True)
     rate, cores, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), args.cpu_sample_requests, args.window)
     out = {"value": rate, "unit": "selections/s", "cores": cores, "kind": "port",
            "sample": f"C4 shape: {n_s} scenarios x {args.cpu_sample_requests} requests (W={args.window}), "

@@ -103,3 +103,23 @@ def test_device_triggers_uncovered(cuda_ready, membership_cases):
     assert int(hole[0]) == w["decision"][3][0]
     st = rp.status.cpu().numpy()
     assert st[0] == 1 and int(rp.aux.cpu()[0]) == w["decision"][3][0]
+
+
+def test_device_departures_equal_host_churn_c4(cuda_ready):
+    """C4 (leave-only events): the device-drawn departures equal the host churn sets scenario for scenario."""
+    import json
+    from helpers_golden import plan_from_golden
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    plan = plan_from_golden(json.load(open(os.path.join(HERE, "golden", "router_replays.json")))["c4_plan"])
+    cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+    seeds = np.arange(500, 564)
+    host = scen.build_scenarios(cl, model, plan, 64, seeds=seeds, churn=0.05, jitter=True)
+    dev = scen.build_scenarios(cl, model, plan, 64, seeds=seeds, churn=0.05, jitter=True, host_events=False)
+    rp = ScenarioReplayer(dev, window=64)
+    rp.build()
+    leave = rp.leave.view(64, -1).cpu().numpy().astype(bool)
+    assert (leave == host.leave).all()
+    rph = ScenarioReplayer(host, window=64)
+    a, b = rp.run(16), rph.run(16)
+    assert (a.cost.cpu().numpy() == b.cost.cpu().numpy()).all()
