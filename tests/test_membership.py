@@ -109,3 +109,64 @@ def test_uncovered_trigger(membership_cases):
                                                  np.zeros(ss.n_gpus, dtype=np.int64), ss.present0)
     scope, reason, cov, unc, _ = membership_ref.evaluate_triggers(ss.layer_count, gpus, slices, kv, occupancy)
     assert [scope, reason, cov.hex(), list(unc)] == want["decision"]
+
+
+@pytest.fixture(scope="module")
+def rebalance_cases():
+    with open(os.path.join(HERE, "golden", "rebalance_cases.json")) as fh:
+        return json.load(fh)
+
+
+def oracle_rebalance_flow(case, want):
+    """The oracle's rebalance loop for one golden scenario (oracle/rebalance_ref.py)."""
+    from oracle import alloc_ref, rebalance_ref
+    from paper_2509_26182_b200 import scenarios as scen
+    full, model, plan, join_ids, order = pool_for_case(case)
+    ss = scen.build_scenarios(full, model, plan, 1, seeds=[want["seed"]], churn=case["churn"], jitter=False,
+                              join_pool=join_ids, joins=case["joins"])
+    L, W, r1, r2 = case["L"], case["window"], case["r1"], case["r2"]
+    rtt = ss.scenario_rtt(0)
+    occpow = chain_ref.occ_power_table(W + 4)
+    absent0 = ~ss.present0
+    cols = rebalance_ref.columns_of(absent0, ss.slice_lo, ss.slice_hi, L)
+    picks1, costs1, occ, live = chain_ref.replay(cols, ss.base_tau, rtt, r1, W, occpow)
+    first = r1 - len(live)
+    absent, lo, hi = ss.leave[0].copy(), ss.slice_lo_s[0].copy(), ss.slice_hi_s[0].copy()
+    left = np.nonzero(ss.leave[0] & ss.present0)[0].tolist()
+    joined = want["joined"]
+    ab_leave = []
+    for g in sorted(left):
+        ab_leave += [first + j for j in rebalance_ref.abort(live, occ, [g])]
+    gpus, slices, kv, occupancy = trigger_inputs(full, ss.ids, order, left, joined, lo, hi, occ, ss.present0)
+    scope, reason, cov, _, _ = membership_ref.evaluate_triggers(L, gpus, slices, kv, occupancy,
+                                                                cov_threshold=case["cov_threshold"])
+    changed, ab_reb = [], []
+    if scope == "global":
+        pos = {g: i for i, g in enumerate(ss.ids)}
+        d = alloc_ref.allocate(rebalance_ref.churned_cluster(full, ss.ids, absent), model)
+        lo1, hi1, _ = rebalance_ref.plan_slices(d, pos, ss.n_gpus)
+        changed = rebalance_ref.changed_gpus(lo, hi, lo1, hi1)
+        ab_reb = [first + j for j in rebalance_ref.abort(live, occ, changed)]
+        lo, hi = lo1, hi1
+    cols2 = rebalance_ref.columns_of(absent, lo, hi, L)
+    picks2, costs2, occ, live = chain_ref.replay(cols2, ss.base_tau, rtt, r2, W, occpow, occ=occ, start=r1, live=live)
+    return dict(picks=picks1 + picks2, costs=costs1 + costs2, occ=occ, decision=[scope, reason, cov.hex()],
+                changed=changed, ab_leave=ab_leave, ab_reb=ab_reb, lo=lo, hi=hi, absent=absent)
+
+
+@pytest.mark.parametrize("name", ["n64_w8", "c1_w4", "n64_nochange"])
+def test_oracle_rebalance_loop_matches_reference(rebalance_cases, name):
+    case = rebalance_cases[name]
+    for want in case["scenarios"]:
+        got = oracle_rebalance_flow(case, want)
+        for r, row in enumerate(got["picks"]):
+            assert _hops(None, row) == want["chains"][r]["hops"], (name, want["seed"], r)
+            assert got["costs"][r] == hx(want["chains"][r]["cost"]), (name, want["seed"], r)
+        assert got["decision"] == want["decision"]
+        assert got["changed"] == want["changed"]
+        assert sorted(got["ab_leave"]) == sorted(want["aborted_leave"])
+        assert got["ab_reb"] == want["aborted_rebalance"]
+        assert got["occ"].tolist() == want["occ"]
+        slices = sorted([g, int(got["lo"][g]), int(got["hi"][g])] for g in range(len(got["lo"]))
+                        if not got["absent"][g] and got["lo"][g] <= got["hi"][g])
+        assert slices == want["slices"]
