@@ -155,17 +155,30 @@ int ss_scenario_membership(int32_t n_scen, int32_t layers, int32_t n_gpus, const
  * mean / variance are compensated sum()s; per-layer kv / compute are plain
  * folds in slices order.  gpu_order lists the base pool in _gpus (cluster)
  * order, slice_order the plan GPUs in plan.gpu_slices() order; joined GPUs
- * (joined[s * n_join + j], -1 = none) are appended to both.  State rows
+ * (joined[s * n_join + j], -1 = none) are appended to both.  order_stride > 0:
+ * per-scenario slice orders (after a rebalance: the new plan's order, joins
+ * included), joined GPUs are then appended to the _gpus order only.  State rows
  * (kv_reserved int64, occ int32; either may be NULL = 0) use state_stride.
  * decision: 0 local/balanced, 1 global/uncovered_layers, 2 global/load_cov_exceeded;
  * first_uncovered = 0 when covered; loads may be NULL. */
 int ss_membership_triggers(int32_t n_scen, int32_t layers, int32_t n_gpus, const uint8_t* absent,
                            const int32_t* lo_s, const int32_t* hi_s, int64_t slice_stride, const int32_t* gpu_order,
-                           int32_t n_order, const int32_t* slice_order, int32_t n_slice_order, const int32_t* joined,
+                           int32_t n_order, const int32_t* slice_order, int32_t n_slice_order, int64_t order_stride,
+                           const int32_t* joined,
                            int32_t n_join, const double* vram, const double* reserve, const double* flops,
                            const int64_t* token_cap, const int64_t* kv_reserved, const int32_t* occ,
                            int64_t state_stride, double mix_alpha, double cov_threshold, double* loads, double* cov,
                            int32_t* decision, int32_t* first_uncovered, void* stream);
+
+/* Abort of live chains (sim.py:401-411 _abort_chains_on): for every scenario, each
+ * chain of requests [next_req - W, next_req) whose distinct GPUs (ring slot)
+ * include a marked GPU (mark[s * n_gpus + g] != 0) is released now -- occ -1
+ * on each of its GPUs -- and its ring slot emptied, so release(i - W) later is
+ * a no-op.  n_aborted[s] / aborted[s * W + i % W] (optional) report them.
+ * W = 0 is a no-op; W < 0 (no window) keeps no ring and is rejected. */
+int ss_ring_abort(int32_t n_scen, int32_t n_gpus, int32_t max_layers, int32_t window, const uint8_t* mark,
+                  int32_t* occ, int32_t* ring, const int64_t* next_req, int32_t* n_aborted, uint8_t* aborted,
+                  void* stream);
 
 /* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
  * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring

@@ -258,3 +258,24 @@ def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int
     N.check(lib.ss_objective(I, N.ptr(item_ptr_d), N.ptr(flops_d), N.ptr(off_d), N.ptr(rtt), float(fpl),
                              N.ptr(layers_d), float(tokens), N.ptr(t), N.ptr(r), st), "ss_objective")
     return t, r
+
+
+def objective_dense(flops_cluster_order, rtt_mats, fpl: float, layers: int, tokens: float, stream=None):
+    """estimate_objective_params for many regions given dense rtt_s matrices (cluster order) -> (t_comp, rtt)."""
+    torch = _torch()
+    lib = N.lib()
+    dev = torch.device("cuda")
+    n = np.array([len(f) for f in flops_cluster_order], dtype=np.int64)
+    item_ptr = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
+    mat_off = np.concatenate([[0], np.cumsum(n * n)[:-1]]).astype(np.int64)
+    I = len(n)
+    flops = torch.from_numpy(np.concatenate([np.asarray(f, dtype=np.float64) for f in flops_cluster_order])).to(dev)
+    rtt = torch.from_numpy(np.concatenate([np.asarray(m, dtype=np.float64).reshape(-1) for m in rtt_mats])).to(dev)
+    ip = torch.from_numpy(item_ptr).to(dev)
+    mo = torch.from_numpy(mat_off).to(dev)
+    lay = torch.full((I,), int(layers), dtype=torch.int32, device=dev)
+    t = torch.empty(I, dtype=torch.float64, device=dev)
+    r = torch.empty(I, dtype=torch.float64, device=dev)
+    N.check(lib.ss_objective(I, N.ptr(ip), N.ptr(flops), N.ptr(mo), N.ptr(rtt), float(fpl), N.ptr(lay), float(tokens),
+                             N.ptr(t), N.ptr(r), N.stream_handle(stream)), "ss_objective")
+    return t, r

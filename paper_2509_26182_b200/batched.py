@@ -57,6 +57,9 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
         if L > 1 else np.zeros(1, dtype=np.int64)
     cap = cap + scen.joins
     held = held + scen.joins
+    if scen.slice_lo_s is not None and not scen.device_events and scen.joins == 0:
+        # explicit per-scenario placements (e.g. after a rebalance): the widest scenario bounds the layout
+        cap, held = _explicit_widths(scen)
     s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
     occ_len = window + 2 if window > 0 else (max_requests or 1 << 16) + 2
     probe = N.DagSet(scen.n_scenarios, int(cap.max()), L, scen.n_gpus, None, None, None, None, None, None, None)
@@ -68,6 +71,25 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
     if L < 2 and mode == "slots":
         mode = "blocks"                      # no boundaries: nothing to tile
     return mode, cap, s_cap, occ_len
+
+
+def _explicit_widths(scen: ScenarioSet):
+    """Max over scenarios of hosts per layer and of frontier slots (+ the zombie boundary) per boundary."""
+    L = scen.layer_count
+    lo, hi = scen.slice_lo_s.astype(np.int64), scen.slice_hi_s.astype(np.int64)
+    ok = ~scen.leave & (lo <= hi)
+    s_idx, g_idx = np.nonzero(ok)
+    a, b = lo[s_idx, g_idx], hi[s_idx, g_idx]
+    d = np.zeros((scen.n_scenarios, L + 3), dtype=np.int64)
+    np.add.at(d, (s_idx, a), 1)
+    np.add.at(d, (s_idx, b + 1), -1)
+    cap = np.cumsum(d, axis=1)[:, 1:L + 1].max(axis=0)
+    # frontier interval of a host in boundaries [max(a-2, 0), b] (incl. the zombie boundary), b < L-1
+    h = np.zeros((scen.n_scenarios, L + 2), dtype=np.int64)
+    np.add.at(h, (s_idx, np.maximum(a - 2, 0)), 1)
+    np.add.at(h, (s_idx, np.minimum(b, L - 2) + 1), -1)
+    held = np.cumsum(h, axis=1)[:, :max(L - 1, 1)].max(axis=0)
+    return cap, held
 
 
 def replay_mode(scen: ScenarioSet, *, window: int = 64, max_requests: Optional[int] = None,
@@ -144,7 +166,7 @@ class ScenarioReplayer:
         self.slice_hi = up(hi, t32)
         self.leave = up(scen.leave.astype(np.uint8), torch.uint8)
         # per-scenario slices (joins): host-made, or written by ss_scenario_membership in build()
-        self.per_scenario = scen.joins > 0 or scen.device_events
+        self.per_scenario = scen.joins > 0 or scen.device_events or scen.slice_lo_s is not None
         if self.per_scenario:
             if scen.slice_lo_s is not None and not scen.device_events:
                 self.lo_s, self.hi_s = up(scen.slice_lo_s, t32), up(scen.slice_hi_s, t32)
@@ -152,6 +174,8 @@ class ScenarioReplayer:
                 self.lo_s = torch.zeros(S * G, dtype=t32, device=dev)
                 self.hi_s = torch.zeros(S * G, dtype=t32, device=dev)
             self.joined = torch.full((S * max(scen.joins, 1),), -1, dtype=t32, device=dev)
+            if scen.joined_s is not None and scen.joins > 0:
+                self.joined.copy_(torch.from_numpy(np.ascontiguousarray(scen.joined_s.reshape(-1))))
         if scen.device_events:
             self.present0 = up(scen.present0.astype(np.uint8), torch.uint8)
             self.token_cap = up(scen.token_cap, t64)
@@ -297,14 +321,161 @@ class ScenarioReplayer:
         hole = torch.empty(S, dtype=torch.int32, device=self.dev)
         loads = torch.empty((S, L), dtype=torch.float64, device=self.dev)
         n_join = self.scen.joins if self.per_scenario else 0
+        if sc.slice_order_s is not None:
+            if "sorder_s" not in t:
+                t["sorder_s"] = torch.from_numpy(np.ascontiguousarray(sc.slice_order_s)).to(self.dev,
+                                                                                          dtype=torch.int32)
+                t["joined_s"] = torch.from_numpy(np.ascontiguousarray(sc.joined_s)).to(self.dev, dtype=torch.int32)
+            sorder, n_sorder, ostride = t["sorder_s"], sc.slice_order_s.shape[1], sc.slice_order_s.shape[1]
+            jn, n_join = t["joined_s"], sc.joined_s.shape[1]
+        else:
+            sorder, n_sorder, ostride = t["sorder"], len(sc.plan_order), 0
+            jn = self.joined if n_join else None
         N.check(N.lib().ss_membership_triggers(
             S, L, self.G, N.ptr(self.leave), N.ptr(lo), N.ptr(hi), stride, N.ptr(t["order"]), len(sc.cluster_order),
-            N.ptr(t["sorder"]), len(sc.plan_order), N.ptr(self.joined) if n_join else None, n_join,
+            N.ptr(sorder), n_sorder, ostride, N.ptr(jn) if jn is not None else None, n_join,
             N.ptr(t["vram"]), N.ptr(t["reserve"]), N.ptr(t["flops"]), N.ptr(t["token"]),
             N.ptr(kv_reserved) if kv_reserved is not None else None, N.ptr(self.occ), self.G, float(mix_alpha),
             float(cov_threshold), N.ptr(loads), N.ptr(cov), N.ptr(dec), N.ptr(hole), N.stream_handle(self.stream)),
             "ss_membership_triggers")
         return dec, cov, hole, loads
+
+    def rebalance(self, *, cov_threshold: float = 0.5, mix_alpha: float = 0.5, alpha: float = 1.0,
+                  tokens: float = 128.0, force=None):
+        """Global rebalance of the scenarios whose evaluate_triggers() says "global" (or of ``force``).
+
+        Per scenario, as MembershipManager.global_rebalance (membership.py:398-411) and the simulator
+        (sim.py:425-429): allocate() on the churned pool -- all selected scenarios' regions in ONE device
+        Phase-1 batch (stage counts, objective, score, best k, water-fill) -- then apply_plan (new slices,
+        changed_gpus) and the abort of every live chain on a changed GPU (ss_ring_abort).  A scenario whose
+        pool has no feasible pipeline keeps its placement (degraded).
+
+        Returns (replayer for the new placements carrying occupancy / ring / request counters, info) where
+        info has per-scenario "decision", "rebalanced", "degraded", "changed" (GPU indices), "aborted".
+        """
+        import dataclasses
+        from ._phase1 import PoolBatch, PoolSpec, objective_dense
+        torch = self.torch
+        sc = self.scen
+        S, G, L = self.S, self.G, self.L
+        dec = self.triggers(cov_threshold=cov_threshold, mix_alpha=mix_alpha)[0].cpu().numpy()
+        sel = np.nonzero(dec != 0)[0] if force is None else np.asarray(force, dtype=np.int64)
+        absent = self.leave.view(S, G).cpu().numpy().astype(bool)
+        if self.per_scenario:
+            lo = self.lo_s.view(S, G).cpu().numpy().copy()
+            hi = self.hi_s.view(S, G).cpu().numpy().copy()
+        else:
+            lo = np.broadcast_to(sc.slice_lo, (S, G)).astype(np.int32).copy()
+            hi = np.broadcast_to(sc.slice_hi, (S, G)).astype(np.int32).copy()
+        if sc.joins > 0:
+            joined = self.joined.view(S, -1).cpu().numpy().copy()
+        else:
+            joined = np.full((S, 1), -1, dtype=np.int32) if sc.joined_s is None else sc.joined_s.copy()
+        # current slices order per scenario: the plan's then the joins (or the last rebalance's plan order)
+        if sc.slice_order_s is not None:
+            order = sc.slice_order_s.copy()
+        else:
+            order = np.full((S, G), -1, dtype=np.int32)
+            for s in range(S):
+                cur = [g for g in sc.plan_order if not absent[s, g]] + [g for g in joined[s] if g >= 0
+                                                                        and lo[s, g] <= hi[s, g]]
+                order[s, :len(cur)] = cur
+        pools, mats, flops_c, owners = [], [], [], []
+        for s in sel:
+            present = ~absent[s]
+            rtt = sc.scenario_rtt(int(s))
+            for r in range(len(sc.region_names)):
+                idx = np.nonzero(present & (sc.region_idx == r))[0]        # cluster_snapshot(): id order
+                if idx.size == 0:
+                    continue
+                caps = sc.layer_cap[idx].astype(np.int64)
+                limit = min(int(idx.size), int(caps.sum()) // L)
+                if limit < 1:
+                    continue
+                o = np.lexsort((idx, -caps))                                # (-capacity, id) (allocator.py:570)
+                pools.append(PoolSpec(caps[o].tolist(), sc.flops[idx][o].tolist(), L, limit))
+                flops_c.append(sc.flops[idx])
+                mats.append(rtt[np.ix_(idx, idx)])
+                owners.append((int(s), idx[o]))
+        info = {"decision": dec, "rebalanced": np.zeros(S, dtype=bool), "degraded": np.zeros(S, dtype=bool),
+                "changed": [[] for _ in range(S)], "aborted": np.zeros(S, dtype=np.int32)}
+        new_lo, new_hi = lo.copy(), hi.copy()
+        if pools:
+            batch = PoolBatch(pools, stream=self.stream)
+            batch.stage_counts()
+            t, r = objective_dense(flops_c, mats, sc.fpl, L, tokens, stream=self.stream)
+            km = int(batch.km.max())
+            batch.score_and_best(t, r, np.array([0.0] + [float(k ** alpha) for k in range(1, km + 1)]))
+            res = batch.fetch()
+            by_s = {}
+            for p, (s, og) in enumerate(owners):
+                by_s.setdefault(s, []).append((p, og))
+            for s in sel:
+                s = int(s)
+                pipes = []
+                for p, og in by_s.get(s, []):
+                    res.raise_pool(p)
+                    sols = res.solutions(p)
+                    if not sols:
+                        continue
+                    best = int(res.best_k[p])
+                    counts = res.counts_of(p, best)
+                    pos = 0
+                    for grp in sols[best][1]:
+                        cursor = 1
+                        for m in grp:
+                            pipes.append((int(og[m]), cursor, cursor + counts[pos] - 1))
+                            cursor += counts[pos]
+                            pos += 1
+                if not pipes:                                        # NoFeasiblePipeline: keep the slices
+                    info["degraded"][s] = True
+                    continue
+                new_lo[s], new_hi[s] = 0, -1
+                for g, a, b in pipes:
+                    new_lo[s, g], new_hi[s, g] = a, b
+                order[s] = -1
+                order[s, :len(pipes)] = [g for g, _, _ in pipes]
+                info["rebalanced"][s] = True
+        key0 = np.where(lo <= hi, lo.astype(np.int64) * 100000 + hi, -1)
+        key1 = np.where(new_lo <= new_hi, new_lo.astype(np.int64) * 100000 + new_hi, -1)
+        changed = key0 != key1
+        for s in range(S):
+            info["changed"][s] = np.nonzero(changed[s])[0].tolist()
+        if self.window != 0 and changed.any():
+            if self.window < 0:
+                raise ValueError("aborting live chains needs a release window (W > 0)")
+            mark = torch.from_numpy(changed.astype(np.uint8).reshape(-1)).to(self.dev)
+            n_ab = torch.zeros(S, dtype=torch.int32, device=self.dev)
+            N.check(N.lib().ss_ring_abort(S, G, L, self.window, N.ptr(mark), N.ptr(self.occ), N.ptr(self.ring),
+                                          N.ptr(self.next_req), N.ptr(n_ab), None, N.stream_handle(self.stream)),
+                    "ss_ring_abort")
+            info["aborted"] = n_ab.cpu().numpy()
+        new_set = dataclasses.replace(sc, leave=absent, slice_lo_s=new_lo.astype(np.int32),
+                                      slice_hi_s=new_hi.astype(np.int32), device_events=False, joins=0,
+                                      slice_order_s=order, joined_s=joined)
+        rp = ScenarioReplayer(new_set, window=self.window, max_requests=self.occpow_len - 2, stream=self.stream)
+        rp.adopt_state(self)
+        rp.build()
+        return rp, info
+
+    def adopt_state(self, other: "ScenarioReplayer") -> None:
+        """Continue another replayer's request stream (same scenarios, pool and window): occupancy, release
+        ring and request counters move over, the placement stays this replayer's."""
+        if (other.S, other.G, other.L, other.window) != (self.S, self.G, self.L, self.window):
+            raise ValueError("adopt_state needs the same scenarios, pool, depth and window")
+        self.occ.copy_(other.occ)
+        self.ring.copy_(other.ring)
+        self.next_req.copy_(other.next_req)
+
+    def abort_on(self, mark) -> np.ndarray:
+        """Release the live chains touching the marked GPUs ([S, N] bool); returns aborts per scenario."""
+        torch = self.torch
+        m = torch.from_numpy(np.ascontiguousarray(np.asarray(mark, dtype=np.uint8).reshape(-1))).to(self.dev)
+        n_ab = torch.zeros(self.S, dtype=torch.int32, device=self.dev)
+        N.check(N.lib().ss_ring_abort(self.S, self.G, self.L, self.window, N.ptr(m), N.ptr(self.occ),
+                                      N.ptr(self.ring), N.ptr(self.next_req), N.ptr(n_ab), None,
+                                      N.stream_handle(self.stream)), "ss_ring_abort")
+        return n_ab.cpu().numpy()
 
     def raise_first_failure(self) -> None:
         st = self.status.cpu().numpy()

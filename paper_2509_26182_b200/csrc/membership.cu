@@ -170,7 +170,8 @@ __global__ void membership_kernel(int32_t layers, int32_t n_gpus, int32_t n2, co
 
 __global__ void triggers_kernel(int32_t layers, int32_t n_gpus, const uint8_t* absent, const int32_t* lo_s,
                                 const int32_t* hi_s, int64_t slice_stride, const int32_t* gpu_order, int32_t n_order,
-                                const int32_t* slice_order, int32_t n_slice_order, const int32_t* joined,
+                                const int32_t* slice_order, int32_t n_slice_order, int64_t order_stride,
+                                const int32_t* joined,
                                 int32_t n_join, const double* vram, const double* reserve, const double* flops,
                                 const int64_t* token_cap, const int64_t* kv_reserved, const int32_t* occ,
                                 int64_t state_stride, double mix_alpha, double cov_threshold, double* loads_out,
@@ -225,8 +226,12 @@ __global__ void triggers_kernel(int32_t layers, int32_t n_gpus, const uint8_t* a
             const int o = oc ? oc[g] : 0;
             comp = __dadd_rn(comp, __dmul_rn(flops[g], (double)(o < 1 ? o : 1)));
         };
-        for (int i = 0; i < n_slice_order; ++i) visit(slice_order[i]);
-        for (int j = 0; j < n_join && jn; ++j) visit(jn[j]);
+        // slices order: the plan's, then joins (on_join appends); after a rebalance each scenario has its own
+        // plan order (order_stride > 0) that already contains every serving GPU
+        const int32_t* so = slice_order + s * order_stride;
+        for (int i = 0; i < n_slice_order; ++i) visit(so[i]);
+        if (order_stride == 0)
+            for (int j = 0; j < n_join && jn; ++j) visit(jn[j]);
         const double kvf = tmem > 0.0 ? __ddiv_rn(kvb, tmem) : 0.0;
         const double cf = tflops > 0.0 ? __ddiv_rn(comp, tflops) : 0.0;
         loads[l - 1] = __dadd_rn(__dmul_rn(mix_alpha, kvf), __dmul_rn(__dsub_rn(1.0, mix_alpha), cf));
@@ -287,7 +292,8 @@ extern "C" int ss_scenario_membership(int32_t n_scen, int32_t layers, int32_t n_
 extern "C" int ss_membership_triggers(int32_t n_scen, int32_t layers, int32_t n_gpus, const uint8_t* absent,
                                       const int32_t* lo_s, const int32_t* hi_s, int64_t slice_stride,
                                       const int32_t* gpu_order, int32_t n_order, const int32_t* slice_order,
-                                      int32_t n_slice_order, const int32_t* joined, int32_t n_join, const double* vram,
+                                      int32_t n_slice_order, int64_t order_stride, const int32_t* joined, int32_t n_join,
+                                      const double* vram,
                                       const double* reserve, const double* flops, const int64_t* token_cap,
                                       const int64_t* kv_reserved, const int32_t* occ, int64_t state_stride,
                                       double mix_alpha, double cov_threshold, double* loads, double* cov,
@@ -301,10 +307,58 @@ extern "C" int ss_membership_triggers(int32_t n_scen, int32_t layers, int32_t n_
     if (cudaFuncSetAttribute(triggers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SS_CUDA_ERROR;
     triggers_kernel<<<n_scen, 128, smem, ss_stream(stream)>>>(layers, n_gpus, absent, lo_s, hi_s, slice_stride,
-                                                              gpu_order, n_order, slice_order, n_slice_order, joined,
+                                                              gpu_order, n_order, slice_order, n_slice_order,
+                                                              order_stride, joined,
                                                               n_join, vram, reserve, flops, token_cap, kv_reserved,
                                                               occ, state_stride, mix_alpha, cov_threshold, loads, cov,
                                                               decision, first_uncovered);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// abort of live chains (sim.py:401-411 _abort_chains_on): every chain still in the release window that
+// touches a marked GPU is released now (occupancy -1 on each of its distinct GPUs) and its ring slot
+// emptied, so the later release(i - W) is a no-op.  One warp per scenario.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void ring_abort_kernel(int32_t n_gpus, int32_t max_layers, int32_t window, const uint8_t* mark,
+                                  int32_t* occ, int32_t* ring, const int64_t* next_req, int32_t* n_aborted,
+                                  uint8_t* aborted) {
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int stride = max_layers + 1;
+    const uint8_t* mk = mark + (int64_t)s * n_gpus;
+    int32_t* oc = occ + (int64_t)s * n_gpus;
+    int32_t* rg = ring + (int64_t)s * window * stride;
+    const int64_t nr = next_req[s];
+    const int64_t first = nr - window < 0 ? 0 : nr - window;
+    int count = 0;
+    for (int64_t i = first; i < nr; ++i) {                    // request-id order, as sim.py sorts victims
+        int32_t* slot = rg + (int)(i % window) * stride;
+        const int cnt = slot[0];
+        bool hit = false;
+        for (int k = lane; k < cnt; k += 32) hit |= mk[slot[1 + k]] != 0;
+        hit = __any_sync(0xffffffffu, hit);
+        if (hit) {
+            for (int k = lane; k < cnt; k += 32) oc[slot[1 + k]] -= 1;
+            __syncwarp();
+            if (lane == 0) slot[0] = 0;
+            ++count;
+        }
+        if (aborted && lane == 0) aborted[(int64_t)s * window + (int)(i % window)] = hit ? 1 : 0;
+        __syncwarp();
+    }
+    if (lane == 0 && n_aborted) n_aborted[s] = count;
+}
+}  // namespace
+
+extern "C" int ss_ring_abort(int32_t n_scen, int32_t n_gpus, int32_t max_layers, int32_t window, const uint8_t* mark,
+                             int32_t* occ, int32_t* ring, const int64_t* next_req, int32_t* n_aborted,
+                             uint8_t* aborted, void* stream) {
+    if (n_scen <= 0 || window == 0) return SS_OK;            // W = 0 keeps no live chain
+    if (window < 0 || n_gpus < 1 || max_layers < 1 || !mark || !occ || !ring || !next_req) return SS_BAD_INPUT;
+    ring_abort_kernel<<<n_scen, 32, 0, ss_stream(stream)>>>(n_gpus, max_layers, window, mark, occ, ring, next_req,
+                                                            n_aborted, aborted);
     SS_CHECK_LAUNCH();
     return SS_OK;
 }

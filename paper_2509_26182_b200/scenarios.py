@@ -264,6 +264,11 @@ class ScenarioSet:
     vram: Optional[np.ndarray] = None
     reserve: Optional[np.ndarray] = None
     flops: Optional[np.ndarray] = None
+    region_idx: Optional[np.ndarray] = None      # per GPU, index into region_names (sorted)
+    region_names: Tuple[str, ...] = ()
+    fpl: float = 0.0                             # model.flops_per_layer_per_token
+    slice_order_s: Optional[np.ndarray] = None   # [S, n] per-scenario plan.gpu_slices() order (-1 padded)
+    joined_s: Optional[np.ndarray] = None        # [S, joins] join sequence per scenario (-1 padded)
 
     @property
     def n_scenarios(self) -> int:
@@ -358,9 +363,12 @@ def build_scenarios(cluster: ClusterSnapshot, model: ModelSpec, plan, n_scenario
     vram = np.array([by_id[g].vram_bytes for g in ids], dtype=np.float64)
     reserve = np.array([by_id[g].reserve_fraction for g in ids], dtype=np.float64)
     flops = np.array([by_id[g].flops for g in ids], dtype=np.float64)
+    region_names = tuple(sorted({g.region for g in cluster.gpus}))
+    rpos = {r: i for i, r in enumerate(region_names)}
+    region_idx = np.array([rpos[by_id[g].region] for g in ids], dtype=np.int32)
     return ScenarioSet(model.layer_count, ids, rtt, base_tau, lo, hi, seeds, leave, jitter, present0, lo_s, hi_s,
                        churn, joins, token_cap, layer_cap, not host_events, want, cluster_order, plan_order, vram,
-                       reserve, flops)
+                       reserve, flops, region_idx, region_names, model.flops_per_layer_per_token)
 
 
 # ---------------------------------------------------------------------------

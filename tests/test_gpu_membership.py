@@ -123,3 +123,54 @@ def test_device_departures_equal_host_churn_c4(cuda_ready):
     rph = ScenarioReplayer(host, window=64)
     a, b = rp.run(16), rph.run(16)
     assert (a.cost.cpu().numpy() == b.cost.cpu().numpy()).all()
+
+
+@pytest.fixture(scope="module")
+def rebalance_cases():
+    with open(os.path.join(HERE, "golden", "rebalance_cases.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["n64_w8", "c1_w4", "n64_nochange"])
+def test_device_rebalance_loop(cuda_ready, rebalance_cases, name):
+    """route R1 -> device membership events (+ aborts on departing GPUs) -> device triggers -> device
+    allocate() on the churned pools -> abort on changed GPUs -> route R2; == the reference, scenario batch."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    case = rebalance_cases[name]
+    want = case["scenarios"]
+    seeds = [w["seed"] for w in want]
+    full, model, plan, join_ids, _ = pool_for_case(case)
+    W, r1, r2 = case["window"], case["r1"], case["r2"]
+    kw = dict(seeds=seeds, jitter=False, join_pool=join_ids)
+    base = scen.build_scenarios(full, model, plan, len(seeds), churn=0.0, **kw)
+    ev = scen.build_scenarios(full, model, plan, len(seeds), churn=case["churn"], joins=case["joins"],
+                              host_events=False, **kw)
+    rp0 = ScenarioReplayer(base, window=W, max_requests=r1 + r2 + 4)
+    a = rp0.run(r1, gpus=True)
+    rp1 = ScenarioReplayer(ev, window=W, max_requests=r1 + r2 + 4)
+    rp1.build()                                                    # device membership events
+    S, G = rp1.S, rp1.G
+    departed = rp1.leave.view(S, G).cpu().numpy().astype(bool) & ev.present0
+    ab_leave = rp0.abort_on(departed)
+    rp1.adopt_state(rp0)
+    rp2, info = rp1.rebalance(cov_threshold=case["cov_threshold"])
+    b = rp2.run(r2, gpus=True)
+    rp2.raise_first_failure()
+    gpus = np.concatenate([a.gpus.cpu().numpy(), b.gpus.cpu().numpy()], axis=1)
+    cost = np.concatenate([a.cost.cpu().numpy(), b.cost.cpu().numpy()], axis=1)
+    occ = rp2.occ.view(S, G).cpu().numpy()
+    lo = rp2.lo_s.view(S, G).cpu().numpy()
+    hi = rp2.hi_s.view(S, G).cpu().numpy()
+    absent = rp2.leave.view(S, G).cpu().numpy().astype(bool)
+    for s, w in enumerate(want):
+        for r in range(r1 + r2):
+            assert _hops(gpus[s, r].tolist()) == w["chains"][r]["hops"], (name, s, r)
+            assert float(cost[s, r]) == hx(w["chains"][r]["cost"]), (name, s, r)
+        assert DECISION[int(info["decision"][s])] == w["decision"][:2]
+        assert info["changed"][s] == w["changed"]
+        assert int(ab_leave[s]) == len(w["aborted_leave"])
+        assert int(info["aborted"][s]) == len(w["aborted_rebalance"])
+        assert occ[s].tolist() == w["occ"]
+        got = sorted([g, int(lo[s, g]), int(hi[s, g])] for g in range(G) if not absent[s, g] and lo[s, g] <= hi[s, g])
+        assert got == w["slices"]
