@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--c5-scenarios", type=int, default=4096, help="C5 scenarios per sub-pool (whole job)")
     ap.add_argument("--c5-steps", type=int, default=8)
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--c2-requests", type=int, default=20000)
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
@@ -305,6 +306,7 @@ def run_ours(args):
 
     c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
+    reb = None if args.no_rebalance else run_rebalance(args, rank, world, stream, barrier, reduce_max)
 
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None
@@ -343,6 +345,7 @@ def run_ours(args):
             "phase1": p1,
             "c5": c5,
             "c2": c2,
+            "rebalance": reb,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -400,6 +403,61 @@ def run_c5(args, rank, world, stream, barrier, reduce_max):
                                     for (name, cl, model), plan, rp in zip(pools, plans, reps)],
                       "scenarios_per_sub_pool": args.c5_scenarios, "parallelism": f"scenario-sharded x{world}"}}
     del reps, outs
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_rebalance(args, rank, world, stream, barrier, reduce_max):
+    """SURVEY.md 8(f) rows 1-2 at C4 scale: route R requests, then per scenario the membership events on device
+    (5% departures with their chains aborted, 4 joins from a 16-GPU join pool), evaluate_triggers on device,
+    global rebalance of every scenario whose decision is global (one Phase-1 batch over all churned pools,
+    apply_plan, abort of the chains on changed GPUs), and R more requests on the new placements."""
+    import torch
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    R, W, S = args.requests_per_step, args.window, args.scenarios_per_gpu
+    thr = 0.02                       # low CoV threshold: every scenario takes the global path
+    rc = scen.default_region_count(256)
+    full, model = scen.synthetic_cluster(256 + 16, seed=0, model=scen.bench_model(64), region_count=rc)
+    base, _ = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64), region_count=rc)
+    plan = allocate(base, model)
+    seeds = shard(S, rank, world)
+    kw = dict(seeds=seeds, jitter=True, join_pool=[g.id for g in full.gpus[256:]])
+    b = scen.build_scenarios(full, model, plan, len(seeds), churn=0.0, **kw)
+    e = scen.build_scenarios(full, model, plan, len(seeds), churn=0.05, joins=4, host_events=False, **kw)
+    with torch.cuda.stream(stream):
+        rp0 = ScenarioReplayer(b, window=W, stream=stream)
+        rp1 = ScenarioReplayer(e, window=W, stream=stream)
+        rp0.run(R)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        rp1.build()                                               # device membership events
+        dep = rp1.leave.view(rp1.S, rp1.G).cpu().numpy().astype(bool) & e.present0
+        rp0.abort_on(dep)
+        rp1.adopt_state(rp0)
+        rp2, info = rp1.rebalance(cov_threshold=thr)
+        torch.cuda.synchronize()
+        t_reb = reduce_max(time.perf_counter() - t0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rp2.run(R)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rp2.raise_first_failure()
+        t_route = reduce_max(e0.elapsed_time(e1) / 1e3)
+    n = len(seeds) * world
+    res = {"metric": "rebalance loop: scenarios re-placed per second (whole job)", "value": n / t_reb,
+           "unit": "scenarios/s", "rebalance_ms": 1e3 * t_reb, "route_after_sel_per_s": len(seeds) * R * world / t_route,
+           "rebalanced_fraction": float(info["rebalanced"].mean()),
+           "changed_gpus_mean": float(np.mean([len(c) for c in info["changed"]])),
+           "aborted_chains_mean": float(info["aborted"].mean()), "kernel_after": rp2.mode,
+           "config": {"workload": "C4 pool + 16-GPU join pool: %d scenarios x (R=%d routes, device membership events: "
+                                  "5%% departures + 4 joins, device triggers, global rebalance = device allocate() of "
+                                  "every churned pool, abort on changed GPUs, R more routes), W=%d" % (n, R, W),
+                      "parallelism": f"scenario-sharded x{world}"}}
+    del rp0, rp1, rp2
     torch.cuda.empty_cache()
     return res
 

@@ -239,6 +239,14 @@ int ss_objective(int32_t n_items, const int32_t* item_ptr, const double* flops, 
                  const double* rtt, double fpl, const int32_t* layers, double tokens, double* out_t,
                  double* out_r, void* stream);
 
+/* estimate_objective_params of regions gathered from one pool: region item i =
+ * pool GPUs gpu[item_ptr[i] .. item_ptr[i+1]) in cluster order, flops from
+ * pool_flops, rtt_s(a, b) = base_rtt[a * n_pool + b] times the scenarios.py
+ * pair jitter of seeds[i] when seeds != NULL.  Same arithmetic as ss_objective. */
+int ss_objective_pool(int32_t n_items, const int32_t* item_ptr, const int32_t* gpu, const double* pool_flops,
+                      const double* base_rtt, int32_t n_pool, const int64_t* seeds, double fpl, const int32_t* layers,
+                      double tokens, double* out_t, double* out_r, void* stream);
+
 /* score (allocator.py:104-111) of every (pool, k) candidate, z[koff[p]+k-1] =
  * kpow[k] / (t + (s/k) * r) with kpow[k] = k**alpha from the host; with
  * fill_all != 0 every present k's groups are also water-filled

@@ -206,6 +206,18 @@ class PoolResults:
             out[k] = (s, tuple(groups))
         return out
 
+    def best_groups(self, p: int):
+        """(member arrays of the groups of the best k, water-filled layer counts in the same order) or None."""
+        b = self.b
+        k = int(self.best_k[p])
+        if k < 1 or int(self.stages[b.koff_h[p] + k - 1]) == 0:
+            return None
+        n, km = int(b.n[p]), int(b.km[p])
+        base = int(b.memb_h[p] + (k - 1) * n)
+        total = int(self.stages[b.koff_h[p] + k - 1])
+        sizes = self.gsize[int(b.gsz_h[p] + (k - 1) * km): int(b.gsz_h[p] + (k - 1) * km) + k]
+        return self.members[base: base + total], sizes, self.counts[base: base + total]
+
     def z_of(self, p: int, k: int) -> float:
         return float(self.z[self.b.koff_h[p] + k - 1])
 

@@ -354,7 +354,7 @@ class ScenarioReplayer:
         info has per-scenario "decision", "rebalanced", "degraded", "changed" (GPU indices), "aborted".
         """
         import dataclasses
-        from ._phase1 import PoolBatch, PoolSpec, objective_dense
+        from ._phase1 import PoolBatch, PoolSpec
         torch = self.torch
         sc = self.scen
         S, G, L = self.S, self.G, self.L
@@ -380,10 +380,9 @@ class ScenarioReplayer:
                 cur = [g for g in sc.plan_order if not absent[s, g]] + [g for g in joined[s] if g >= 0
                                                                         and lo[s, g] <= hi[s, g]]
                 order[s, :len(cur)] = cur
-        pools, mats, flops_c, owners = [], [], [], []
+        pools, items, item_seed, owners = [], [], [], []
         for s in sel:
             present = ~absent[s]
-            rtt = sc.scenario_rtt(int(s))
             for r in range(len(sc.region_names)):
                 idx = np.nonzero(present & (sc.region_idx == r))[0]        # cluster_snapshot(): id order
                 if idx.size == 0:
@@ -394,8 +393,8 @@ class ScenarioReplayer:
                     continue
                 o = np.lexsort((idx, -caps))                                # (-capacity, id) (allocator.py:570)
                 pools.append(PoolSpec(caps[o].tolist(), sc.flops[idx][o].tolist(), L, limit))
-                flops_c.append(sc.flops[idx])
-                mats.append(rtt[np.ix_(idx, idx)])
+                items.append(idx)
+                item_seed.append(int(sc.seeds[s]))
                 owners.append((int(s), idx[o]))
         info = {"decision": dec, "rebalanced": np.zeros(S, dtype=bool), "degraded": np.zeros(S, dtype=bool),
                 "changed": [[] for _ in range(S)], "aborted": np.zeros(S, dtype=np.int32)}
@@ -403,7 +402,21 @@ class ScenarioReplayer:
         if pools:
             batch = PoolBatch(pools, stream=self.stream)
             batch.stage_counts()
-            t, r = objective_dense(flops_c, mats, sc.fpl, L, tokens, stream=self.stream)
+            # estimate_objective_params per churned region, gathered from the pool on device (no dense copies)
+            n_it = len(items)
+            iptr = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int32)
+            up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=self.dev, dtype=dt)
+            if not hasattr(self, "_pool_flops"):
+                self._pool_flops = up(sc.flops, torch.float64)
+            t = torch.empty(n_it, dtype=torch.float64, device=self.dev)
+            r = torch.empty(n_it, dtype=torch.float64, device=self.dev)
+            ip_d, g_d = up(iptr, torch.int32), up(np.concatenate(items), torch.int32)
+            lay_d = torch.full((n_it,), L, dtype=torch.int32, device=self.dev)
+            seed_d = up(np.array(item_seed, dtype=np.int64), torch.int64) if sc.jitter else None
+            N.check(N.lib().ss_objective_pool(n_it, N.ptr(ip_d), N.ptr(g_d), N.ptr(self._pool_flops),
+                                              N.ptr(self.base_rtt), G, N.ptr(seed_d) if seed_d is not None else None,
+                                              float(sc.fpl), N.ptr(lay_d), float(tokens), N.ptr(t), N.ptr(r),
+                                              N.stream_handle(self.stream)), "ss_objective_pool")
             km = int(batch.km.max())
             batch.score_and_best(t, r, np.array([0.0] + [float(k ** alpha) for k in range(1, km + 1)]))
             res = batch.fetch()
@@ -412,29 +425,30 @@ class ScenarioReplayer:
                 by_s.setdefault(s, []).append((p, og))
             for s in sel:
                 s = int(s)
-                pipes = []
+                gs, starts, ends = [], [], []
                 for p, og in by_s.get(s, []):
                     res.raise_pool(p)
-                    sols = res.solutions(p)
-                    if not sols:
+                    bg = res.best_groups(p)
+                    if bg is None:
                         continue
-                    best = int(res.best_k[p])
-                    counts = res.counts_of(p, best)
-                    pos = 0
-                    for grp in sols[best][1]:
-                        cursor = 1
-                        for m in grp:
-                            pipes.append((int(og[m]), cursor, cursor + counts[pos] - 1))
-                            cursor += counts[pos]
-                            pos += 1
-                if not pipes:                                        # NoFeasiblePipeline: keep the slices
+                    members, sizes, counts = bg
+                    # contiguous slices from layer 1 inside every group (allocator.py:595-606)
+                    ends_all = np.cumsum(counts)
+                    grp_start = np.repeat(np.concatenate([[0], np.cumsum(sizes)[:-1]]), sizes)
+                    before = np.concatenate([[0], ends_all])[grp_start]
+                    e = ends_all - before
+                    gs.append(og[members])
+                    starts.append(e - counts + 1)
+                    ends.append(e)
+                if not gs:                                           # NoFeasiblePipeline: keep the slices
                     info["degraded"][s] = True
                     continue
+                g_all = np.concatenate(gs)
                 new_lo[s], new_hi[s] = 0, -1
-                for g, a, b in pipes:
-                    new_lo[s, g], new_hi[s, g] = a, b
+                new_lo[s, g_all] = np.concatenate(starts)
+                new_hi[s, g_all] = np.concatenate(ends)
                 order[s] = -1
-                order[s, :len(pipes)] = [g for g, _, _ in pipes]
+                order[s, :g_all.size] = g_all
                 info["rebalanced"][s] = True
         key0 = np.where(lo <= hi, lo.astype(np.int64) * 100000 + hi, -1)
         key1 = np.where(new_lo <= new_hi, new_lo.astype(np.int64) * 100000 + new_hi, -1)

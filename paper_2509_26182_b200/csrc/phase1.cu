@@ -834,6 +834,37 @@ __global__ void objective_kernel(int32_t n_items, const int32_t* item_ptr, const
     out_r[it] = cnt ? __ddiv_rn(s.value(), (double)cnt) : 0.0;
 }
 
+// Same arithmetic as objective_kernel with the region gathered from a pool: flops[gpu[i]] in cluster order and
+// rtt_s(a, b) = base_rtt[a][b] (x the scenario's pair jitter when a seed is given, scenarios.py), so churned pools
+// of many scenarios need no per-scenario dense matrices.
+__global__ void objective_pool_kernel(int32_t n_items, const int32_t* item_ptr, const int32_t* gpu,
+                                      const double* pool_flops, const double* base_rtt, int32_t n_pool,
+                                      const int64_t* seeds, double fpl, const int32_t* layers, double tokens,
+                                      double* out_t, double* out_r) {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= n_items) return;
+    const int off = item_ptr[it], n = item_ptr[it + 1] - off;
+    const int32_t* g = gpu + off;
+    PySum inv;
+    inv.init();
+    for (int i = 0; i < n; ++i) inv.add_float(__ddiv_rn(1.0, pool_flops[g[i]]));
+    const double harmonic = __ddiv_rn((double)n, inv.value());
+    const double t = __ddiv_rn(__dmul_rn(__dmul_rn(fpl, (double)layers[it]), tokens), harmonic);
+    const uint64_t mix = seeds ? ss_splitmix64((uint64_t)seeds[it]) : 0;
+    PySum s;
+    s.init();
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            if (a == b) continue;
+            double v = base_rtt[(int64_t)g[a] * n_pool + g[b]];
+            if (seeds) v = __dmul_rn(v, ss_jitter(mix, (uint32_t)g[a], (uint32_t)g[b]));
+            s.add_float(v);
+        }
+    const long long cnt = (long long)n * (n - 1);
+    out_t[it] = t;
+    out_r[it] = cnt ? __ddiv_rn(s.value(), (double)cnt) : 0.0;
+}
+
 __device__ __forceinline__ int score_one(int k, int s, double kp, double t, double r, double* z) {
     if (k < 1 || s < k) return SS_BAD_INPUT;
     const double denom = __dadd_rn(t, __dmul_rn(__ddiv_rn((double)s, (double)k), r));
@@ -1059,6 +1090,18 @@ extern "C" int ss_objective(int32_t n_items, const int32_t* item_ptr, const doub
     if (n_items <= 0) return SS_OK;
     objective_kernel<<<grid_for(n_items, 64), 64, 0, ss_stream(stream)>>>(n_items, item_ptr, flops, rtt_off, rtt, fpl,
                                                                          layers, tokens, out_t, out_r);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_objective_pool(int32_t n_items, const int32_t* item_ptr, const int32_t* gpu, const double* pool_flops,
+                                 const double* base_rtt, int32_t n_pool, const int64_t* seeds, double fpl,
+                                 const int32_t* layers, double tokens, double* out_t, double* out_r, void* stream) {
+    if (n_items <= 0) return SS_OK;
+    if (!item_ptr || !gpu || !pool_flops || !base_rtt || n_pool < 1 || !layers || !out_t || !out_r)
+        return SS_BAD_INPUT;
+    objective_pool_kernel<<<grid_for(n_items, 64), 64, 0, ss_stream(stream)>>>(
+        n_items, item_ptr, gpu, pool_flops, base_rtt, n_pool, seeds, fpl, layers, tokens, out_t, out_r);
     SS_CHECK_LAUNCH();
     return SS_OK;
 }
