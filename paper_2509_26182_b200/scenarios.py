@@ -169,6 +169,14 @@ def churn_set(seed: int, plan_gpus: Sequence[int], slices: Dict[int, Tuple[int, 
     return sorted(out)
 
 
+TOKEN_SALT = 0x70 << 40
+
+
+def request_tokens(seed: int, i: int, lo: int, hi: int) -> int:
+    """Total tokens (prompt + output) of request i of a scenario: uniform in [lo, hi] from splitmix64."""
+    return lo + splitmix64((splitmix64(seed & MASK64) ^ TOKEN_SALT ^ i) & MASK64) % (hi - lo + 1)
+
+
 LEAVE_SALT = 0xC4 << 40
 JOIN_SALT = 0x4A << 40
 

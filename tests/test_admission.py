@@ -1,0 +1,73 @@
+"""Admission path vs the reference (tests/golden/admission_cases.json).
+
+CPU: the oracle (KV-headroom exclusion as +inf latency, strict FIFO drain) reproduces the reference
+simulator's admission decisions, chains and costs bit for bit.  GPU: ss_admission_warp does the same on device.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import hx
+from helpers_golden import plan_from_golden
+from oracle import admission_ref, alloc_ref, chain_ref
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = ["c1", "c1_tight", "c2", "c2_light", "c2_tight"]
+
+
+@pytest.fixture(scope="module")
+def admission_cases():
+    with open(os.path.join(HERE, "golden", "admission_cases.json")) as fh:
+        return json.load(fh)
+
+
+def _hops(row):
+    out, start = [], 1
+    for layer in range(2, len(row) + 1):
+        if row[layer - 1] != row[layer - 2]:
+            out.append([row[layer - 2], start, layer - 1])
+            start = layer
+    out.append([row[-1], start, len(row)])
+    return out
+
+
+def scenario_set(case, seeds):
+    from paper_2509_26182_b200 import scenarios as scen
+    cl, model = scen.synthetic_cluster(case["n"], seed=0, model=scen.bench_model(case["L"]))
+    d = alloc_ref.allocate(cl, model)
+    d["objective"] = d["objective"].hex()
+    d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+    plan = plan_from_golden(d)
+    return scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.0, jitter=False)
+
+
+def check(case, want, admitted, queue_left, kv, occ):
+    for i, w in enumerate(want["admitted"]):
+        got = admitted[i]
+        if w is None:
+            assert got is None, i
+            continue
+        step, gpus, cost = got
+        assert step == w["step"], i
+        assert _hops(gpus) == w["hops"], i
+        assert cost == hx(w["cost"]), i
+    assert list(queue_left) == want["queue_left"]
+    assert [int(x) for x in kv] == want["kv"]
+    assert [int(x) for x in occ] == want["occ"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_admission_matches_reference(admission_cases, name):
+    from paper_2509_26182_b200 import scenarios as scen
+    case = admission_cases[name]
+    seeds = [w["seed"] for w in case["scenarios"]]
+    ss = scenario_set(case, seeds)
+    for s, want in enumerate(case["scenarios"]):
+        toks = [scen.request_tokens(want["seed"], i, case["tok_lo"], case["tok_hi"]) for i in range(case["steps"])]
+        got = admission_ref.admission_replay(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap, toks,
+                                             case["steps"], case["window"],
+                                             chain_ref.occ_power_table(case["steps"] + 4))
+        check(case, want, *got)
