@@ -180,6 +180,24 @@ int ss_ring_abort(int32_t n_scen, int32_t n_gpus, int32_t max_layers, int32_t wi
                   int32_t* occ, int32_t* ring, const int64_t* next_req, int32_t* n_aborted, uint8_t* aborted,
                   void* stream);
 
+/* Admission path (sim.py:319-366) per scenario on a time-free step schedule,
+ * for DAGs with <= 32 hosts per layer (one warp per scenario, edges resident):
+ * at step t the requests admitted at step t - W complete (occupancy -1 and
+ * tokens released on their distinct GPUs), request t joins the queue, and the
+ * queue drains strictly FIFO: the head (tokens uniform in [tok_lo, tok_hi]
+ * from its scenario seed, scenarios.request_tokens) is routed with every GPU
+ * whose token_cap - reserved < tokens excluded, reserves its tokens and +1
+ * occupancy on the chain's distinct GPUs, and the drain stops at the first
+ * head with no finite chain.  Occupancy and reservations start at 0.
+ * Outputs per request (stride steps): step_out (admission step, -1 = still
+ * queued), cost_out, gpus_out (optional); per GPU: kv_out, occ_out.
+ * adm_gpus is scratch of n_dags * steps * (max_layers + 1) int32. */
+int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* base_tau, const int64_t* token_cap,
+                      const double* occpow, int32_t occpow_len, const int64_t* seeds, int32_t tok_lo, int32_t tok_hi,
+                      int32_t steps, int32_t window, int32_t* adm_gpus, int32_t* step_out, double* cost_out,
+                      int16_t* gpus_out, int64_t* kv_out, int32_t* occ_out, int32_t* status, int32_t* aux,
+                      void* stream);
+
 /* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
  * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring
  * and state staged in shared memory once per launch; no CTA barriers on the

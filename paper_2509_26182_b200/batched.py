@@ -472,6 +472,38 @@ class ScenarioReplayer:
         rp.build()
         return rp, info
 
+    def admit(self, steps: int, *, tok_lo: int, tok_hi: int, gpus: bool = False):
+        """The simulator's admission path (sim.py:319-366) for every scenario on device (ss_admission_warp):
+        step t completes the admissions of step t - W, enqueues request t and drains the queue strictly FIFO,
+        each head routed with the KV-blocked GPUs excluded.  Needs mode "warp" (<= 32 hosts per layer); starts
+        from zero occupancy / reservations.  Returns dict of device tensors: step [S, steps] (-1 = still
+        queued), cost [S, steps], gpus [S, steps, L] (optional), kv [S, N], occ [S, N].
+        """
+        torch = self.torch
+        if self.mode != "warp":
+            raise ValueError("admission replay runs on the warp-resident kernel (<= 32 hosts per layer)")
+        if self.window < 1:
+            raise ValueError("admission needs a completion window W >= 1")
+        if not self.built:
+            self.build()
+        S, G, L = self.S, self.G, self.L
+        if not hasattr(self, "_tokcap"):
+            self._tokcap = torch.from_numpy(np.tile(self.scen.token_cap, S)).to(self.dev)
+        occpow = torch.from_numpy(occ_power_table(steps + 2)).to(self.dev)
+        adm = torch.empty(S * steps * (L + 1), dtype=torch.int32, device=self.dev)
+        out = {"step": torch.empty((S, steps), dtype=torch.int32, device=self.dev),
+               "cost": torch.empty((S, steps), dtype=torch.float64, device=self.dev),
+               "gpus": torch.empty((S, steps, L), dtype=torch.int16, device=self.dev) if gpus else None,
+               "kv": torch.empty((S, G), dtype=torch.int64, device=self.dev),
+               "occ": torch.empty((S, G), dtype=torch.int32, device=self.dev)}
+        N.check(N.lib().ss_admission_warp(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau),
+                                          N.ptr(self._tokcap), N.ptr(occpow), steps + 2, N.ptr(self.seeds),
+                                          int(tok_lo), int(tok_hi), int(steps), self.window, N.ptr(adm),
+                                          N.ptr(out["step"]), N.ptr(out["cost"]), N.ptr(out["gpus"]), N.ptr(out["kv"]),
+                                          N.ptr(out["occ"]), N.ptr(self.status), N.ptr(self.aux),
+                                          N.stream_handle(self.stream)), "ss_admission_warp")
+        return out
+
     def adopt_state(self, other: "ScenarioReplayer") -> None:
         """Continue another replayer's request stream (same scenarios, pool and window): occupancy, release
         ring and request counters move over, the placement stays this replayer's."""

@@ -26,7 +26,7 @@ constexpr unsigned FULL = 0xffffffffu;
 struct WarpLayout {
     int e_cap, ring_len, pow_len;
     int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
-        off_ring, off_pow, off_cost, total;
+        off_ring, off_pow, off_cost, off_kv, off_tcap, total;
 };
 
 struct WarpReplay {
@@ -41,6 +41,111 @@ struct WarpReplay {
 
 __device__ __forceinline__ void lexmin(double& v, int& i, double v2, int i2) {
     if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+
+// Stages one DAG's host columns and edge blocks into shared memory (compact, row-major per boundary).
+// Returns false (warp-uniform) when a column exceeds 32 hosts or the edges exceed the layout.
+__device__ bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l0, int nl, double* E, int* node, int* cl,
+                          int* noff, int* eoff, int lane) {
+    const int nblk = nl - 1;
+    for (int l = lane; l < nl; l += 32) cl[l] = D.col_len[l0 + l];
+    __syncwarp();
+    if (lane == 0) {
+        int n = 0, e = 0, bad = 0;
+        for (int l = 0; l < nl; ++l) {
+            if (cl[l] > 32) bad = 1;
+            noff[l] = n;
+            n += cl[l];
+            if (l < nblk) {
+                eoff[l] = e;
+                e += cl[l] * cl[l + 1];
+            }
+        }
+        if (e > A.e_cap) bad = 1;
+        cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
+    }
+    __syncwarp();
+    if (cl[nl]) return false;
+    for (int l = 0; l < nl; ++l) {
+        const int len = cl[l];
+        if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
+        if (l < nblk) {
+            const double* src = D.edge_val + D.edge_off[l0 + l];
+            const int cnt = len * cl[l + 1];
+            for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// Chain DP of one request on a warp-resident DAG (router.py:163-197): lane j owns host j of the next column;
+// candidates c_i + E_b[i][j] eight sources at a time (independent loads / DADDs) and a first-index tournament
+// (left operand = lower positions, loses only to a strictly smaller right value), groups merged in ascending
+// order with the same rule == numpy first-index argmin; cost = (c_i + r_ij) + tau_j.  Returns the chain cost
+// (+inf: no path); when finite, picks[l] (shared memory) holds the chosen position of every layer.
+__device__ double warp_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
+                             int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, int lane) {
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    double* cur = costs;                                     // 32 hosts + 8 pad for the group loop
+    double* nxt = costs + 40;
+    cur[lane] = lane < cl[0] ? tau[node[lane]] : INF;
+    __syncwarp();
+    double c = cur[lane];
+    for (int b = 0; b < nblk; ++b) {
+        const int rs = cl[b], rd = cl[b + 1];
+        const bool act = lane < rd;
+        const double tdst = act ? tau[node[noff[b + 1] + lane]] : 0.0;
+        const double* ep = E + eoff[b] + lane;
+        double best = INF;
+        int bi = 0;                                          // +inf everywhere -> 0 == np.argmin
+        for (int g0 = 0; g0 < rs; g0 += 8) {
+            double a[8];
+            int ix[8];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                const double2 c2 = *reinterpret_cast<const double2*>(cur + g0 + q);
+                const double e0 = (act && g0 + q < rs) ? ep[q * rd] : INF;
+                const double e1 = (act && g0 + q + 1 < rs) ? ep[(q + 1) * rd] : INF;
+                a[q] = __dadd_rn(c2.x, e0);
+                a[q + 1] = __dadd_rn(c2.y, e1);
+                ix[q] = g0 + q;
+                ix[q + 1] = g0 + q + 1;
+            }
+#pragma unroll
+            for (int st = 1; st < 8; st *= 2) {
+#pragma unroll
+                for (int q = 0; q < 8; q += 2 * st) {
+                    if (a[q + st] < a[q]) { a[q] = a[q + st]; ix[q] = ix[q + st]; }
+                }
+            }
+            if (a[0] < best) { best = a[0]; bi = ix[0]; }
+            ep += 8 * rd;
+        }
+        if (act) bp[b * 32 + lane] = (uint8_t)bi;
+        c = act ? __dadd_rn(best, tdst) : INF;
+        nxt[lane] = c;
+        __syncwarp();
+        double* t = cur; cur = nxt; nxt = t;
+    }
+    double v = c;
+    int idx = lane < cl[nblk] ? lane : NONE;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(FULL, v, o);
+        const int i2 = __shfl_xor_sync(FULL, idx, o);
+        lexmin(v, idx, v2, i2);
+    }
+    if (lane == 0 && v <= DBL_MAX) {
+        int p = idx;
+        picks[nblk] = p;
+        for (int b = nblk - 1; b >= 0; --b) {
+            p = bp[b * 32 + p];
+            picks[b] = p;
+        }
+    }
+    __syncwarp();
+    return v;
 }
 
 __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
@@ -68,35 +173,9 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
     double* costs = reinterpret_cast<double*>(smem + A.off_cost);   // [2][40] column costs (32 hosts + 8 pad)
 
     // ---- one-time staging: columns, edges, per-GPU state, ring --------------
-    for (int l = lane; l < nl; l += 32) cl[l] = D.col_len[l0 + l];
-    __syncwarp();
-    if (lane == 0) {
-        int n = 0, e = 0, bad = 0;
-        for (int l = 0; l < nl; ++l) {
-            if (cl[l] > 32) bad = 1;
-            noff[l] = n;
-            n += cl[l];
-            if (l < nblk) {
-                eoff[l] = e;
-                e += cl[l] * cl[l + 1];
-            }
-        }
-        if (e > A.e_cap) bad = 1;
-        cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
-    }
-    __syncwarp();
-    if (cl[nl]) {
+    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane)) {
         if (lane == 0) R.st.status[dag] = SS_BAD_INPUT;
         return;
-    }
-    for (int l = 0; l < nl; ++l) {
-        const int len = cl[l];
-        if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
-        if (l < nblk) {
-            const double* src = D.edge_val + D.edge_off[l0 + l];
-            const int cnt = len * cl[l + 1];
-            for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
-        }
     }
     const int gbase = R.st.gpu_ptr[dag];
     const int ng = R.st.gpu_ptr[dag + 1] - gbase;
@@ -154,72 +233,10 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
         }
         __syncwarp();
         mark(0);
-        // ---- DP over the layer columns -------------------------------------------
-        double* cur = costs;
-        double* nxt = costs + 40;
-        cur[lane] = lane < cl[0] ? tau[node[lane]] : INF;
-        __syncwarp();
-        double c = cur[lane];
-        for (int b = 0; b < nblk; ++b) {
-            const int rs = cl[b], rd = cl[b + 1];
-            const bool act = lane < rd;
-            const double tdst = act ? tau[node[noff[b + 1] + lane]] : 0.0;
-            const double* ep = E + eoff[b] + lane;
-            // groups of 8 sources: independent loads / DADDs and a first-index tournament per group (left
-            // operand = lower positions, loses only to a strictly smaller right value); groups merged in
-            // ascending order with the same strict rule
-            double best = INF;
-            int bi = 0;                                          // +inf everywhere -> 0 == np.argmin
-            for (int g0 = 0; g0 < rs; g0 += 8) {
-                double a[8];
-                int ix[8];
-#pragma unroll
-                for (int q = 0; q < 8; q += 2) {
-                    const double2 c2 = *reinterpret_cast<const double2*>(cur + g0 + q);
-                    const double e0 = (act && g0 + q < rs) ? ep[q * rd] : INF;
-                    const double e1 = (act && g0 + q + 1 < rs) ? ep[(q + 1) * rd] : INF;
-                    a[q] = __dadd_rn(c2.x, e0);
-                    a[q + 1] = __dadd_rn(c2.y, e1);
-                    ix[q] = g0 + q;
-                    ix[q + 1] = g0 + q + 1;
-                }
-#pragma unroll
-                for (int st = 1; st < 8; st *= 2) {
-#pragma unroll
-                    for (int q = 0; q < 8; q += 2 * st) {
-                        if (a[q + st] < a[q]) { a[q] = a[q + st]; ix[q] = ix[q + st]; }
-                    }
-                }
-                if (a[0] < best) { best = a[0]; bi = ix[0]; }
-                ep += 8 * rd;
-            }
-            if (act) bp[b * 32 + lane] = (uint8_t)bi;
-            c = act ? __dadd_rn(best, tdst) : INF;
-            nxt[lane] = c;
-            __syncwarp();
-            double* t = cur; cur = nxt; nxt = t;
-        }
+        // ---- DP over the layer columns + final argmin / backtrack ------------------
+        const double v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
         mark(1);
-        // ---- final argmin (first index) + backtrack --------------------------------
-        double v = c;
-        int idx = lane < cl[nblk] ? lane : NONE;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double v2 = __shfl_xor_sync(FULL, v, o);
-            const int i2 = __shfl_xor_sync(FULL, idx, o);
-            lexmin(v, idx, v2, i2);
-        }
-        if (lane == 0) {
-            if (R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
-            if (v <= DBL_MAX) {
-                int p = idx;
-                picks[nblk] = p;
-                for (int b = nblk - 1; b >= 0; --b) {
-                    p = bp[b * 32 + p];
-                    picks[b] = p;
-                }
-            }
-        }
+        if (lane == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         if (!(v <= DBL_MAX)) {
             status = SS_NO_PATH;
             break;
@@ -268,6 +285,160 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
     }
 }
 
+// ---------------------------------------------------------------------------
+// Admission path (sim.py:319-366) on the step schedule of tests/golden/make_admission_golden.py:
+// at step t the chains admitted at step t - W complete (release + release_kv), request t joins the
+// queue, and the queue drains strictly FIFO -- the head is routed with every GPU whose KV headroom
+// (ram_token_capacity - reserved) is below its tokens excluded (+inf latency: the same chain as
+// removing it from the columns), reserves its tokens on the chain's distinct GPUs, and the drain stops
+// at the first head without a finite chain.  Strict FIFO admits in arrival order, so request i's
+// admission record lives at index i.
+// ---------------------------------------------------------------------------
+struct AdmissionArgs {
+    const int32_t* gpu_ptr;
+    const double* base_tau;
+    const int64_t* token_cap;
+    const double* occpow;
+    int32_t occpow_len;
+    const int64_t* seeds;
+    int32_t tok_lo, tok_hi, steps, window;
+    int32_t* adm_gpus;
+    int32_t* step_out;
+    double* cost_out;
+    int16_t* gpus_out;
+    int64_t* kv_out;
+    int32_t* occ_out;
+    int32_t* status;
+    int32_t* aux;
+};
+
+__device__ __forceinline__ long long request_tokens(uint64_t mix, int i, int lo, int hi) {
+    return (long long)lo +
+           (long long)(ss_splitmix64(mix ^ (0x70ull << 40) ^ (uint64_t)i) % (uint64_t)(hi - lo + 1));
+}
+
+__global__ void __launch_bounds__(32) admission_warp_kernel(ss_dag_set D, WarpLayout A, AdmissionArgs Q) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int dag = blockIdx.x;
+    const int lane = threadIdx.x;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const int l0 = D.layer_ptr[dag];
+    const int nl = D.layer_ptr[dag + 1] - l0;
+    const int nblk = nl - 1;
+    double* E = reinterpret_cast<double*>(smem + A.off_E);
+    int* node = reinterpret_cast<int*>(smem + A.off_node);
+    int* cl = reinterpret_cast<int*>(smem + A.off_cl);
+    int* noff = reinterpret_cast<int*>(smem + A.off_noff);
+    int* eoff = reinterpret_cast<int*>(smem + A.off_eoff);
+    uint8_t* bp = smem + A.off_bp;
+    int* picks = reinterpret_cast<int*>(smem + A.off_picks);
+    double* tau = reinterpret_cast<double*>(smem + A.off_tau);
+    double* base = reinterpret_cast<double*>(smem + A.off_base);
+    int* occ = reinterpret_cast<int*>(smem + A.off_occ);
+    int* stamp = reinterpret_cast<int*>(smem + A.off_stamp);
+    double* pw = reinterpret_cast<double*>(smem + A.off_pow);
+    double* costs = reinterpret_cast<double*>(smem + A.off_cost);
+    long long* kv = reinterpret_cast<long long*>(smem + A.off_kv);
+    long long* tcap = reinterpret_cast<long long*>(smem + A.off_tcap);
+    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane)) {
+        if (lane == 0) Q.status[dag] = SS_BAD_INPUT;
+        return;
+    }
+    const int gbase = Q.gpu_ptr[dag];
+    const int ng = Q.gpu_ptr[dag + 1] - gbase;
+    for (int g = lane; g < ng; g += 32) {
+        occ[g] = 0;
+        kv[g] = 0;
+        stamp[g] = 0;
+        base[g] = Q.base_tau[gbase + g];
+        tcap[g] = Q.token_cap[gbase + g];
+    }
+    for (int o = lane; o < A.pow_len; o += 32) pw[o] = Q.occpow[o];
+    if (lane < 8) { costs[32 + lane] = INF; costs[72 + lane] = INF; }
+    __syncwarp();
+    const uint64_t mix = ss_splitmix64((uint64_t)Q.seeds[dag]);
+    const int steps = Q.steps, W = Q.window;
+    const int stride = D.max_layers + 1;
+    int32_t* adm = Q.adm_gpus + (int64_t)dag * steps * stride;
+    int32_t* step_out = Q.step_out + (int64_t)dag * steps;
+    int head = 0, done_head = 0, status = SS_OK, aux = 0;
+    for (int t = 0; t < steps && status == SS_OK; ++t) {
+        // completions: admissions of step t - W, in admission order (sim.py:353-357)
+        while (done_head < head && step_out[done_head] == t - W) {
+            const int32_t* slot = adm + (int64_t)done_head * stride;
+            const int cnt = slot[0];
+            const long long tok = request_tokens(mix, done_head, Q.tok_lo, Q.tok_hi);
+            for (int k = lane; k < cnt; k += 32) {
+                occ[slot[1 + k]] -= 1;
+                kv[slot[1 + k]] -= tok;
+            }
+            __syncwarp();
+            ++done_head;
+        }
+        // request t arrived: drain the queue [head, t] strictly FIFO (sim.py:345-351, 361-366)
+        while (head <= t) {
+            const long long tok = request_tokens(mix, head, Q.tok_lo, Q.tok_hi);
+            int err = 0, errg = 0;
+            for (int g = lane; g < ng; g += 32) {
+                const int o = occ[g];
+                if (o >= Q.occpow_len) { err = SS_BAD_INPUT; errg = g; }
+                const int oc = o >= Q.occpow_len ? Q.occpow_len - 1 : o;
+                const double live = base[g] * (oc < A.pow_len ? pw[oc] : Q.occpow[oc]);
+                tau[g] = tcap[g] - kv[g] < tok ? INF : live;      // KV-blocked GPUs are excluded (sim.py:321-325)
+            }
+            const unsigned em = __ballot_sync(FULL, err != 0);
+            if (em) {
+                status = __shfl_sync(FULL, err, __ffs(em) - 1);
+                aux = __shfl_sync(FULL, errg, __ffs(em) - 1);
+                break;
+            }
+            __syncwarp();
+            const double v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+            if (!(v <= DBL_MAX)) break;                          // UncoveredLayer / NoPath: the head waits
+            // admit: reserve the tokens and +1 occupancy on the chain's distinct GPUs (sim.py:330-331)
+            int32_t* slot = adm + (int64_t)head * stride;
+            const int tag = head + 1;
+            int cnt = 0;
+            for (int c0 = 0; c0 < nl; c0 += 32) {
+                const int l = c0 + lane;
+                int g = 0;
+                bool first = false;
+                if (l < nl) {
+                    g = node[noff[l] + picks[l]];
+                    if (Q.gpus_out) Q.gpus_out[((int64_t)dag * steps + head) * D.max_layers + l] = (int16_t)g;
+                    first = atomicExch(&stamp[g], tag) != tag;
+                }
+                const unsigned m = __ballot_sync(FULL, first);
+                if (first) {
+                    occ[g] += 1;
+                    kv[g] += tok;
+                    slot[1 + cnt + __popc(m & ((1u << lane) - 1u))] = g;
+                }
+                cnt += __popc(m);
+            }
+            if (lane == 0) {
+                slot[0] = cnt;
+                step_out[head] = t;
+                Q.cost_out[(int64_t)dag * steps + head] = v;
+            }
+            __syncwarp();
+            ++head;
+        }
+    }
+    for (int i = head + lane; i < steps; i += 32) {              // still queued at the end
+        step_out[i] = -1;
+        Q.cost_out[(int64_t)dag * steps + i] = INF;
+    }
+    for (int g = lane; g < ng; g += 32) {
+        Q.kv_out[gbase + g] = kv[g];
+        Q.occ_out[gbase + g] = occ[g];
+    }
+    if (lane == 0) {
+        Q.status[dag] = status;
+        Q.aux[dag] = aux;
+    }
+}
+
 inline int align16(int x) { return (x + 15) / 16 * 16; }
 
 bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A) {
@@ -293,6 +464,8 @@ bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLa
     A.off_ring = o;   o += align16(A.ring_len * 4);
     A.off_pow = o;    o += align16(A.pow_len * 8);
     A.off_cost = o;   o += 2 * 40 * 8;
+    A.off_kv = o;     o += align16(D.max_gpus * 8);
+    A.off_tcap = o;   o += align16(D.max_gpus * 8);
     A.total = o;
     return A.total <= 227 * 1024;
 }
@@ -340,5 +513,29 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
                 h[1] / d, h[2] / d);
         cudaFree(R.prof);
     }
+    return SS_OK;
+}
+
+extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* base_tau,
+                                 const int64_t* token_cap, const double* occpow, int32_t occpow_len,
+                                 const int64_t* seeds, int32_t tok_lo, int32_t tok_hi, int32_t steps, int32_t window,
+                                 int32_t* adm_gpus, int32_t* step_out, double* cost_out, int16_t* gpus_out,
+                                 int64_t* kv_out, int32_t* occ_out, int32_t* status, int32_t* aux, void* stream_h) {
+    if (!dags || !gpu_ptr || !base_tau || !token_cap || !occpow || occpow_len < 1 || !seeds || !adm_gpus ||
+        !step_out || !cost_out || !kv_out || !occ_out || !status || !aux)
+        return SS_BAD_INPUT;
+    if (steps < 1 || window < 1 || tok_lo < 0 || tok_hi < tok_lo) return SS_BAD_INPUT;
+    const ss_dag_set& D = *dags;
+    if (D.n_dags <= 0) return SS_OK;
+    if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
+    WarpLayout A{};
+    if (!warp_layout(D, 0, occpow_len, A)) return SS_BAD_INPUT;
+    AdmissionArgs Q{gpu_ptr, base_tau, token_cap, occpow, occpow_len, seeds, tok_lo, tok_hi, steps, window,
+                    adm_gpus, step_out, cost_out, gpus_out, kv_out, occ_out, status, aux};
+    if (cudaFuncSetAttribute(admission_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) !=
+        cudaSuccess)
+        return SS_CUDA_ERROR;
+    admission_warp_kernel<<<D.n_dags, 32, A.total, ss_stream(stream_h)>>>(D, A, Q);
+    SS_CHECK_LAUNCH();
     return SS_OK;
 }

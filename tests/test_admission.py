@@ -71,3 +71,22 @@ def test_oracle_admission_matches_reference(admission_cases, name):
                                              case["steps"], case["window"],
                                              chain_ref.occ_power_table(case["steps"] + 4))
         check(case, want, *got)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_device_admission_matches_reference(cuda_ready, admission_cases, name):
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    case = admission_cases[name]
+    seeds = [w["seed"] for w in case["scenarios"]]
+    ss = scenario_set(case, seeds)
+    rp = ScenarioReplayer(ss, window=case["window"], mode="warp")
+    out = rp.admit(case["steps"], tok_lo=case["tok_lo"], tok_hi=case["tok_hi"], gpus=True)
+    rp.raise_first_failure()
+    step, cost, gpus = out["step"].cpu().numpy(), out["cost"].cpu().numpy(), out["gpus"].cpu().numpy()
+    kv, occ = out["kv"].cpu().numpy(), out["occ"].cpu().numpy()
+    for s, want in enumerate(case["scenarios"]):
+        admitted = [None if step[s, i] < 0 else (int(step[s, i]), gpus[s, i].tolist(), float(cost[s, i]))
+                    for i in range(case["steps"])]
+        queue_left = [i for i in range(case["steps"]) if step[s, i] < 0]
+        check(case, want, admitted, queue_left, kv[s], occ[s])
