@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--c5-steps", type=int, default=8)
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true")
+    ap.add_argument("--no-admission", action="store_true")
     ap.add_argument("--c2-requests", type=int, default=20000)
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
@@ -307,6 +308,7 @@ def run_ours(args):
     c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
     reb = None if args.no_rebalance else run_rebalance(args, rank, world, stream, barrier, reduce_max)
+    adm = None if args.no_admission else run_admission(args, rank, world, stream, barrier, reduce_max)
 
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None
@@ -346,6 +348,7 @@ def run_ours(args):
             "c5": c5,
             "c2": c2,
             "rebalance": reb,
+            "admission": adm,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -460,6 +463,45 @@ def run_rebalance(args, rank, world, stream, barrier, reduce_max):
     del rp0, rp1, rp2
     torch.cuda.empty_cache()
     return res
+
+
+def run_admission(args, rank, world, stream, barrier, reduce_max):
+    """the simulator's admission path (KV-headroom exclusion, strict FIFO drain) for a
+    batch of C2-shaped scenarios (L=64 over 64 GPUs, k=17), one warp per scenario."""
+    import torch
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    S, steps, W = args.scenarios_per_gpu, 256, 24
+    lo, hi = 30000, 90000
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = allocate(cl, model)
+    seeds = shard(S, rank, world)
+    ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.0, jitter=True)
+    with torch.cuda.stream(stream):
+        rp = ScenarioReplayer(ss, window=W, mode="warp", stream=stream)
+        rp.build()
+        rp.admit(8, tok_lo=lo, tok_hi=hi)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = rp.admit(steps, tok_lo=lo, tok_hi=hi)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rp.raise_first_failure()
+    t = reduce_max(e0.elapsed_time(e1) / 1e3)
+    step = out["step"].cpu().numpy()
+    admitted = int((step >= 0).sum())
+    delayed = int(((step >= 0) & (step > np.arange(steps)[None, :])).sum())
+    return {"metric": "admission path: admitted requests/sec (whole job)", "value": admitted * world / t,
+            "unit": "requests/s", "ms": 1e3 * t, "admitted_fraction": admitted / step.size,
+            "delayed_fraction": delayed / max(admitted, 1), "kernel": "admission_warp_kernel (ss_admission_warp)",
+            "config": {"workload": "C2 pool (L=64 over 64 GPUs, k=%d), %d scenarios x %d arrival steps, completion "
+                                   "after W=%d steps, tokens U[%d, %d] vs 100k-token KV per GPU: route with "
+                                   "KV-blocked GPUs excluded, strict FIFO drain"
+                                   % (plan.replication_count, len(seeds) * world, steps, W, lo, hi),
+                       "parallelism": f"scenario-sharded x{world}"}}
 
 
 def run_c2(args, stream):
