@@ -15,7 +15,8 @@ allocations/sec at 1/2/4/8 B200"):
   on every scenario of the rank.  Inputs are resident in HBM (3+ GB of edge
   blocks per GPU, far larger than the 126 MB L2).
 * Phase-1 (``phase1``): C3 -- allocate() candidates of 256-GPU / 80-layer
-  bench pools (variants v = rank + world * i), every (variant, region, k)
+  bench pools, one full ~100k-candidate sweep (1,812 variants) per GPU
+  (variants v = rank + world * i), every (variant, region, k)
   stage-count + score + water-fill, then the per-variant objective fold and a
   global argmax over ranks (NCCL all-gather over NVLink when N > 1).
 * ``e2e``: the same Phase-2 metric through ``ScenarioReplayer.run_from_host``:
@@ -54,7 +55,8 @@ def parse():
     ap.add_argument("--scenarios-per-gpu", type=int, default=1184)
     ap.add_argument("--requests-per-step", type=int, default=64)
     ap.add_argument("--window", type=int, default=64)
-    ap.add_argument("--variants-per-gpu", type=int, default=227)
+    ap.add_argument("--variants-per-gpu", type=int, default=1812,
+                    help="C3 pool variants per GPU (1812 = one full ~100k-candidate C3 sweep per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phase1", action="store_true")
     ap.add_argument("--mode", default="slots", choices=["slots", "blocks"],
