@@ -232,6 +232,16 @@ def run_ours(args):
         return rp, first, t_rank, reduce_max(t_rank), clk
 
     rp, first_cost, t_rank, t_max, clk = measure(args.mode, True)
+    # gather of the chosen chains: the last step's per-selection chain hashes, summed over ranks
+    # on NVLink (all-reduce); gather_chains moves full int16 host[L] records the same way when they are wanted
+    from paper_2509_26182_b200.distributed import chain_checksum
+    with torch.cuda.stream(stream):
+        last = rp.run(R)
+        torch.cuda.synchronize()
+        if dist:
+            checksum = chain_checksum(last.chain_hash)
+        else:
+            checksum = int(last.chain_hash.to(torch.int64).sum().item()) & ((1 << 64) - 1)
     b2 = rp.bytes_per_selection()
     total_sel = sel_per_step_rank * world * args.steps
     value = total_sel / t_max
@@ -338,6 +348,7 @@ def run_ours(args):
                             "build, replay, D2H results",
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
+            "chain_checksum": "%016x" % checksum,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": _traffic(traffic_key, sel_per_step_rank), "peak_source": peak_src,
                          "kernel": kernel_name, "note": bound_note,
