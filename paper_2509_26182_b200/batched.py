@@ -504,6 +504,77 @@ class ScenarioReplayer:
                                           N.stream_handle(self.stream)), "ss_admission_warp")
         return out
 
+    def simulate(self, traces, *, publish_interval: float = 1.5, amortize_rtt: bool = False,
+                 contention: float = 1.0, max_live: int = 200):
+        """The serving simulator (sim.py:_Simulation, no membership events) for every scenario on device.
+
+        traces: one (arrival_s, prompt_tokens, output_tokens) array triple per scenario, sorted by arrival (e.g.
+        scenarios.generate_trace).  Each scenario starts idle.  Returns a list of per-scenario dicts with the
+        MetricsReport fields (sim.py:190-224, latency mean over completion order with Python's sum(), nearest-
+        rank percentiles) plus per-request completion times and the event count.  Needs mode "warp".
+        """
+        import math
+        torch = self.torch
+        if self.mode != "warp":
+            raise ValueError("the simulator runs on the warp-resident kernel (<= 32 hosts per layer)")
+        if len(traces) != self.S:
+            raise ValueError("one trace per scenario")
+        if not self.built:
+            self.build()
+        S, G = self.S, self.G
+        n = np.array([len(t[0]) for t in traces], dtype=np.int64)
+        ptr = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
+        arr = np.concatenate([np.asarray(t[0], dtype=np.float64) for t in traces]) if n.sum() else np.zeros(1)
+        pr = np.concatenate([np.asarray(t[1], dtype=np.int32) for t in traces]) if n.sum() else np.zeros(1, np.int32)
+        ou = np.concatenate([np.asarray(t[2], dtype=np.int32) for t in traces]) if n.sum() else np.zeros(1, np.int32)
+        pow_len = min(max_live + 2, 256)
+        if max_live + 2 > 256:
+            raise ValueError("max_live must be <= 254")
+        pub = np.array([float((1 + o) ** contention) for o in range(pow_len)])
+        exe = np.array([float(max(1, o) ** contention) for o in range(pow_len)])
+        rtt = np.stack([self.scen.scenario_rtt(s) for s in range(S)]) if self.scen.jitter else \
+            np.broadcast_to(self.scen.base_rtt, (S, G, G)).copy()
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=self.dev, dtype=dt)
+        if not hasattr(self, "_tokcap"):
+            self._tokcap = torch.from_numpy(np.tile(self.scen.token_cap, S)).to(self.dev)
+        total = max(int(n.sum()), 1)
+        done_t = torch.full((total,), float("nan"), dtype=torch.float64, device=self.dev)
+        done_r = torch.full((total,), -1, dtype=torch.int32, device=self.dev)
+        dur = torch.zeros(S, dtype=torch.float64, device=self.dev)
+        comp = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        peak = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        nev = torch.zeros(S, dtype=torch.int64, device=self.dev)
+        ptr_d, arr_d, pr_d, ou_d = up(ptr, torch.int32), up(arr, torch.float64), up(pr, torch.int32), up(ou, torch.int32)
+        rtt_d, pub_d, exe_d = up(rtt, torch.float64), up(pub, torch.float64), up(exe, torch.float64)
+        N.check(N.lib().ss_sim_warp(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self._tokcap),
+                                    N.ptr(rtt_d), N.ptr(pub_d), N.ptr(exe_d), pow_len, N.ptr(ptr_d), N.ptr(arr_d),
+                                    N.ptr(pr_d), N.ptr(ou_d), float(publish_interval), int(amortize_rtt),
+                                    int(max_live), N.ptr(done_t), N.ptr(done_r), N.ptr(dur), N.ptr(comp),
+                                    N.ptr(peak), N.ptr(nev), N.ptr(self.status), N.ptr(self.aux),
+                                    N.stream_handle(self.stream)), "ss_sim_warp")
+        self.raise_first_failure()
+        done_t, done_r = done_t.cpu().numpy(), done_r.cpu().numpy()
+        dur, comp, peak, nev = dur.cpu().numpy(), comp.cpu().numpy(), peak.cpu().numpy(), nev.cpu().numpy()
+        reports = []
+        for s in range(S):
+            a, b = int(ptr[s]), int(ptr[s + 1])
+            ranks = done_r[a:b]
+            done = np.nonzero(ranks >= 0)[0]
+            order = done[np.argsort(ranks[done], kind="stable")]
+            lat = [float(done_t[a + i]) - float(arr[a + i]) for i in order]     # completion order (sim.py:397)
+            mean = p50 = p95 = p99 = 0.0
+            if lat:
+                mean = sum(lat) / len(lat)                                     # CPython 3.12 sum, as sim.py:457
+                srt = sorted(lat)
+                rank = lambda q: srt[max(1, math.ceil(q * len(srt) / 100.0)) - 1]
+                p50, p95, p99 = rank(50), rank(95), rank(99)
+            d = float(dur[s])
+            reports.append({"submitted": b - a, "completed": int(comp[s]), "unserved": b - a - int(comp[s]),
+                            "aborted": 0, "duration_s": d, "throughput_rps": int(comp[s]) / d if d > 0 else 0.0,
+                            "latency_mean_s": mean, "latency_p50_s": p50, "latency_p95_s": p95, "latency_p99_s": p99,
+                            "queue_peak": int(peak[s]), "latencies": lat, "events": int(nev[s])})
+        return reports
+
     def adopt_state(self, other: "ScenarioReplayer") -> None:
         """Continue another replayer's request stream (same scenarios, pool and window): occupancy, release
         ring and request counters move over, the placement stays this replayer's."""

@@ -1,0 +1,163 @@
+// Warp-resident DAG helpers shared by the warp replay, admission and simulator kernels.
+//
+// One warp owns one scenario: its host columns, node ids and edge blocks (the ss_dag_edges layout, <= 32
+// hosts per column) live in shared memory, and warp_route() runs one chain DP (router.py:163-197) without a
+// CTA barrier.
+#pragma once
+
+#include <float.h>
+
+#include "ss_common.cuh"
+
+namespace ssw {
+
+constexpr int NONE = 0x7fffffff;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct WarpLayout {
+    int e_cap, ring_len, pow_len;
+    int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
+        off_ring, off_pow, off_cost, off_kv, off_tcap, total;
+};
+
+__device__ __forceinline__ void lexmin(double& v, int& i, double v2, int i2) {
+    if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+
+// Stages one DAG's host columns and edge blocks into shared memory (compact, row-major per boundary).
+// Returns false (warp-uniform) when a column exceeds 32 hosts or the edges exceed the layout.
+__device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l0, int nl, double* E, int* node, int* cl,
+                          int* noff, int* eoff, int lane) {
+    const int nblk = nl - 1;
+    for (int l = lane; l < nl; l += 32) cl[l] = D.col_len[l0 + l];
+    __syncwarp();
+    if (lane == 0) {
+        int n = 0, e = 0, bad = 0;
+        for (int l = 0; l < nl; ++l) {
+            if (cl[l] > 32) bad = 1;
+            noff[l] = n;
+            n += cl[l];
+            if (l < nblk) {
+                eoff[l] = e;
+                e += cl[l] * cl[l + 1];
+            }
+        }
+        if (e > A.e_cap) bad = 1;
+        cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
+    }
+    __syncwarp();
+    if (cl[nl]) return false;
+    for (int l = 0; l < nl; ++l) {
+        const int len = cl[l];
+        if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
+        if (l < nblk) {
+            const double* src = D.edge_val + D.edge_off[l0 + l];
+            const int cnt = len * cl[l + 1];
+            for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// Chain DP of one request on a warp-resident DAG (router.py:163-197): lane j owns host j of the next column;
+// candidates c_i + E_b[i][j] eight sources at a time (independent loads / DADDs) and a first-index tournament
+// (left operand = lower positions, loses only to a strictly smaller right value), groups merged in ascending
+// order with the same rule == numpy first-index argmin; cost = (c_i + r_ij) + tau_j.  Returns the chain cost
+// (+inf: no path); when finite, picks[l] (shared memory) holds the chosen position of every layer.
+__device__ inline double warp_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
+                             int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, int lane) {
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    double* cur = costs;                                     // 32 hosts + 8 pad for the group loop
+    double* nxt = costs + 40;
+    cur[lane] = lane < cl[0] ? tau[node[lane]] : INF;
+    __syncwarp();
+    double c = cur[lane];
+    for (int b = 0; b < nblk; ++b) {
+        const int rs = cl[b], rd = cl[b + 1];
+        const bool act = lane < rd;
+        const double tdst = act ? tau[node[noff[b + 1] + lane]] : 0.0;
+        const double* ep = E + eoff[b] + lane;
+        double best = INF;
+        int bi = 0;                                          // +inf everywhere -> 0 == np.argmin
+        for (int g0 = 0; g0 < rs; g0 += 8) {
+            double a[8];
+            int ix[8];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                const double2 c2 = *reinterpret_cast<const double2*>(cur + g0 + q);
+                const double e0 = (act && g0 + q < rs) ? ep[q * rd] : INF;
+                const double e1 = (act && g0 + q + 1 < rs) ? ep[(q + 1) * rd] : INF;
+                a[q] = __dadd_rn(c2.x, e0);
+                a[q + 1] = __dadd_rn(c2.y, e1);
+                ix[q] = g0 + q;
+                ix[q + 1] = g0 + q + 1;
+            }
+#pragma unroll
+            for (int st = 1; st < 8; st *= 2) {
+#pragma unroll
+                for (int q = 0; q < 8; q += 2 * st) {
+                    if (a[q + st] < a[q]) { a[q] = a[q + st]; ix[q] = ix[q + st]; }
+                }
+            }
+            if (a[0] < best) { best = a[0]; bi = ix[0]; }
+            ep += 8 * rd;
+        }
+        if (act) bp[b * 32 + lane] = (uint8_t)bi;
+        c = act ? __dadd_rn(best, tdst) : INF;
+        nxt[lane] = c;
+        __syncwarp();
+        double* t = cur; cur = nxt; nxt = t;
+    }
+    double v = c;
+    int idx = lane < cl[nblk] ? lane : NONE;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(FULL, v, o);
+        const int i2 = __shfl_xor_sync(FULL, idx, o);
+        lexmin(v, idx, v2, i2);
+    }
+    if (lane == 0 && v <= DBL_MAX) {
+        int p = idx;
+        picks[nblk] = p;
+        for (int b = nblk - 1; b >= 0; --b) {
+            p = bp[b * 32 + p];
+            picks[b] = p;
+        }
+    }
+    __syncwarp();
+    return v;
+}
+
+inline int align16(int x) { return (x + 15) / 16 * 16; }
+
+inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A) {
+    if (D.max_hosts > 32 || D.max_layers < 1) return false;
+    const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * D.max_hosts * D.max_hosts;
+    const int64_t ring_len = window > 0 ? (int64_t)window * (D.max_layers + 1) : 0;
+    if (e_cap > (1 << 20) || ring_len > (1 << 20)) return false;
+    A.e_cap = (int)e_cap;
+    A.ring_len = (int)ring_len;
+    A.pow_len = occpow_len < 256 ? occpow_len : 256;
+    int o = 0;
+    A.off_E = o;      o += align16(A.e_cap * 8);
+    A.off_node = o;   o += align16(D.max_layers * D.max_hosts * 4);
+    A.off_cl = o;     o += align16((D.max_layers + 1) * 4);
+    A.off_noff = o;   o += align16(D.max_layers * 4);
+    A.off_eoff = o;   o += align16(D.max_layers * 4);
+    A.off_bp = o;     o += align16(D.max_layers * 32);
+    A.off_picks = o;  o += align16(D.max_layers * 4);
+    A.off_tau = o;    o += align16(D.max_gpus * 8);
+    A.off_base = o;   o += align16(D.max_gpus * 8);
+    A.off_occ = o;    o += align16(D.max_gpus * 4);
+    A.off_stamp = o;  o += align16(D.max_gpus * 4);
+    A.off_ring = o;   o += align16(A.ring_len * 4);
+    A.off_pow = o;    o += align16(A.pow_len * 8);
+    A.off_cost = o;   o += 2 * 40 * 8;
+    A.off_kv = o;     o += align16(D.max_gpus * 8);
+    A.off_tcap = o;   o += align16(D.max_gpus * 8);
+    A.total = o;
+    return A.total <= 227 * 1024;
+}
+
+}  // namespace ssw

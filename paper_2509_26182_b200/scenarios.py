@@ -169,6 +169,29 @@ def churn_set(seed: int, plan_gpus: Sequence[int], slices: Dict[int, Tuple[int, 
     return sorted(out)
 
 
+def generate_trace(rate_rps: float, duration_s: float, *, seed: int = 0, prompt_tokens=(32, 256),
+                   output_tokens=(16, 128)):
+    """Poisson arrivals with uniform token counts, draw for draw as sim.py:121-150 (random.Random(seed)).
+
+    Returns (arrival_s float64[n], prompt int32[n], output int32[n]) in arrival order.
+    """
+    if rate_rps <= 0:
+        raise ValueError(f"rate_rps must be positive, got {rate_rps}")
+    if duration_s <= 0:
+        raise ValueError(f"duration_s must be positive, got {duration_s}")
+    rng = random.Random(seed)
+    arr, pr, out = [], [], []
+    t = 0.0
+    while True:
+        t += rng.expovariate(rate_rps)
+        if t >= duration_s:
+            break
+        arr.append(t)
+        pr.append(rng.randint(*prompt_tokens))
+        out.append(rng.randint(*output_tokens))
+    return np.array(arr, dtype=np.float64), np.array(pr, dtype=np.int32), np.array(out, dtype=np.int32)
+
+
 TOKEN_SALT = 0x70 << 40
 
 

@@ -50,3 +50,40 @@ def test_oracle_simulator_matches_reference(sim_cases, name):
                                    amortize_rtt=case["amortize"], contention=case["contention"])
     assert report_hex(rep) == case["report"]
     assert [v.hex() for v in lat] == case["latencies"]
+
+
+@pytest.mark.gpu
+def test_device_simulator_matches_reference(cuda_ready, sim_cases):
+    """All four golden runs in one batch per pool shape (one warp per scenario)."""
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    for names in (["c1_light", "c1_heavy"], ["c2_mid", "c2_amortized"]):
+        cases = [sim_cases[n] for n in names]
+        for amortize in (False, True):
+            sel = [c for c in cases if c["amortize"] == amortize]
+            if not sel:
+                continue
+            ss = pool(sel[0])
+            from paper_2509_26182_b200 import scenarios as scen
+            ss = scen.ScenarioSet(ss.layer_count, ss.ids, ss.base_rtt, ss.base_tau, ss.slice_lo, ss.slice_hi,
+                                  np.arange(len(sel)), np.zeros((len(sel), ss.n_gpus), dtype=bool), False,
+                                  token_cap=ss.token_cap)
+            rp = ScenarioReplayer(ss, window=1, mode="warp")
+            traces = []
+            for c in sel:
+                t = trace_of(c)
+                traces.append((np.array([x[0] for x in t]), np.array([x[1] for x in t], dtype=np.int32),
+                               np.array([x[2] for x in t], dtype=np.int32)))
+            reps = rp.simulate(traces, amortize_rtt=amortize, contention=sel[0]["contention"], max_live=250)
+            for c, rep in zip(sel, reps):
+                lat = rep.pop("latencies")
+                rep.pop("events")
+                assert report_hex(rep) == c["report"]
+                assert [v.hex() for v in lat] == c["latencies"]
+
+
+def test_generate_trace_matches_reference_draws(sim_cases):
+    from paper_2509_26182_b200.scenarios import generate_trace
+    for c in sim_cases.values():
+        a, p, o = generate_trace(c["rate"], c["duration"], seed=c["seed"], prompt_tokens=tuple(c["prompt"]),
+                                 output_tokens=tuple(c["output"]))
+        assert [[x.hex(), int(y), int(z)] for x, y, z in zip(a.tolist(), p, o)] == c["trace"]
