@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-admission", action="store_true")
+    ap.add_argument("--no-sim", action="store_true")
     ap.add_argument("--c2-requests", type=int, default=20000)
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
@@ -321,6 +322,7 @@ def run_ours(args):
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
     reb = None if args.no_rebalance else run_rebalance(args, rank, world, stream, barrier, reduce_max)
     adm = None if args.no_admission else run_admission(args, rank, world, stream, barrier, reduce_max)
+    simr = None if args.no_sim else run_sim(args, rank, world, stream, barrier, reduce_max)
 
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None
@@ -362,6 +364,7 @@ def run_ours(args):
             "c2": c2,
             "rebalance": reb,
             "admission": adm,
+            "simulator": simr,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -515,6 +518,56 @@ def run_admission(args, rank, world, stream, barrier, reduce_max):
                                    "KV-blocked GPUs excluded, strict FIFO drain"
                                    % (plan.replication_count, len(seeds) * world, steps, W, lo, hi),
                        "parallelism": f"scenario-sharded x{world}"}}
+
+
+def run_sim(args, rank, world, stream, barrier, reduce_max):
+    """SURVEY.md 8(f) row 3 end to end: the reference's serving simulator (sim.py, no membership events) for
+    a batch of C2-shaped scenarios, each its own Poisson trace, one warp per scenario; the oracle event loop on
+    one host core times the same work for comparison (rank 0, N = 1)."""
+    import torch
+    from paper_2509_26182_b200 import allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    S = args.scenarios_per_gpu
+    rate, dur, prompt, output = 150.0, 2.0, (500, 20000), (8, 48)
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = allocate(cl, model)
+    seeds = shard(S, rank, world)
+    ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.0, jitter=True)
+    traces = [scen.generate_trace(rate, dur, seed=int(s), prompt_tokens=prompt, output_tokens=output) for s in seeds]
+    with torch.cuda.stream(stream):
+        rp = ScenarioReplayer(ss, window=1, mode="warp", stream=stream)
+        rp.build()
+        rp.simulate(traces, max_live=250)                          # warm-up (same work)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        reps = rp.simulate(traces, max_live=250)
+        t = reduce_max(time.perf_counter() - t0)
+    events = sum(r["events"] for r in reps) * world
+    reqs = sum(r["submitted"] for r in reps) * world
+    res = {"metric": "serving simulator: simulated events/sec (whole job)", "value": events / t, "unit": "events/s",
+           "requests_per_s": reqs / t, "wall_ms": 1e3 * t, "completed_fraction": float(
+               sum(r["completed"] for r in reps) / max(1, sum(r["submitted"] for r in reps))),
+           "kernel": "sim_warp_kernel (ss_sim_warp)",
+           "config": {"workload": "C2 pool (L=64 over 64 GPUs, k=%d), %d scenarios, each a Poisson trace at %.0f "
+                                  "req/s for %.0f s (prompt U%s, output U%s tokens), KV-gated strict-FIFO admission, "
+                                  "occupancy-dependent decode steps; wall time includes trace upload and the host "
+                                  "MetricsReport" % (plan.replication_count, len(seeds) * world, rate, dur,
+                                                     list(prompt), list(output)),
+                      "parallelism": f"scenario-sharded x{world}"}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import sim_ref
+        tr = traces[0]
+        c0 = time.perf_counter()
+        rep0, _, _ = sim_ref.simulate(ss.columns(0), ss.base_tau, ss.scenario_rtt(0), ss.token_cap,
+                                      list(zip(tr[0].tolist(), tr[1].tolist(), tr[2].tolist())))
+        cpu_s = time.perf_counter() - c0
+        res["cpu_baseline"] = {"value": reps[0]["events"] / cpu_s, "unit": "events/s", "cores": 1, "kind": "port",
+                               "sample": "scenario 0 only (%d requests) through the oracle event loop" % len(tr[0]),
+                               "matches_device": rep0["completed"] == reps[0]["completed"] and
+                               rep0["duration_s"] == reps[0]["duration_s"]}
+    return res
 
 
 def run_c2(args, stream):
