@@ -538,11 +538,11 @@ def run_sim(args, rank, world, stream, barrier, reduce_max):
     with torch.cuda.stream(stream):
         rp = ScenarioReplayer(ss, window=1, mode="warp", stream=stream)
         rp.build()
-        rp.simulate(traces, max_live=250)                          # warm-up (same work)
+        rp.simulate(traces)                          # warm-up (same work)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        reps = rp.simulate(traces, max_live=250)
+        reps = rp.simulate(traces)
         t = reduce_max(time.perf_counter() - t0)
     events = sum(r["events"] for r in reps) * world
     reqs = sum(r["submitted"] for r in reps) * world

@@ -206,7 +206,9 @@ int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const doub
  * layer).  Scenario s simulates requests [trace_ptr[s], trace_ptr[s+1]) sorted
  * by arrival; rtt is the scenario's dense one-way RTT matrix (stride
  * max_gpus^2), pub_pow[o] = (1+o)^e and exec_pow[o] = max(1,o)^e for o <
- * pow_len (<= 256, > max_live).  Per request: done_time / done_rank (completion
+ * pow_len (>= max_live + 2; the first 256 entries are cached in shared memory).
+ * max_live is clamped to the live-chain table that fits in shared memory.
+ * Per request: done_time / done_rank (completion
  * order), left untouched when unserved (callers pre-fill NaN / -1); per
  * scenario: duration (time of the last event, ticks included), completed,
  * queue_peak, n_events, status (SS_BAD_INPUT: more than max_live concurrent
@@ -217,6 +219,16 @@ int ss_sim_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* ba
                 double publish_interval, int32_t amortize_rtt, int32_t max_live, double* done_time,
                 int32_t* done_rank, double* duration, int32_t* completed, int32_t* queue_peak, int64_t* n_events,
                 int32_t* status, int32_t* aux, void* stream);
+
+/* ss_sim_warp for wide pools (columns of up to 256 hosts): one CTA of 128
+ * threads per scenario, edge blocks (ss_dag_edges layout) read from global
+ * memory by the chain DP.  Same arguments, semantics and outputs. */
+int ss_sim_cta(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* base_tau, const int64_t* token_cap,
+               const double* rtt, const double* pub_pow, const double* exec_pow, int32_t pow_len,
+               const int32_t* trace_ptr, const double* arrival, const int32_t* prompt, const int32_t* output,
+               double publish_interval, int32_t amortize_rtt, int32_t max_live, double* done_time, int32_t* done_rank,
+               double* duration, int32_t* completed, int32_t* queue_peak, int64_t* n_events, int32_t* status,
+               int32_t* aux, void* stream);
 
 /* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
  * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring

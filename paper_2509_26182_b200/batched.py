@@ -505,7 +505,7 @@ class ScenarioReplayer:
         return out
 
     def simulate(self, traces, *, publish_interval: float = 1.5, amortize_rtt: bool = False,
-                 contention: float = 1.0, max_live: int = 200):
+                 contention: float = 1.0, max_live: Optional[int] = None):
         """The serving simulator (sim.py:_Simulation, no membership events) for every scenario on device.
 
         traces: one (arrival_s, prompt_tokens, output_tokens) array triple per scenario, sorted by arrival (e.g.
@@ -515,8 +515,8 @@ class ScenarioReplayer:
         """
         import math
         torch = self.torch
-        if self.mode != "warp":
-            raise ValueError("the simulator runs on the warp-resident kernel (<= 32 hosts per layer)")
+        if self.mode not in ("warp", "blocks"):
+            raise ValueError("the simulator runs with mode 'warp' (<= 32 hosts per layer) or 'blocks' (<= 256)")
         if len(traces) != self.S:
             raise ValueError("one trace per scenario")
         if not self.built:
@@ -527,9 +527,9 @@ class ScenarioReplayer:
         arr = np.concatenate([np.asarray(t[0], dtype=np.float64) for t in traces]) if n.sum() else np.zeros(1)
         pr = np.concatenate([np.asarray(t[1], dtype=np.int32) for t in traces]) if n.sum() else np.zeros(1, np.int32)
         ou = np.concatenate([np.asarray(t[2], dtype=np.int32) for t in traces]) if n.sum() else np.zeros(1, np.int32)
-        pow_len = min(max_live + 2, 256)
-        if max_live + 2 > 256:
-            raise ValueError("max_live must be <= 254")
+        if max_live is None:
+            max_live = max(1, int(n.max()) if n.size else 1)         # every request live at once, at most
+        pow_len = max_live + 2
         pub = np.array([float((1 + o) ** contention) for o in range(pow_len)])
         exe = np.array([float(max(1, o) ** contention) for o in range(pow_len)])
         rtt = np.stack([self.scen.scenario_rtt(s) for s in range(S)]) if self.scen.jitter else \
@@ -546,12 +546,17 @@ class ScenarioReplayer:
         nev = torch.zeros(S, dtype=torch.int64, device=self.dev)
         ptr_d, arr_d, pr_d, ou_d = up(ptr, torch.int32), up(arr, torch.float64), up(pr, torch.int32), up(ou, torch.int32)
         rtt_d, pub_d, exe_d = up(rtt, torch.float64), up(pub, torch.float64), up(exe, torch.float64)
-        N.check(N.lib().ss_sim_warp(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self._tokcap),
+        fn = N.lib().ss_sim_warp if self.mode == "warp" else N.lib().ss_sim_cta
+        N.check(fn(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self._tokcap),
                                     N.ptr(rtt_d), N.ptr(pub_d), N.ptr(exe_d), pow_len, N.ptr(ptr_d), N.ptr(arr_d),
                                     N.ptr(pr_d), N.ptr(ou_d), float(publish_interval), int(amortize_rtt),
                                     int(max_live), N.ptr(done_t), N.ptr(done_r), N.ptr(dur), N.ptr(comp),
                                     N.ptr(peak), N.ptr(nev), N.ptr(self.status), N.ptr(self.aux),
-                                    N.stream_handle(self.stream)), "ss_sim_warp")
+                                    N.stream_handle(self.stream)), "ss_sim_" + self.mode)
+        st = self.status.cpu().numpy()
+        if (st == 8).any():
+            raise ValueError("a scenario had more concurrent chains than the simulator's shared-memory table holds, "
+                             "or a chain with more than 32 hops")
         self.raise_first_failure()
         done_t, done_r = done_t.cpu().numpy(), done_r.cpu().numpy()
         dur, comp, peak, nev = dur.cpu().numpy(), comp.cpu().numpy(), peak.cpu().numpy(), nev.cpu().numpy()

@@ -46,6 +46,8 @@ def main():
         "c1_heavy": case(8, 32, 2, 400.0, 1.0, (1000, 40000), (16, 64)),
         "c2_mid": case(64, 64, 3, 150.0, 2.0, (500, 20000), (8, 48)),
         "c2_amortized": case(64, 64, 4, 150.0, 1.0, (500, 20000), (8, 48), amortize=True),
+        "c4_light": case(256, 64, 5, 60.0, 1.5, (500, 40000), (8, 32)),
+        "n192_wide": case(192, 10, 6, 300.0, 1.0, (1000, 60000), (4, 24)),
     }
     path = os.path.join(HERE, "sim_cases.json")
     with open(path, "w") as fh:

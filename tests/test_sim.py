@@ -15,7 +15,7 @@ from helpers_golden import plan_from_golden
 from oracle import alloc_ref, sim_ref
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = ["c1_light", "c1_heavy", "c2_mid", "c2_amortized"]
+CASES = ["c1_light", "c1_heavy", "c2_mid", "c2_amortized", "c4_light", "n192_wide"]
 
 
 @pytest.fixture(scope="module")
@@ -53,32 +53,27 @@ def test_oracle_simulator_matches_reference(sim_cases, name):
 
 
 @pytest.mark.gpu
-def test_device_simulator_matches_reference(cuda_ready, sim_cases):
-    """All four golden runs in one batch per pool shape (one warp per scenario)."""
-    from paper_2509_26182_b200.batched import ScenarioReplayer
-    for names in (["c1_light", "c1_heavy"], ["c2_mid", "c2_amortized"]):
-        cases = [sim_cases[n] for n in names]
-        for amortize in (False, True):
-            sel = [c for c in cases if c["amortize"] == amortize]
-            if not sel:
-                continue
-            ss = pool(sel[0])
-            from paper_2509_26182_b200 import scenarios as scen
-            ss = scen.ScenarioSet(ss.layer_count, ss.ids, ss.base_rtt, ss.base_tau, ss.slice_lo, ss.slice_hi,
-                                  np.arange(len(sel)), np.zeros((len(sel), ss.n_gpus), dtype=bool), False,
-                                  token_cap=ss.token_cap)
-            rp = ScenarioReplayer(ss, window=1, mode="warp")
-            traces = []
-            for c in sel:
-                t = trace_of(c)
-                traces.append((np.array([x[0] for x in t]), np.array([x[1] for x in t], dtype=np.int32),
-                               np.array([x[2] for x in t], dtype=np.int32)))
-            reps = rp.simulate(traces, amortize_rtt=amortize, contention=sel[0]["contention"], max_live=250)
-            for c, rep in zip(sel, reps):
-                lat = rep.pop("latencies")
-                rep.pop("events")
-                assert report_hex(rep) == c["report"]
-                assert [v.hex() for v in lat] == c["latencies"]
+@pytest.mark.parametrize("name", CASES)
+def test_device_simulator_matches_reference(cuda_ready, sim_cases, name):
+    """ss_sim_warp (<= 32 hosts per layer) or ss_sim_cta (wide pools: C4's k = 73, k = 172) vs the reference."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer, replay_mode
+    c = sim_cases[name]
+    base = pool(c)
+    # two copies of the scenario in one launch: both must reproduce the reference
+    ss = scen.ScenarioSet(base.layer_count, base.ids, base.base_rtt, base.base_tau, base.slice_lo, base.slice_hi,
+                          np.arange(2), np.zeros((2, base.n_gpus), dtype=bool), False, token_cap=base.token_cap)
+    mode = "warp" if replay_mode(ss, window=1) == "warp" else "blocks"
+    rp = ScenarioReplayer(ss, window=1, mode=mode)
+    t = trace_of(c)
+    tr = (np.array([x[0] for x in t]), np.array([x[1] for x in t], dtype=np.int32),
+          np.array([x[2] for x in t], dtype=np.int32))
+    reps = rp.simulate([tr, tr], amortize_rtt=c["amortize"], contention=c["contention"])
+    for rep in reps:
+        lat = rep.pop("latencies")
+        rep.pop("events")
+        assert report_hex(rep) == c["report"], mode
+        assert [v.hex() for v in lat] == c["latencies"], mode
 
 
 def test_generate_trace_matches_reference_draws(sim_cases):
