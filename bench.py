@@ -535,6 +535,7 @@ def run_sim(args, rank, world, stream, barrier, reduce_max):
     seeds = shard(S, rank, world)
     ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.0, jitter=True)
     traces = [scen.generate_trace(rate, dur, seed=int(s), prompt_tokens=prompt, output_tokens=output) for s in seeds]
+    wide = _sim_wide(args, rank, world, stream, barrier, reduce_max)
     with torch.cuda.stream(stream):
         rp = ScenarioReplayer(ss, window=1, mode="warp", stream=stream)
         rp.build()
@@ -556,6 +557,7 @@ def run_sim(args, rank, world, stream, barrier, reduce_max):
                                   "MetricsReport" % (plan.replication_count, len(seeds) * world, rate, dur,
                                                      list(prompt), list(output)),
                       "parallelism": f"scenario-sharded x{world}"}}
+    res["c4_pool"] = wide
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import sim_ref
         tr = traces[0]
@@ -568,6 +570,32 @@ def run_sim(args, rank, world, stream, barrier, reduce_max):
                                "matches_device": rep0["completed"] == reps[0]["completed"] and
                                rep0["duration_s"] == reps[0]["duration_s"]}
     return res
+
+
+def _sim_wide(args, rank, world, stream, barrier, reduce_max):
+    """The simulator on the C4 pool (L=64 over 256 GPUs, k=73): one CTA per scenario (ss_sim_cta)."""
+    import torch
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    cl, model, plan = base_pool()
+    seeds = shard(args.scenarios_per_gpu, rank, world)
+    ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.0, jitter=True)
+    traces = [scen.generate_trace(60.0, 1.5, seed=int(s), prompt_tokens=(500, 40000), output_tokens=(8, 32))
+              for s in seeds]
+    with torch.cuda.stream(stream):
+        rp = ScenarioReplayer(ss, window=1, mode="blocks", stream=stream)
+        rp.build()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        reps = rp.simulate(traces)
+        t = reduce_max(time.perf_counter() - t0)
+    events = sum(r["events"] for r in reps) * world
+    return {"value": events / t, "unit": "events/s", "requests_per_s": sum(r["submitted"] for r in reps) * world / t,
+            "wall_ms": 1e3 * t, "kernel": "sim_cta_kernel (ss_sim_cta)",
+            "workload": "C4 pool (k=%d), %d scenarios, Poisson traces at 60 req/s for 1.5 s"
+                        % (plan.replication_count, len(seeds) * world)}
 
 
 def run_c2(args, stream):
