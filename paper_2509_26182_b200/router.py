@@ -151,24 +151,35 @@ class _DeviceDag:
                         N.ptr(self.edge_val))
 
 
-def _select_on_device(ddag: _DeviceDag, rtt_dev, n_gpus: int):
-    """ss_dag_edges + ss_select for one DAG; returns (picks, cost, status)."""
+def _select_on_device(ddag: _DeviceDag, rtt_dev, n_gpus: int, count_edges: bool = True):
+    """ss_dag_edges (once per DAG) + ss_select; returns (picks, cost, status, finite edge count)."""
     torch = _torch()
     lib = N.lib()
     dev = _dev()
     ds = ddag.dag_set(n_gpus)
-    rmeta = torch.tensor([0], dtype=torch.int64).to(dev, non_blocking=True)
-    rdim = torch.tensor([n_gpus], dtype=torch.int32).to(dev, non_blocking=True)
     st = N.stream_handle()
-    N.check(lib.ss_dag_edges(ds, N.ptr(rmeta), N.ptr(rdim), N.ptr(rtt_dev), None, 0, N.ptr(ddag.edge_val), st),
-            "ss_dag_edges")
-    picks = torch.empty(ddag.L, dtype=torch.int32, device=dev)
-    cost = torch.empty(1, dtype=torch.float64, device=dev)
-    status = torch.empty(1, dtype=torch.int32, device=dev)
+    if not getattr(ddag, "edges_built", False):
+        rmeta = torch.tensor([0], dtype=torch.int64).to(dev, non_blocking=True)
+        rdim = torch.tensor([n_gpus], dtype=torch.int32).to(dev, non_blocking=True)
+        N.check(lib.ss_dag_edges(ds, N.ptr(rmeta), N.ptr(rdim), N.ptr(rtt_dev), None, 0, N.ptr(ddag.edge_val), st),
+                "ss_dag_edges")
+        ddag.edges_built = True
+    if not hasattr(ddag, "out"):
+        ddag.out = torch.empty(ddag.L + 4, dtype=torch.float64, device=dev)   # picks (as int32 pairs), cost, status
+    out = ddag.out
+    picks = out[:(ddag.L + 1) // 2 + 1].view(torch.int32)[:ddag.L]
+    cost = out[ddag.L // 2 + 2: ddag.L // 2 + 3]
+    status = out[ddag.L // 2 + 3: ddag.L // 2 + 4].view(torch.int32)[:1]
     N.check(lib.ss_select(ds, N.ptr(picks), N.ptr(cost), N.ptr(status), st), "ss_select")
-    # finite edge count (router.py:176-177); block pads are +inf
-    edges = torch.isfinite(ddag.edge_val[:ddag.edge_used]).sum() if ddag.L > 1 else torch.zeros((), device=dev)
-    return picks.cpu().tolist(), float(cost.cpu()[0]), int(status.cpu()[0]), int(edges.cpu())
+    edges = 0
+    if count_edges and ddag.L > 1:
+        # finite edge count (router.py:176-177); block pads are +inf
+        edges = int(torch.isfinite(ddag.edge_val[:ddag.edge_used]).sum())
+    host = out.cpu()                                                          # one D2H for picks + cost + status
+    picks_h = host[:(ddag.L + 1) // 2 + 1].view(torch.int32)[:ddag.L].tolist()
+    cost_h = float(host[ddag.L // 2 + 2])
+    status_h = int(host[ddag.L // 2 + 3:ddag.L // 2 + 4].view(torch.int32)[0])
+    return picks_h, cost_h, status_h, edges
 
 
 def _chain_from_picks(hosts: Sequence[Sequence[str]], picks: Sequence[int], cost: float) -> PipelineChain:
@@ -284,8 +295,32 @@ def _select_with_matrix(dag: LayerDag, rtt_dev, index, n_gpus, stats) -> Pipelin
     return _chain_from_picks(dag.hosts, picks, cost)
 
 
+class _RouteCache:
+    """A device DAG kept across routes while the perf map's tau key set, the exclude set and the RTT table are
+    unchanged and no entry can have expired: only republished tau values move, host mirror -> device."""
+
+    def __init__(self, keys_version, exclude, rtt_key, min_pub, dag, ddag, index, edges, tau_h, nodes_of):
+        self.keys_version = keys_version
+        self.exclude = exclude
+        self.rtt_key = rtt_key
+        self.min_pub = min_pub          # oldest tau publish time when built; entries only get newer
+        self.dag = dag
+        self.ddag = ddag
+        self.index = index
+        self.edges = edges
+        self.tau_h = tau_h              # host mirror of ddag.node_tau
+        self.nodes_of = nodes_of        # gpu -> [(node position, layer)]
+
+
 class ChainRouter:
-    """Snapshot -> device DAG -> device DP -> occupancy feedback on the PerfMap."""
+    """Snapshot -> device DAG -> device DP -> occupancy feedback on the PerfMap.
+
+    Between membership / placement changes consecutive routes differ only in the latencies that the previous
+    select / release republished, so the router keeps its device DAG (columns, edge blocks) and uploads just the
+    tau column of the republished GPUs: the chain is the one router.py:247-257 would select from a fresh snapshot
+    (same live keys -- none can have expired while now - oldest publish <= ttl --, same exclude set, same RTT
+    table, current values).
+    """
 
     def __init__(self, perf_map: PerfMap, layer_count: int):
         self.perf_map = perf_map
@@ -295,6 +330,7 @@ class ChainRouter:
         self._matrix = None
         self._index: Dict[str, int] = {}
         self._valid_until = -math.inf
+        self._cache: Optional[_RouteCache] = None
 
     def _matrix_for(self, snapshot: PerfSnapshot, gpu_ids: Tuple[str, ...]):
         key = (snapshot.rtt_version, gpu_ids)
@@ -308,14 +344,61 @@ class ChainRouter:
         return self._matrix, self._index
 
     def route(self, now: float, *, exclude: AbstractSet[str] = _EMPTY) -> PipelineChain:
-        snapshot = self.perf_map.snapshot(now)
+        pm = self.perf_map
+        keys_version, dirty = pm._drain_tau_updates()
+        c = self._cache
+        excl = frozenset(exclude)
+        if (c is not None and c.keys_version == keys_version and c.exclude == excl
+                and c.rtt_key == (pm._rtt_version, c.dag.gpu_ids()) and now <= self._valid_until
+                and now - c.min_pub <= pm.ttl_s):
+            return self._route_cached(c, dirty, now)
+        snapshot = pm.snapshot(now)
         dag = build_dag(snapshot, self.layer_count, exclude=exclude)
         self.stats.dags_built += 1
         ids = dag.gpu_ids()
         matrix, index = self._matrix_for(snapshot, ids)
-        chain = _select_with_matrix(dag, matrix, index, len(ids), self.stats)
-        self.perf_map.on_chain_event(chain, "select", now)
+        ddag = _pack_dag(dag, index)
+        picks, cost, status, edges = _select_on_device(ddag, matrix, len(ids))
+        chain = self._finish(dag, picks, cost, status, edges)
+        with pm._lock:
+            min_pub = min((pm._tau[(g, l + 1)].published_at for l, col in enumerate(dag.hosts) for g in col),
+                          default=math.inf)
+        nodes_of: Dict[str, list] = {}
+        pos = 0
+        for l, col in enumerate(dag.hosts):
+            for g in col:
+                nodes_of.setdefault(g, []).append((pos, l + 1))
+                pos += 1
+        tau_h = np.array([dag.latencies[(g, l + 1)] for l, col in enumerate(dag.hosts) for g in col],
+                         dtype=np.float64)
+        self._cache = _RouteCache(keys_version, excl, (pm._rtt_version, ids), min_pub, dag, ddag, index, edges,
+                                  tau_h, nodes_of)
+        pm.on_chain_event(chain, "select", now)
         return chain
+
+    def _route_cached(self, c: _RouteCache, dirty, now: float) -> PipelineChain:
+        pm = self.perf_map
+        torch = _torch()
+        if dirty:
+            with pm._lock:
+                for g in dirty:
+                    for p, layer in c.nodes_of.get(g, ()):
+                        c.tau_h[p] = pm._tau[(g, layer)].value
+            c.ddag.node_tau.copy_(torch.from_numpy(c.tau_h), non_blocking=False)
+        self.stats.dags_built += 1
+        self.stats.matrix_reuses += 1
+        picks, cost, status, _ = _select_on_device(c.ddag, self._matrix, len(c.index), count_edges=False)
+        chain = self._finish(c.dag, picks, cost, status, c.edges)
+        pm.on_chain_event(chain, "select", now)
+        return chain
+
+    def _finish(self, dag, picks, cost, status, edges) -> PipelineChain:
+        self.stats.edges_relaxed += edges
+        if status == 2:
+            raise NoPath()
+        raise_for_status(status)
+        self.stats.chains_selected += 1
+        return _chain_from_picks(dag.hosts, picks, cost)
 
     def release(self, chain: PipelineChain, now: float) -> None:
         self.perf_map.on_chain_event(chain, "release", now)
