@@ -1,4 +1,5 @@
 // Latency microbenchmark (dependent chains, one warp): DADD, DSETP+FSEL min, int64 compare+select, LDS.64.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o tests/micro/lat tests/micro/lat.cu
 #include <cstdio>
 #include <cstdint>
 __global__ void k(double* out, long long* cyc, double x0, int n) {
