@@ -32,10 +32,115 @@ struct WarpReplay {
     unsigned long long* prof;   // diagnostics (env SS_WARP_PROF=1): cycles per phase, else NULL
 };
 
-__global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
+// Chain DP spread over NWD warps (9..32 hosts per column): warp w owns destinations [8w, 8w+8); lane
+// (d, q) = (lane & 7, lane >> 3) takes the sources q, q+4, ..., q+28 of destination 8w+d.  The argmin is a
+// lexicographic (value, index) minimum -- identical to numpy's first-index argmin with a strict `<` scan
+// (all-+inf resolves to index 0, as np.argmin does) -- formed as an in-lane tree plus two shuffle rounds, so
+// every merge stays inside the warp and a boundary costs one CTA barrier.  The boundary's edge entries,
+// column lengths and destination latencies do not depend on the running costs: they are fetched into
+// registers one boundary ahead, leaving only cur[] loads -> DADD -> tree -> shuffles -> store on the
+// critical path.  Same contract as warp_route (picks valid when the returned cost is finite).
+struct MwBoundary {
+    int rs, rd;
+    double e[8];
+    double td;
+};
+
+__device__ __forceinline__ void mw_fetch(MwBoundary& m, const double* E, const int* node, const int* cl,
+                                         const int* noff, const int* eoff, const double* tau, int b, int j, int q) {
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    m.rs = cl[b];
+    m.rd = cl[b + 1];
+    const bool act = j < m.rd;
+    const double* ep = E + eoff[b] + j;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = q + 4 * k;
+        m.e[k] = (act && i < m.rs) ? ep[i * m.rd] : INF;
+    }
+    m.td = act ? tau[node[noff[b + 1] + j]] : 0.0;
+}
+
+template <int NWD>
+__device__ double mw_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
+                           int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, double* vshare,
+                           int tid) {
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    constexpr int NT = NWD * 32;
+    const int warp = tid >> 5, lane = tid & 31, d = lane & 7, q = lane >> 3;
+    const int j = warp * 8 + d;
+    const uint32_t bp_s = (uint32_t)__cvta_generic_to_shared(bp);   // hoisted: no per-boundary window lookup
+    double* cur = costs;                                     // [40]: 32 hosts + 8 pad (+inf)
+    double* nxt = costs + 40;
+    for (int p = tid; p < 32; p += NT) cur[p] = p < cl[0] ? tau[node[p]] : INF;
+    MwBoundary m;
+    if (nblk > 0) mw_fetch(m, E, node, cl, noff, eoff, tau, 0, j, q);
+    __syncthreads();
+    for (int b = 0; b < nblk; ++b) {
+        double a[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(cur[q + 4 * k], m.e[k]);
+        const int rd = m.rd;
+        const double td = m.td;
+        // in-lane tree: left operands always carry the smaller source index -> take the right one on `<`
+        int ix[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ix[k] = k;
+#pragma unroll
+        for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+            for (int k = 0; k < 8; k += 2 * w)
+                if (a[k + w] < a[k]) { a[k] = a[k + w]; ix[k] = ix[k + w]; }
+        double best = a[0];
+        int bi = q + 4 * ix[0];
+#pragma unroll
+        for (int o = 8; o <= 16; o <<= 1) {
+            const double v2 = __shfl_xor_sync(FULL, best, o);
+            const int i2 = __shfl_xor_sync(FULL, bi, o);
+            lexmin(best, bi, v2, i2);
+        }
+        if (q == 0 && j < rd) {
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(bp_s + b * 32 + j), "r"(bi));
+            nxt[j] = __dadd_rn(best, td);
+        }
+        // next boundary's operands: issued behind the shuffles (shared LSU queue), landing during the barrier
+        if (b + 1 < nblk) mw_fetch(m, E, node, cl, noff, eoff, tau, b + 1, j, q);
+        __syncthreads();
+        double* t = cur; cur = nxt; nxt = t;
+    }
+    if (warp == 0) {
+        double v = lane < cl[nblk] ? cur[lane] : INF;
+        int idx = lane < cl[nblk] ? lane : NONE;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(FULL, v, o);
+            const int i2 = __shfl_xor_sync(FULL, idx, o);
+            lexmin(v, idx, v2, i2);
+        }
+        if (lane == 0) {
+            *vshare = v;
+            if (v <= DBL_MAX) {
+                int p = idx;
+                picks[nblk] = p;
+                for (int b = nblk - 1; b >= 0; --b) {
+                    p = bp[b * 32 + p];
+                    picks[b] = p;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return *vshare;
+}
+
+// NWD = 1: one warp owns the scenario (<= 8 hosts per column, warp_route).  NWD = 2..4: the destinations of
+// every boundary are spread over NWD warps (mw_route); the rest of the request stays on warp 0.
+template <int NWD>
+__global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NT = NWD * 32;
     const int dag = blockIdx.x;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     if (R.st.status[dag] != SS_OK) return;                      // sticky failure: skip
     const int l0 = D.layer_ptr[dag];
@@ -55,10 +160,14 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
     int* ring = reinterpret_cast<int*>(smem + A.off_ring);
     double* pw = reinterpret_cast<double*>(smem + A.off_pow);
     double* costs = reinterpret_cast<double*>(smem + A.off_cost);   // [2][40] column costs (32 hosts + 8 pad)
+    __shared__ double vshare;
+    __shared__ int flag[3];
 
     // ---- one-time staging: columns, edges, per-GPU state, ring --------------
-    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane)) {
-        if (lane == 0) R.st.status[dag] = SS_BAD_INPUT;
+    if (warp == 0) flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? 0 : 1;
+    __syncthreads();
+    if (flag[0]) {
+        if (tid == 0) R.st.status[dag] = SS_BAD_INPUT;
         return;
     }
     const int gbase = R.st.gpu_ptr[dag];
@@ -66,15 +175,15 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
     const int window = R.window;
     const int ring_stride = D.max_layers + 1;
     int* ring_g = R.st.ring + (int64_t)dag * (window > 0 ? window : 1) * ring_stride;
-    for (int g = lane; g < ng; g += 32) {
+    for (int g = tid; g < ng; g += NT) {
         occ[g] = R.st.occ[gbase + g];
         base[g] = R.st.base_tau[gbase + g];
         stamp[g] = 0;
     }
-    for (int o = lane; o < A.pow_len; o += 32) pw[o] = R.occpow[o];
-    for (int q = lane; q < A.ring_len; q += 32) ring[q] = ring_g[q];
-    if (lane < 8) { costs[32 + lane] = INF; costs[72 + lane] = INF; }
-    __syncwarp();
+    for (int o = tid; o < A.pow_len; o += NT) pw[o] = R.occpow[o];
+    for (int q = tid; q < A.ring_len; q += NT) ring[q] = ring_g[q];
+    if (tid < 8) { costs[32 + tid] = INF; costs[72 + tid] = INF; }
+    __syncthreads();
 
     const int n_req = R.n_req;
     const int64_t req0 = R.st.next_req[dag];
@@ -95,42 +204,43 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
         if (window > 0 && req >= window) {
             const int* slot = ring + (int)(req % window) * ring_stride;
             const int cnt = slot[0];
-            for (int k = lane; k < cnt; k += 32) occ[slot[1 + k]] -= 1;   // distinct GPUs: no collisions
+            for (int k = tid; k < cnt; k += NT) occ[slot[1 + k]] -= 1;   // distinct GPUs: no collisions
         }
-        __syncwarp();
-        int err = 0, errg = 0;
-        for (int g = lane; g < ng; g += 32) {
+        if (tid == 0) flag[1] = 0;
+        __syncthreads();
+        for (int g = tid; g < ng; g += NT) {
             const int o = occ[g];
             if (o < 0 || o >= R.occpow_len) {
-                err = o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT;
-                errg = g;
+                flag[1] = o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT;
+                flag[2] = g;
             }
             const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
             tau[g] = base[g] * (oc < A.pow_len ? pw[oc] : R.occpow[oc]);
         }
-        const unsigned em = __ballot_sync(FULL, err != 0);
-        if (em) {
-            const int src = __ffs(em) - 1;
-            status = __shfl_sync(FULL, err, src);
-            aux = __shfl_sync(FULL, errg, src);
+        __syncthreads();
+        if (flag[1]) {
+            status = flag[1];
+            aux = flag[2];
             break;
         }
-        __syncwarp();
         mark(0);
         // ---- DP over the layer columns + final argmin / backtrack ------------------
-        const double v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+        double v;
+        if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+        else v = mw_route<NWD>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
         mark(1);
-        if (lane == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
+        if (tid == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         if (!(v <= DBL_MAX)) {
             status = SS_NO_PATH;
             break;
         }
-        __syncwarp();
+        __syncthreads();
         // ---- load update: +1 per distinct GPU of the chain, ring, outputs ---------
         const int tag = (int)(req & 0x3fffffff) + 1;
         int* slot = window > 0 ? ring + (int)(req % window) * ring_stride : nullptr;
         uint64_t h = 0;
         int cnt = 0;
+        if (warp == 0) {
         for (int l0c = 0; l0c < nl; l0c += 32) {
             const int l = l0c + lane;
             int g = 0;
@@ -154,16 +264,17 @@ __global__ void __launch_bounds__(32) replay_warp_kernel(ss_dag_set D, WarpLayou
             if (lane == 0) R.out.chain_hash[(int64_t)dag * n_req + r] = h;
         }
         if (lane == 0 && slot) slot[0] = cnt;
-        __syncwarp();
+        }
+        __syncthreads();
         ++done;
     }
-    __syncwarp();
+    __syncthreads();
     mark(2);
-    if (R.prof && lane == 0)
+    if (R.prof && tid == 0)
         for (int k = 0; k < 3; ++k) atomicAdd(&R.prof[k], pacc[k]);
-    for (int g = lane; g < ng; g += 32) R.st.occ[gbase + g] = occ[g];
-    for (int q = lane; q < A.ring_len; q += 32) ring_g[q] = ring[q];
-    if (lane == 0) {
+    for (int g = tid; g < ng; g += NT) R.st.occ[gbase + g] = occ[g];
+    for (int q = tid; q < A.ring_len; q += NT) ring_g[q] = ring[q];
+    if (tid == 0) {
         R.st.next_req[dag] = req0 + done;
         if (status != SS_OK) { R.st.status[dag] = status; R.st.aux[dag] = aux; }
     }
@@ -350,12 +461,22 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
     cudaStream_t s = ss_stream(stream_h);
     if (getenv("SS_WARP_PROF") && cudaMalloc(&R.prof, 4 * sizeof(unsigned long long)) == cudaSuccess)
         cudaMemsetAsync(R.prof, 0, 4 * sizeof(unsigned long long), s);
-    // One warp per scenario.  Splitting a column's sources over 2-4 warps (one barrier per boundary, each warp
-    // merging its own next positions) measured slower at C2 (27e3 vs 33e3 sel/s): at <= 32 hosts the per-warp
-    // fixed work (partial merge, shuffles, the 8-wide tournament) outweighs the shorter source ranges.
-    if (cudaFuncSetAttribute(replay_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
-        return SS_CUDA_ERROR;
-    replay_warp_kernel<<<D.n_dags, 32, A.total, s>>>(D, A, R);
+    // One CTA per scenario.  An earlier split of each column's SOURCES over warps (partials merged through
+    // shared memory) measured slower at C2 (27e3 vs 33e3 sel/s); splitting the DESTINATIONS (mw_route) keeps
+    // every merge inside a warp and only adds the boundary barrier.
+    auto run = [&](auto kern, int threads) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
+            return SS_CUDA_ERROR;
+        kern<<<D.n_dags, threads, A.total, s>>>(D, A, R);
+        return SS_OK;
+    };
+    // destinations per boundary over ceil(hosts / 8) warps (latency: C2's 17 hosts -> 3 warps)
+    int rc;
+    if (D.max_hosts <= 8) rc = run(replay_warp_kernel<1>, 32);
+    else if (D.max_hosts <= 16) rc = run(replay_warp_kernel<2>, 64);
+    else if (D.max_hosts <= 24) rc = run(replay_warp_kernel<3>, 96);
+    else rc = run(replay_warp_kernel<4>, 128);
+    if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
     if (R.prof) {
         unsigned long long h[4];

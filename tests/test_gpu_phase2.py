@@ -277,3 +277,28 @@ def test_warp_replay_c2_shape_vs_oracle(cuda_ready, window):
         assert rp.occ.view(S, -1)[s].cpu().numpy().tolist() == want_occ.tolist(), s
         for r in range(n_req):
             assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,L,nwd", [(16, 48, 1), (24, 32, 2), (36, 24, 3), (48, 24, 4)])
+def test_warp_replay_destination_split_widths_vs_oracle(cuda_ready, n, L, nwd):
+    """replay_warp_kernel<NWD> at every warp count (column widths 1-8, 9-16, 17-24, 25-32 hosts) vs the oracle."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from oracle import alloc_ref
+    cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    S, n_req, window = 4, 36, 16
+    ss = scen.build_scenarios(cl, model, plan, S, seed0=900 + n, churn=0.05, jitter=True)
+    widest = max(max(len(c) for c in ss.columns(s)) for s in range(S))
+    assert (widest + 7) // 8 == nwd, widest
+    rp = ScenarioReplayer(ss, window=window, max_requests=n_req + 4, mode="warp")
+    out = rp.run(n_req, gpus=True)
+    rp.raise_first_failure()
+    gpus, cost = out.gpus.cpu().numpy(), out.cost.cpu().numpy()
+    for s in range(S):
+        want_g, want_c, want_occ, _ = chain_ref.replay(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), n_req, window,
+                                                       chain_ref.occ_power_table(n_req + 4))
+        assert gpus[s].tolist() == want_g, s
+        assert cost[s].tolist() == want_c, s
+        assert rp.occ.view(S, -1)[s].cpu().numpy().tolist() == want_occ.tolist(), s
