@@ -62,3 +62,12 @@ def hops_from_gpus(gpus):
             start = l
     hops.append([gpus[-1], start, len(gpus)])
     return hops
+
+
+def stream_digests(hashes, costs, block):
+    """Per-block digests of (chain hash, cost bits), as tests/golden/make_c2_stream_golden.py writes them."""
+    import hashlib
+    h = np.asarray(hashes, dtype=np.int64).astype("<u8", copy=False)
+    c = np.asarray(costs, dtype="<f8").view("<u8")
+    rec = np.stack([h, c], axis=1)
+    return [hashlib.sha256(rec[i:i + block].tobytes()).hexdigest()[:16] for i in range(0, len(rec), block)]
