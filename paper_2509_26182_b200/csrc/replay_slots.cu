@@ -427,12 +427,19 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         }
     };
     // apply(b), b >= 1: row + column of every GPU entering the frontier at b (TMA-staged units)
+    unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};    // prologue, relax, apply, barrier, epilogue, TMA wait
     auto apply = [&](int b) {
         const BlkMeta m = bm[b];
         const int units = 2 * m.n_ins;
         for (int u0 = 0; u0 < units; u0 += upc) {
             const int nu = min(upc, units - u0);
-            mbar_wait(&full[cbuf], cphase);
+            if (A.prof) {
+                const long long t0 = clock64();
+                mbar_wait(&full[cbuf], cphase);
+                pacc[5] += (unsigned long long)(clock64() - t0);
+            } else {
+                mbar_wait(&full[cbuf], cphase);
+            }
             const double* stg = reinterpret_cast<const double*>(smem + A.off_stage + (size_t)cbuf * A.stage_bytes);
             for (int ul = warp; ul < nu; ul += NW) {
                 const int u = u0 + ul;
@@ -482,7 +489,6 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     int done = 0;
     consumer_sync(NC);
 
-    unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};    // prologue, merge+relax, apply, barrier, epilogue
     long long tp = clock64();
 #define SS_PROF(k)                                                   \
     if (A.prof) {                                                    \
@@ -629,7 +635,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     SS_PROF(4)
 #undef SS_PROF
     if (A.prof && lane == 0)
-        for (int k = 0; k < 5; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
+        for (int k = 0; k < 6; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
     for (int g = tid; g < ng; g += NC) R.st.occ[gbase + g] = occ_s[g];
     if (tid == 0) {
         R.st.next_req[dag] = req0 + done;
@@ -755,8 +761,9 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
                     A.total, A.nbuf, A.stage_bytes, A.s_rows);
             for (int w = 0; w < 9; ++w) {
                 const double d = (double)D.n_dags * n_req;
-                fprintf(stderr, "  w%d prologue %.0f relax %.0f apply %.0f barrier %.0f epilogue %.0f\n", w,
-                        h[w * 8 + 0] / d, h[w * 8 + 1] / d, h[w * 8 + 2] / d, h[w * 8 + 3] / d, h[w * 8 + 4] / d);
+                fprintf(stderr, "  w%d prologue %.0f relax %.0f apply %.0f (of which TMA wait %.0f) barrier %.0f epilogue %.0f\n",
+                        w, h[w * 8 + 0] / d, h[w * 8 + 1] / d, h[w * 8 + 2] / d, h[w * 8 + 5] / d, h[w * 8 + 3] / d,
+                        h[w * 8 + 4] / d);
             }
             cudaFree(A.prof);
         }

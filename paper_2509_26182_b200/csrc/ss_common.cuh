@@ -82,8 +82,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // producer-side wait: back off so a spinning lane does not steal issue slots from the consumers
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+// Producer-side wait with exponential backoff (128 ns .. max_ns): a ring refill is due about once per
+// boundary, so a polling producer would only steal issue slots from the consumer warps of its SM sub-partition
+// (a fixed 64 ns sleep measured 25% of the slot kernel's instructions in this loop).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, unsigned max_ns = 1024) {
+    unsigned ns = 128;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < max_ns ? 2 * ns : max_ns;
+    }
 }
 
 // ---------------------------------------------------------------------------
