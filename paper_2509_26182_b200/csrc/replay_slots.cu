@@ -445,11 +445,15 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
                 const int u = u0 + ul;
                 const int slot = ins[2 * (m.ins_start + (u >> 1))];
                 const double* su = stg + ul * Wp;
-                if (u & 1) {
-                    for (int t = lane; t < tw; t += 32) T[t * W + slot] = su[t];
-                } else {
-                    for (int t = lane; t < tw; t += 32) T[slot * W + t] = su[t];
-                }
+                // tw <= s_rows <= SC: all DPL loads in flight before the stores (one LDS latency per unit)
+                double x[DPL];
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) x[d] = lane + 32 * d < tw ? su[lane + 32 * d] : 0.0;
+                const int step = (u & 1) ? 32 * W : 32;                  // column: stride W; row: contiguous
+                double* dst = T + ((u & 1) ? lane * W + slot : slot * W + lane);
+#pragma unroll
+                for (int d = 0; d < DPL; ++d)
+                    if (lane + 32 * d < tw) dst[d * step] = x[d];
             }
             release_chunk();
         }

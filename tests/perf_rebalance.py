@@ -66,4 +66,14 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--profile" in sys.argv:                      # host-side hot spots of the loop (cProfile)
+        import cProfile
+        import pstats
+        sys.argv.remove("--profile")
+        pr = cProfile.Profile()
+        pr.enable()
+        main()
+        pr.disable()
+        pstats.Stats(pr).sort_stats("cumulative").print_stats("paper_2509|_phase1|batched|method .to|cpu", 40)
+    else:
+        main()
