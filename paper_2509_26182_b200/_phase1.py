@@ -63,6 +63,12 @@ class PoolBatch:
         cand_k = np.concatenate([np.arange(1, km[p] + 1) for p in cover_p]) if cover_p.size else np.zeros(0)
         all_pool = np.repeat(np.arange(P), km)
         all_k = np.concatenate([np.arange(1, k + 1) for k in km]) if km.sum() else np.zeros(0)
+        # one thread per candidate: order by (k, pool) so a warp's 32 candidates share k (and hence loop
+        # trip counts) -- outputs are addressed by (pool, k), so the order is free
+        o = np.lexsort((cand_pool, cand_k))
+        cand_pool, cand_k = cand_pool[o], cand_k[o]
+        o = np.lexsort((all_pool, all_k))
+        all_pool, all_k = all_pool[o], all_k[o]
         self.exact = exact
         self.n_cover = int(cand_pool.size)
         self.n_cand = int(all_pool.size)
