@@ -68,3 +68,19 @@ def test_device_path_reproduces_reference_json(cuda_ready, tmp_path, wire_cases,
         rp.raise_first_failure()
         chains = chains_from_replay(ss.ids, res.gpus.cpu().numpy()[0], res.cost.cpu().numpy()[0])
         assert chains_to_json(chains) + "\n" == c["route_json"], mode
+
+
+def test_layer_load_helpers_known_values():
+    """perfmap.py:73-114 exports: blend, zero denominators, population CoV (known answers)."""
+    import math
+    from paper_2509_26182_b200 import LayerLoad, layer_load, layer_load_cov
+    assert layer_load(2.0, 1.0, 8.0, 4.0) == 0.5 * 0.25 + 0.5 * 0.25
+    assert layer_load(2.0, 1.0, 0.0, 0.0, mix_alpha=0.3) == 0.0
+    assert layer_load(2.0, 3.0, 4.0, 6.0, mix_alpha=1.0) == 0.5
+    with pytest.raises(ValueError):
+        layer_load(1.0, 1.0, 1.0, 1.0, mix_alpha=1.5)
+    assert layer_load_cov([]) == 0.0 and layer_load_cov([0.0, 0.0]) == 0.0
+    assert layer_load_cov([1.0, 3.0]) == 0.5
+    assert layer_load_cov([2.0, 2.0, 2.0]) == 0.0
+    assert math.isclose(layer_load_cov([1.0, 2.0, 3.0, 4.0]), math.sqrt(1.25) / 2.5, rel_tol=0, abs_tol=0)
+    assert LayerLoad(3, 0.2, 0.6, 0.25).value == 0.25 * 0.2 + 0.75 * 0.6
