@@ -1,0 +1,148 @@
+"""Serving-simulator entry points of the drop-in (``pkg/src/swarmsched/sim.py``), backed by the device simulator.
+
+Same names, fields and semantics as the reference for the pieces the hot path feeds:
+
+* ``Request`` (sim.py:62-76), the trace wire format ``request_from_dict`` / ``request_to_dict`` /
+  ``load_trace`` / ``save_trace`` (79-115, JSON lines ``{"id", "t", "prompt_tokens", "output_tokens"}``);
+* ``generate_trace`` (118-148): Poisson arrivals from ``random.Random(seed)``, ids ``r00000``...;
+* ``percentile`` (151-159, nearest rank) and ``MetricsReport`` (190-217);
+* ``run_simulation`` (478-510): the discrete-event serving simulation of one cluster / plan / trace.  The event
+  loop runs on the GPU (``ss_sim_warp`` for <= 32 hosts per layer, ``ss_sim_cta`` up to 256) through
+  ``ScenarioReplayer.simulate``; this wrapper only packs the pool and unpacks the report.
+
+Not on the device path: membership events inside the simulator timeline (``sim.py:_on_membership``) -- the batched
+replayer runs that loop instead (``ScenarioReplayer.rebalance``) -- and latency entries that expire between publish
+ticks (``ttl_multiplier < 1``).  Both raise ``NotImplementedError`` rather than silently diverging.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import Iterable, List, Sequence, Tuple
+
+import numpy as np
+
+from .errors import EmptySample
+from .perfmap import DEFAULT_PUBLISH_INTERVAL_S, DEFAULT_TTL_MULTIPLIER
+from .plan import AllocationPlan
+from .topology import ClusterSnapshot, ModelSpec
+
+
+@dataclass(frozen=True)
+class Request:
+    id: str
+    arrival_s: float
+    prompt_tokens: int
+    output_tokens: int
+
+    def __post_init__(self) -> None:
+        if self.prompt_tokens < 1:
+            raise ValueError(f"prompt_tokens must be >= 1, got {self.prompt_tokens}")
+        if self.output_tokens < 0:
+            raise ValueError(f"output_tokens must be >= 0, got {self.output_tokens}")
+
+    @property
+    def total_tokens(self) -> int:
+        return self.prompt_tokens + self.output_tokens
+
+
+def request_from_dict(raw: dict) -> Request:
+    return Request(id=str(raw["id"]), arrival_s=float(raw["t"]), prompt_tokens=int(raw["prompt_tokens"]),
+                   output_tokens=int(raw["output_tokens"]))
+
+
+def request_to_dict(request: Request) -> dict:
+    return {"id": request.id, "t": request.arrival_s, "prompt_tokens": request.prompt_tokens,
+            "output_tokens": request.output_tokens}
+
+
+def load_trace(path: str) -> List[Request]:
+    """JSON-lines trace, blank lines skipped, sorted by arrival (stable)."""
+    out = []
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, 1):
+            line = line.strip()
+            if not line:
+                continue
+            try:
+                out.append(request_from_dict(json.loads(line)))
+            except (TypeError, KeyError, AttributeError) as exc:
+                raise ValueError(f"{path}:{lineno}: bad trace line ({exc})") from exc
+    out.sort(key=lambda r: r.arrival_s)
+    return out
+
+
+def save_trace(requests: Iterable[Request], path: str) -> None:
+    with open(path, "w", encoding="utf-8") as fh:
+        for r in requests:
+            fh.write(json.dumps(request_to_dict(r), sort_keys=True) + "\n")
+
+
+def generate_trace(rate_rps: float, duration_s: float, *, seed: int = 0, prompt_tokens: Tuple[int, int] = (32, 256),
+                   output_tokens: Tuple[int, int] = (16, 128)) -> List[Request]:
+    """Poisson arrivals at rate_rps over [0, duration_s) with uniform token counts (the reference's draws)."""
+    from .scenarios import generate_trace as draws
+    arrival, prompt, output = draws(rate_rps, duration_s, seed=seed, prompt_tokens=tuple(prompt_tokens),
+                                    output_tokens=tuple(output_tokens))
+    return [Request(f"r{i:05d}", float(a), int(p), int(o))
+            for i, (a, p, o) in enumerate(zip(arrival.tolist(), prompt.tolist(), output.tolist()))]
+
+
+def percentile(values: Sequence[float], p: float) -> float:
+    """Nearest-rank percentile, p in (0, 100]."""
+    if not values:
+        raise EmptySample("percentile of an empty sample")
+    if not 0.0 < p <= 100.0:
+        raise ValueError(f"p must be in (0, 100], got {p}")
+    ordered = sorted(values)
+    return ordered[max(1, math.ceil(p * len(ordered) / 100.0)) - 1]
+
+
+@dataclass(frozen=True)
+class MetricsReport:
+    submitted: int
+    completed: int
+    unserved: int
+    aborted: int
+    duration_s: float
+    throughput_rps: float
+    latency_mean_s: float
+    latency_p50_s: float
+    latency_p95_s: float
+    latency_p99_s: float
+    queue_peak: int
+
+    def to_dict(self) -> dict:
+        return {name: getattr(self, name) for name in self.__dataclass_fields__}
+
+
+def run_simulation(cluster: ClusterSnapshot, model: ModelSpec, plan: AllocationPlan, trace: Sequence[Request], *,
+                   membership_events: Sequence = (), publish_interval_s: float = DEFAULT_PUBLISH_INTERVAL_S,
+                   ttl_multiplier: float = DEFAULT_TTL_MULTIPLIER, contention_exponent: float = 1.0,
+                   amortize_rtt: bool = False, mix_alpha: float = 0.5, cov_threshold: float = 0.5, alpha: float = 1.0,
+                   mean_tokens_per_request: float = 128.0) -> MetricsReport:
+    """Run the trace against the plan on the GPU and report latency / throughput (sim.py:478-510).
+
+    mix_alpha, cov_threshold, alpha and mean_tokens_per_request only steer membership handling, which this entry
+    point does not run (see the module docstring).
+    """
+    if len(membership_events):
+        raise NotImplementedError("membership events inside the simulator timeline are not on the device path; "
+                                  "use batched.ScenarioReplayer.rebalance for the churn / rebalance loop")
+    if ttl_multiplier < 1.0:
+        raise NotImplementedError("ttl_multiplier < 1 lets latency entries expire between publish ticks; "
+                                  "the device simulator keeps every entry live")
+    from . import scenarios as scen
+    from .batched import ScenarioReplayer, replay_mode
+    ss = scen.build_scenarios(cluster, model, plan, 1, churn=0.0, jitter=False)
+    mode = "warp" if replay_mode(ss, window=1) == "warp" else "blocks"
+    order = sorted(range(len(trace)), key=lambda i: trace[i].arrival_s)       # arrival order, ties by position
+    arrays = (np.array([trace[i].arrival_s for i in order], dtype=np.float64),
+              np.array([trace[i].prompt_tokens for i in order], dtype=np.int32),
+              np.array([trace[i].output_tokens for i in order], dtype=np.int32))
+    rp = ScenarioReplayer(ss, window=1, mode=mode)
+    rep = rp.simulate([arrays], publish_interval=float(publish_interval_s), amortize_rtt=bool(amortize_rtt),
+                      contention=float(contention_exponent))[0]
+    return MetricsReport(**{name: rep[name] for name in MetricsReport.__dataclass_fields__})

@@ -82,3 +82,48 @@ def test_generate_trace_matches_reference_draws(sim_cases):
         a, p, o = generate_trace(c["rate"], c["duration"], seed=c["seed"], prompt_tokens=tuple(c["prompt"]),
                                  output_tokens=tuple(c["output"]))
         assert [[x.hex(), int(y), int(z)] for x, y, z in zip(a.tolist(), p, o)] == c["trace"]
+
+
+def test_dropin_trace_api_matches_reference_draws(sim_cases, tmp_path):
+    """sim.py:62-159 drop-ins: generate_trace Requests (ids, draws), JSON-lines round trip, nearest-rank percentile."""
+    from paper_2509_26182_b200 import EmptySample, Request, generate_trace, load_trace, percentile, save_trace
+    c = sim_cases["c2_mid"]
+    tr = generate_trace(c["rate"], c["duration"], seed=c["seed"], prompt_tokens=tuple(c["prompt"]),
+                        output_tokens=tuple(c["output"]))
+    assert [[r.arrival_s.hex(), r.prompt_tokens, r.output_tokens] for r in tr] == c["trace"]
+    assert tr[0].id == "r00000" and tr[-1].id == f"r{len(tr) - 1:05d}"
+    path = str(tmp_path / "trace.jsonl")
+    save_trace(list(reversed(tr)), path)
+    assert load_trace(path) == tr
+    assert percentile([5.0, 1.0, 3.0], 50) == 3.0 and percentile([5.0, 1.0, 3.0], 100) == 5.0
+    assert percentile([2.0], 0.1) == 2.0
+    with pytest.raises(EmptySample):
+        percentile([], 50)
+    with pytest.raises(ValueError):
+        Request("x", 0.0, 0, 1)
+
+
+def test_run_simulation_rejects_what_the_device_path_does_not_run():
+    from paper_2509_26182_b200 import run_simulation
+    with pytest.raises(NotImplementedError):
+        run_simulation(None, None, None, [], membership_events=[object()])
+    with pytest.raises(NotImplementedError):
+        run_simulation(None, None, None, [], ttl_multiplier=0.5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_run_simulation_dropin_matches_reference(cuda_ready, sim_cases, name):
+    """The public run_simulation (sim.py:478-510) on the device vs the reference's MetricsReport, bit for bit."""
+    from paper_2509_26182_b200 import Request, run_simulation
+    from paper_2509_26182_b200 import scenarios as scen
+    c = sim_cases[name]
+    cl, model = scen.synthetic_cluster(c["n"], seed=0, model=scen.bench_model(c["L"]))
+    d = alloc_ref.allocate(cl, model)
+    d["objective"] = d["objective"].hex()
+    d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+    plan = plan_from_golden(d)
+    trace = [Request(f"r{i:05d}", a, p, o) for i, (a, p, o) in enumerate(trace_of(c))]
+    rep = run_simulation(cl, model, plan, trace[::-1], amortize_rtt=c["amortize"],
+                         contention_exponent=c["contention"])
+    assert report_hex(rep.to_dict()) == c["report"]
