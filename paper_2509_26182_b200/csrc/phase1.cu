@@ -173,7 +173,7 @@ struct Lists {
 
 __device__ __forceinline__ int cval(const int* caps, int i, int L) { return caps[i] < L ? caps[i] : L; }
 
-__device__ bool best_fit(const int* caps, int m, int k, int L, Lists& G) {
+__device__ bool best_fit(const int* caps, int m, int k, int L, Lists& G, const volatile int32_t* cancel = nullptr) {
     G.reset(k);
     for (int g = 0; g < k; ++g) {
         G.item[g] = (uint16_t)g;
@@ -191,6 +191,7 @@ __device__ bool best_fit(const int* caps, int m, int k, int L, Lists& G) {
     }
     uint16_t opened[KMAX];
     for (int round = 0; round < 4; ++round) {
+        if (cancel && *cancel < m) return false;            // parallel-m search: a smaller m already succeeded
         int n_open = 0;
         for (int g = 0; g < k; ++g) if (G.tot[g] < L) opened[n_open++] = (uint16_t)g;
         if (n_open == 0) break;
@@ -335,7 +336,9 @@ __device__ void compute_reach(const int* caps, int L, const uint16_t* items, int
 }
 
 // returns true on success; the k groups are then fr[0..k-1].picked, in peel order
-__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reach, uint16_t* items) {
+// cancel (optional): the parallel-m search's best success so far; an attempt at a larger m gives up
+__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reach, uint16_t* items,
+                     const volatile int32_t* cancel = nullptr) {
     int budget = m <= 24 ? 300 : 80;
     int d = 0;
     int total = 0;
@@ -351,6 +354,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
             if (f.need == 0) { ok = true; state = RET; continue; }
             if (budget <= 0) { ok = false; state = RET; continue; }
             --budget;
+            if (cancel && *cancel < m) return false;        // a smaller m already succeeded
             Mask pool;
             frame_pool(fr, d, m, pool);
             if (f.total < f.need * L || pool.count() < f.need) { ok = false; state = RET; continue; }
@@ -722,6 +726,70 @@ __global__ void exact_sweep_kernel(ss_pool_set P, const int64_t* koff, int32_t* 
     }
 }
 
+constexpr int COVER_UNSET = 0x7f7f7f7f;
+
+// Constructive path of one (pool, k) candidate (allocator.py:426-470): m runs from m0 upward and the first m
+// whose best-fit or (failing that) peel succeeds gives the groups.  Split into setup / one attempt so the m
+// loop can run serially (cover_kernel, large batches) or with every m in parallel (cover_try_kernel +
+// cover_finish_kernel, small batches such as one allocate() call) -- the smallest successful m is the same.
+struct CoverCand {
+    const int* caps;
+    int n, n_all, L, kmax, m0;
+    int64_t ko;
+};
+
+// false: k is infeasible for the pool (the reference's `break` on prefix < k*L)
+__device__ bool cover_setup(const ss_pool_set& P, const int64_t* koff, int p, int k, CoverCand& cc) {
+    const int off = P.pool_ptr[p];
+    cc.n_all = P.pool_ptr[p + 1] - off;
+    cc.caps = P.caps + off;
+    cc.L = P.layers[p];
+    cc.kmax = P.kmax[p];
+    cc.n = usable_count(cc.caps, cc.n_all);
+    cc.ko = koff[p] + k - 1;
+    long long prefix_n = 0;
+    for (int i = 0; i < cc.n; ++i) prefix_n += cval(cc.caps, i, cc.L);
+    const long long target = (long long)k * cc.L;
+    if (prefix_n < target) return false;
+    const int pgm = (cc.L + cval(cc.caps, 0, cc.L) - 1) / cval(cc.caps, 0, cc.L);
+    int m_cap = 0;
+    long long acc = 0;
+    while (m_cap < cc.n && acc < target) acc += cval(cc.caps, m_cap++, cc.L);   // bisect_left(prefix, target)
+    cc.m0 = k * pgm > m_cap ? k * pgm : m_cap;
+    return true;
+}
+
+// One attempt at group count m: best-fit, then peel.  On success writes the groups when mout != nullptr.
+__device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr, Bits* reach, uint16_t* items,
+                          int* mout, int* gout, int32_t* stage_out, const volatile int32_t* cancel = nullptr) {
+    if (best_fit(cc.caps, m, k, cc.L, G, cancel)) {
+        if (mout) {
+            int pos = 0, stg = 0;
+            for (int g = 0; g < k; ++g) {
+                for (int nd = G.head[g]; nd != NIL; nd = G.next[nd]) mout[pos++] = G.item[nd];
+                gout[g] = G.size[g];
+                stg += G.size[g];
+            }
+            *stage_out = stg;
+        }
+        return true;
+    }
+    if (peel(cc.caps, m, k, cc.L, fr, reach, items, cancel)) {
+        if (mout) {
+            int pos = 0, stg = 0;
+            for (int g = 0; g < k; ++g) {
+                int cnt = 0;
+                for (int i = 0; i < m; ++i) if (fr[g].picked.test(i)) { mout[pos++] = i; ++cnt; }
+                gout[g] = cnt;
+                stg += cnt;
+            }
+            *stage_out = stg;
+        }
+        return true;
+    }
+    return false;
+}
+
 // one thread per (pool, k) on the constructive path; stage 0 = absent / stalled
 __global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members, int32_t* gsize,
                              const int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k, int n_cand,
@@ -730,52 +798,66 @@ __global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages
     if (c >= n_cand) return;
     const int p = cand_pool[c], k = cand_k[c];
     if (pool_status[p] != SS_OK) return;
-    const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
-    const int* caps = P.caps + off;
-    const int L = P.layers[p], kmax = P.kmax[p];
-    const int n = usable_count(caps, n_all);
-    const int64_t ko = koff[p] + k - 1;
-    stages[ko] = 0;
-    stall[ko] = 0;
-    long long prefix_n = 0;
-    for (int i = 0; i < n; ++i) prefix_n += cval(caps, i, L);
-    const long long target = (long long)k * L;
-    if (prefix_n < target) { stall[ko] = 2; return; }         // reference `break` (infeasible k)
-    const int pgm = (L + cval(caps, 0, L) - 1) / cval(caps, 0, L);
-    int m_cap = 0;
-    long long acc = 0;
-    while (m_cap < n && acc < target) acc += cval(caps, m_cap++, L);   // bisect_left(prefix, target)
-    int m0 = k * pgm > m_cap ? k * pgm : m_cap;
+    CoverCand cc;
+    const bool feasible = cover_setup(P, koff, p, k, cc);
+    stages[cc.ko] = 0;
+    stall[cc.ko] = 0;
+    if (!feasible) { stall[cc.ko] = 2; return; }                // reference `break` (infeasible k)
     Lists G;
     Frame fr[KMAX + 2];
     Bits reach[NMAX + 1];
     uint16_t items[NMAX];
-    int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * n_all;
-    int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * kmax;
-    for (int m = m0; m <= n; ++m) {
-        if (best_fit(caps, m, k, L, G)) {
-            int pos = 0, stg = 0;
-            for (int g = 0; g < k; ++g) {
-                for (int nd = G.head[g]; nd != NIL; nd = G.next[nd]) mout[pos++] = G.item[nd];
-                gout[g] = G.size[g];
-                stg += G.size[g];
-            }
-            stages[ko] = stg;
-            return;
-        }
-        if (peel(caps, m, k, L, fr, reach, items)) {
-            int pos = 0, stg = 0;
-            for (int g = 0; g < k; ++g) {
-                int cnt = 0;
-                for (int i = 0; i < m; ++i) if (fr[g].picked.test(i)) { mout[pos++] = i; ++cnt; }
-                gout[g] = cnt;
-                stg += cnt;
-            }
-            stages[ko] = stg;
-            return;
-        }
-    }
-    stall[ko] = 1;                                               // constructive grouping stalled
+    int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
+    int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
+    for (int m = cc.m0; m <= cc.n; ++m)
+        if (cover_try(cc, k, m, G, fr, reach, items, mout, gout, stages + cc.ko)) return;
+    stall[cc.ko] = 1;                                            // constructive grouping stalled
+}
+
+// small batches, one round: thread (c, j) attempts m = m0 + m_off + j of candidate c unless an earlier round (a
+// smaller m) already succeeded; best_m[c] = the smallest m that succeeds
+__global__ void cover_try_kernel(ss_pool_set P, const int64_t* koff, const int32_t* pool_status,
+                                 const int32_t* cand_pool, const int32_t* cand_k, int n_cand, int m_off, int span,
+                                 int32_t* best_m) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_cand * span) return;
+    const int c = (int)(t / span), j = (int)(t % span);
+    if (best_m[c] != COVER_UNSET) return;                   // resolved by an earlier round (smaller m)
+    const int p = cand_pool[c], k = cand_k[c];
+    if (pool_status[p] != SS_OK) return;
+    CoverCand cc;
+    if (!cover_setup(P, koff, p, k, cc)) return;
+    const int m = cc.m0 + m_off + j;
+    if (m > cc.n) return;
+    Lists G;
+    Frame fr[KMAX + 2];
+    Bits reach[NMAX + 1];
+    uint16_t items[NMAX];
+    if (cover_try(cc, k, m, G, fr, reach, items, nullptr, nullptr, nullptr, best_m + c)) atomicMin(&best_m[c], m);
+}
+
+// small batches: rebuild the groups at the smallest successful m (or record the stall)
+__global__ void cover_finish_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members,
+                                    int32_t* gsize, const int32_t* pool_status, const int32_t* cand_pool,
+                                    const int32_t* cand_k, int n_cand, const int32_t* best_m, int32_t* stall) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cand) return;
+    const int p = cand_pool[c], k = cand_k[c];
+    if (pool_status[p] != SS_OK) return;
+    CoverCand cc;
+    const bool feasible = cover_setup(P, koff, p, k, cc);
+    stages[cc.ko] = 0;
+    stall[cc.ko] = 0;
+    if (!feasible) { stall[cc.ko] = 2; return; }
+    const int m = best_m[c];
+    if (m < cc.m0 || m > cc.n) { stall[cc.ko] = 1; return; }
+    Lists G;
+    Frame fr[KMAX + 2];
+    Bits reach[NMAX + 1];
+    uint16_t items[NMAX];
+    int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
+    int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
+    if (!cover_try(cc, k, m, G, fr, reach, items, mout, gout, stages + cc.ko)) stall[cc.ko] = 1;
 }
 
 // per pool: apply "first stalled / infeasible k drops every larger k"; validate order
@@ -1074,7 +1156,26 @@ extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* ko
                                      int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool,
                                      const int32_t* cand_k, int32_t n_cand, int32_t* stall, void* stream) {
     cudaStream_t s = ss_stream(stream);
-    if (n_cand > 0) {
+    // A batch too small to fill the GPU (one allocate() call: ~4 regions x k_max candidates) tries every group
+    // count m of every candidate in parallel; an attempt gives up as soon as a smaller m of its candidate has
+    // succeeded (peel polls best_m), and the smallest success is the reference's first-success m.  A large sweep
+    // keeps the work-efficient serial m loop of cover_kernel.
+    int32_t* best_m = nullptr;
+    if (n_cand > 0 && n_cand <= 2048 && cudaMallocAsync(&best_m, sizeof(int32_t) * n_cand, s) == cudaSuccess) {
+        cudaMemsetAsync(best_m, 0x7f, sizeof(int32_t) * n_cand, s);          // COVER_UNSET
+        int m_off = 0;
+        for (int span : {NMAX}) {                                             // m0 .. m0 + NMAX - 1 >= n
+            const int64_t nt = (int64_t)n_cand * span;
+            cover_try_kernel<<<(unsigned)((nt + 63) / 64), 64, 0, s>>>(*pools, koff, pool_status, cand_pool, cand_k,
+                                                                       n_cand, m_off, span, best_m);
+            SS_CHECK_LAUNCH();
+            m_off += span;
+        }
+        cover_finish_kernel<<<grid_for(n_cand, 64), 64, 0, s>>>(*pools, koff, stages, members, gsize, pool_status,
+                                                                 cand_pool, cand_k, n_cand, best_m, stall);
+        SS_CHECK_LAUNCH();
+        cudaFreeAsync(best_m, s);
+    } else if (n_cand > 0) {
         cover_kernel<<<grid_for(n_cand, 64), 64, 0, s>>>(*pools, koff, stages, members, gsize, pool_status, cand_pool,
                                                           cand_k, n_cand, stall);
         SS_CHECK_LAUNCH();

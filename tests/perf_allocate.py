@@ -15,11 +15,14 @@ def main():
         cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
         allocate(cl, model)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(5):
+        ts = []
+        for _ in range(20):
+            t0 = time.perf_counter()
             plan = allocate(cl, model)
-        t = (time.perf_counter() - t0) / 5
-        print(f"n={n} L={L}: allocate {1e3 * t:.1f} ms (k={plan.replication_count})")
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        print(f"n={n} L={L}: allocate min {1e3 * ts[0]:.1f} / median {1e3 * ts[10]:.1f} / max {1e3 * ts[-1]:.1f} ms "
+              f"(k={plan.replication_count})")
 
 
 if __name__ == "__main__":
