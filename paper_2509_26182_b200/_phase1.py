@@ -96,18 +96,18 @@ class PoolBatch:
         self.koff, self.memb_off, self.gsz_off = i64[:P], i64[P:2 * P], i64[2 * P:]
         self.flops = torch.from_numpy(flops).to(dev)
         K, M, G = int(koff[-1]), int(memb[-1]), int(gsz[-1])
-        self.stages = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
-        self.stall = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
-        self.kstatus = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
-        self.fstatus = torch.zeros(max(K, 1), dtype=torch.int32, device=dev)
-        self.z = torch.zeros(max(K, 1), dtype=torch.float64, device=dev)
-        self.members = torch.zeros(max(M, 1), dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(max(M, 1), dtype=torch.int32, device=dev)
-        self.gsize = torch.zeros(max(G, 1), dtype=torch.int32, device=dev)
-        self.status = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
-        self.aux = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
-        self.best_k = torch.zeros(max(P, 1), dtype=torch.int32, device=dev)
-        self.sweep_stats = torch.zeros(max(exact.size, 1) * 4, dtype=torch.int32, device=dev)
+        # outputs: one zeroed int32 block + one fp64 block (two allocations, two D2H copies in fetch())
+        sizes = [("stages", max(K, 1)), ("stall", max(K, 1)), ("kstatus", max(K, 1)), ("fstatus", max(K, 1)),
+                 ("members", max(M, 1)), ("counts", max(M, 1)), ("gsize", max(G, 1)), ("status", max(P, 1)),
+                 ("aux", max(P, 1)), ("best_k", max(P, 1)), ("sweep_stats", max(exact.size, 1) * 4)]
+        self._iblock = torch.zeros(sum(c for _, c in sizes), dtype=torch.int32, device=dev)
+        o = 0
+        for name, cnt in sizes:
+            setattr(self, name, self._iblock[o:o + cnt])
+            o += cnt
+        self._fblock = torch.zeros(max(K, 1) + 1, dtype=torch.float64, device=dev)
+        self.z = self._fblock[:max(K, 1)]
+        self.total = self._fblock[max(K, 1):]              # spare slot: allocate()'s objective_total
         self.fcap, self.ccap = 4096, 65536
 
     def pool_set(self) -> N.PoolSet:
@@ -178,15 +178,19 @@ class PoolResults:
 
     def __init__(self, b: PoolBatch):
         self.b = b
-        self.stages = b.stages.cpu().numpy()
-        self.members = b.members.cpu().numpy()
-        self.gsize = b.gsize.cpu().numpy()
-        self.status = b.status.cpu().numpy()
-        self.aux = b.aux.cpu().numpy()
-        self.z = b.z.cpu().numpy()
-        self.counts = b.counts.cpu().numpy()
-        self.best_k = b.best_k.cpu().numpy()
-        self.sweep_stats = b.sweep_stats.cpu().numpy().reshape(-1, 4)
+        ib = b._iblock.cpu().numpy()
+        fb = b._fblock.cpu().numpy()
+        view = lambda t: ib[t.storage_offset(): t.storage_offset() + t.numel()]
+        self.stages = view(b.stages)
+        self.members = view(b.members)
+        self.gsize = view(b.gsize)
+        self.status = view(b.status)
+        self.aux = view(b.aux)
+        self.counts = view(b.counts)
+        self.best_k = view(b.best_k)
+        self.sweep_stats = view(b.sweep_stats).reshape(-1, 4)
+        self.z = fb[:b.z.numel()]
+        self.total = float(fb[-1])
 
     def raise_pool(self, p: int) -> None:
         st = int(self.status[p])

@@ -181,11 +181,10 @@ def allocate(cluster: ClusterSnapshot, model: ModelSpec, *, alpha: float = 1.0,
     lib = N.lib()
     dev = batch.dev
     var_ptr = torch.tensor([0, len(pools)], dtype=torch.int32, device=dev)
-    total = torch.empty(1, dtype=torch.float64, device=dev)
     feas = torch.empty(1, dtype=torch.int32, device=dev)
     N.check(lib.ss_variant_reduce(1, N.ptr(var_ptr), N.ptr(batch.koff), N.ptr(batch.best_k), N.ptr(batch.z),
-                                  N.ptr(batch.status), N.ptr(total), N.ptr(feas), None, None, N.stream_handle()),
-            "ss_variant_reduce")
+                                  N.ptr(batch.status), N.ptr(batch.total), N.ptr(feas), None, None,
+                                  N.stream_handle()), "ss_variant_reduce")
     res = batch.fetch()
     pipelines: List[Pipeline] = []
     per_k: List[PerKEntry] = []
@@ -210,5 +209,5 @@ def allocate(cluster: ClusterSnapshot, model: ModelSpec, *, alpha: float = 1.0,
     if not pipelines:
         raise NoFeasiblePipeline(f"no region can host all {L} layers of {model.name!r}")
     return AllocationPlan(replication_count=len(pipelines), pipelines=tuple(pipelines),
-                          stage_total=sum(pp.stage_count for pp in pipelines), objective_score=float(total.cpu()[0]),
+                          stage_total=sum(pp.stage_count for pp in pipelines), objective_score=res.total,
                           per_k_table=tuple(per_k))

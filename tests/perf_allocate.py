@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     from paper_2509_26182_b200 import allocate, scenarios as scen
-    for n, L in [(64, 64), (256, 64), (256, 80)]:
+    for n, L in [(4, 48), (8, 48), (16, 48), (32, 48), (64, 48), (128, 48), (256, 48), (8, 32), (64, 64), (256, 64),
+                 (256, 80)]:
         cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
         allocate(cl, model)
         torch.cuda.synchronize()

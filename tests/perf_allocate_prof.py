@@ -12,16 +12,17 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     from paper_2509_26182_b200 import allocate, scenarios as scen
-    cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+    n = int(os.environ.get("PN", "256")); L = int(os.environ.get("PL", "64"))
+    cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
     allocate(cl, model)
     torch.cuda.synchronize()
     pr = cProfile.Profile()
     pr.enable()
-    for _ in range(5):
+    for _ in range(200):
         allocate(cl, model)
     torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(40)
 
 
 if __name__ == "__main__":
