@@ -414,7 +414,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
 }
 
 // ---------------------------------------------------------------------------
-// exact sweep (allocator.py:114-264), one thread per pool
+// exact sweep (allocator.py:114-264): state records shared by the CTA sweep and the one-thread replay
 // ---------------------------------------------------------------------------
 struct SRec {            // one state: residual bytes (value+1, zero padded) as a 128-bit big-endian key
     uint64_t hi, lo;
@@ -449,172 +449,10 @@ __device__ __forceinline__ bool key_eq(const SRec& a, const SRec& b) {
     return a.hi == b.hi && a.lo == b.lo && a.done == b.done;
 }
 
-// class order: (done, m, residual key)
-__device__ __forceinline__ bool class_less(const SRec& a, const SRec& b) {
-    if (a.done != b.done) return a.done < b.done;
-    if (a.m != b.m) return a.m < b.m;
-    if (a.hi != b.hi) return a.hi < b.hi;
-    return a.lo < b.lo;
-}
-
-template <class Less>
-__device__ void merge_sort_idx(int32_t* idx, int32_t* tmp, int n, Less less) {
-    for (int width = 1; width < n; width *= 2) {
-        for (int lo = 0; lo < n; lo += 2 * width) {
-            const int mid = min(lo + width, n), hi = min(lo + 2 * width, n);
-            int a = lo, b = mid, o = lo;
-            while (a < mid && b < hi) tmp[o++] = less(idx[b], idx[a]) ? idx[b++] : idx[a++];
-            while (a < mid) tmp[o++] = idx[a++];
-            while (b < hi) tmp[o++] = idx[b++];
-        }
-        for (int i = 0; i < n; ++i) idx[i] = tmp[i];
-    }
-}
-
 __device__ __forceinline__ void insert_sorted(uint8_t* res, int& m, uint8_t v) {
     int j = m++;
     while (j > 0 && res[j - 1] > v) { res[j] = res[j - 1]; --j; }
     res[j] = v;
-}
-
-struct SweepWs {
-    SRec* states;     // all kept states, level after level
-    SRec* kids;       // children of the current level
-    int32_t* idx;     // sort permutation
-    int32_t* tmp;
-    int32_t* keep;    // class-sorted kept list scratch
-};
-
-__device__ int exact_sweep(const int* caps, int n, int L, int kmax, SweepWs ws, int fcap, int ccap,
-                           int* level_start, int* found, int* need, int* stats) {
-    // stats (SweepStats, allocator.py:87-94): levels, states_expanded, peak_frontier, pruned_dominated
-    stats[0] = stats[1] = stats[2] = stats[3] = 0;
-    int suffix[EXACT_LIMIT + 1];
-    suffix[n] = 0;
-    for (int i = n - 1; i >= 0; --i) suffix[i] = suffix[i + 1] + caps[i];
-    const int kcap = kmax < EXACT_LIMIT ? kmax : EXACT_LIMIT;
-    for (int k = 0; k <= kcap; ++k) found[k] = 0;
-    int nfound = 0;
-    // level 0: root
-    SRec root;
-    root.hi = root.lo = 0; root.done = 0; root.m = 0; root.action = 0; root.aux = -1;
-    ws.states[0] = root;
-    level_start[0] = 0;
-    level_start[1] = 1;
-    int total_states = 1;
-    int levels = 0;
-    uint8_t res[EXACT_LIMIT + 1], child[EXACT_LIMIT + 1];
-    for (int i = 0; i < n; ++i) {
-        const int cap = caps[i];
-        const int f0 = level_start[i], f1 = level_start[i + 1];
-        int nk = 0;
-        stats[1] += f1 - f0;
-        for (int s = f0; s < f1; ++s) {
-            const SRec st = ws.states[s];
-            unpack(st, res);
-            const int m = st.m;
-            for (int slot = 0; slot <= m; ++slot) {
-                const bool start = slot == m;
-                if (!start && slot > 0 && res[slot] == res[slot - 1]) continue;
-                if (start && !(st.done + m < kmax)) continue;
-                int cm = 0;
-                int left;
-                if (start) {
-                    for (int p = 0; p < m; ++p) child[cm++] = res[p];
-                    left = L - cap;
-                } else {
-                    for (int p = 0; p < m; ++p) if (p != slot) child[cm++] = res[p];
-                    left = (int)res[slot] - cap;
-                }
-                SRec c;
-                c.done = st.done;
-                if (left <= 0) c.done = st.done + 1;
-                else insert_sorted(child, cm, (uint8_t)left);
-                pack(c, child, cm);
-                c.action = start ? 0xFF : (uint8_t)slot;
-                c.aux = (s - f0) * 32 + (start ? 31 : slot);   // producer order
-                if (nk >= ccap) { *need = nk + 1; return SS_WORKSPACE; }
-                ws.kids[nk++] = c;
-            }
-        }
-        // stable "first producer wins": sort by (key, producer order), keep first per key
-        for (int q = 0; q < nk; ++q) ws.idx[q] = q;
-        merge_sort_idx(ws.idx, ws.tmp, nk, [&](int a, int b) {
-            const SRec& x = ws.kids[a];
-            const SRec& y = ws.kids[b];
-            if (!key_eq(x, y)) return key_less(x, y);
-            return x.aux < y.aux;
-        });
-        // dedup + feasibility (in key order) -> idx[0..nu)
-        const int remaining = n - (i + 1);
-        int nu = 0;
-        for (int q = 0; q < nk; ++q) {
-            const SRec& c = ws.kids[ws.idx[q]];
-            if (nu > 0 && key_eq(ws.kids[ws.idx[nu - 1]], c)) continue;
-            ws.idx[nu++] = ws.idx[q];
-        }
-        int nf = 0;
-        for (int q = 0; q < nu; ++q) {
-            const SRec& c = ws.kids[ws.idx[q]];
-            unpack(c, child);
-            int sum = 0;
-            for (int p = 0; p < c.m; ++p) sum += child[p];
-            if (c.m > remaining || sum > suffix[i + 1]) continue;
-            ws.idx[nf++] = ws.idx[q];
-        }
-        // dominance inside (done, m) classes: sort a copy by class order
-        for (int q = 0; q < nf; ++q) ws.keep[q] = ws.idx[q];
-        merge_sort_idx(ws.keep, ws.tmp, nf, [&](int a, int b) { return class_less(ws.kids[a], ws.kids[b]); });
-        // mark kept: reuse SRec.pad as flag
-        for (int q = 0; q < nf; ++q) ws.kids[ws.keep[q]].pad = 0;
-        int cls_start = 0;
-        uint8_t cres[EXACT_LIMIT + 1], ores[EXACT_LIMIT + 1];
-        for (int q = 0; q < nf; ++q) {
-            const SRec& c = ws.kids[ws.keep[q]];
-            if (q > 0) {
-                const SRec& pr = ws.kids[ws.keep[q - 1]];
-                if (pr.done != c.done || pr.m != c.m) cls_start = q;
-            }
-            unpack(c, cres);
-            bool dominated = false;
-            for (int o = cls_start; o < q && !dominated; ++o) {
-                const SRec& other = ws.kids[ws.keep[o]];
-                if (!other.pad) continue;
-                unpack(other, ores);
-                bool all_le = true;
-                for (int p = 0; p < c.m; ++p) if (ores[p] > cres[p]) { all_le = false; break; }
-                dominated = all_le;
-            }
-            if (!dominated) ws.kids[ws.keep[q]].pad = 1;
-            else stats[3] += 1;
-        }
-        // compact kept states in key order into the next level
-        const int base = total_states;
-        int nn = 0;
-        for (int q = 0; q < nf; ++q) {
-            SRec c = ws.kids[ws.idx[q]];
-            if (!c.pad) continue;
-            if (base + nn >= fcap) { *need = base + nn + 1; return SS_WORKSPACE; }
-            c.aux = c.aux / 32;       // parent index within previous level
-            c.pad = 0;
-            ws.states[base + nn++] = c;
-        }
-        total_states = base + nn;
-        level_start[i + 2] = total_states;
-        levels = i + 1;
-        stats[0] = levels;
-        if (nn > stats[2]) stats[2] = nn;
-        for (int q = 0; q < nn; ++q) {
-            const SRec& c = ws.states[base + q];
-            if (c.m == 0 && c.done >= 1 && c.done <= kcap && found[c.done] == 0) {
-                found[c.done] = i + 1;
-                ++nfound;
-            }
-        }
-        if (nfound == kmax || nn == 0) break;
-    }
-    (void)levels;
-    return SS_OK;
 }
 
 // rebuild the k groups of the state ((), k) found at `level` (allocator.py:228-264)
@@ -687,11 +525,74 @@ __device__ bool sorted_nonincreasing(const int* caps, int n) {
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-__global__ void exact_sweep_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members,
-                                   int32_t* gsize, int32_t* pool_status, int32_t* pool_aux, unsigned char* ws_base,
-                                   int64_t ws_bytes_per, int fcap, int ccap, const int32_t* exact_list,
-                                   int n_exact, int32_t* sweep_stats) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+// ---------------------------------------------------------------------------
+// exact sweep, one CTA per pool (the level loop of allocator.py:138-225 with every step data-parallel):
+//   expand   thread per parent state (sorted key order) -> children in producer order (parent, then extend
+//            slots ascending, then start), positions by a block scan of the per-parent counts;
+//   sort     stable merge sort of the children by (residual key, done): each pass places every record by a
+//            binary search in the partner run, so equal keys keep producer order -> "first producer wins";
+//   filter   first of each key run that passes feasibility (open <= remaining, sum(res) <= suffix);
+//   prune    x is dropped iff some other state of its (done, open) class is pointwise <= x.  Sorted
+//            lexicographically a dominator precedes what it dominates and domination is transitive, so this
+//            order-free test equals the reference's forward pass over kept tuples (_prune_dominated 114-135);
+//   keep     survivors in key order become the next level (sorted(frontier.keys())).
+// The per-(pool, k) replay (228-264) stays one thread.
+// ---------------------------------------------------------------------------
+constexpr int SWEEP_NT = 256;
+
+__device__ __forceinline__ bool rec_key_less(const SRec& a, const SRec& b) { return key_less(a, b); }
+
+// exclusive scan of v[0..n) in place (global memory), returns the total; all threads of the CTA call it
+__device__ int block_scan_excl(int* v, int n, int* sh) {
+    const int tid = threadIdx.x;
+    const int per = (n + SWEEP_NT - 1) / SWEEP_NT;
+    const int a = tid * per, b = min(a + per, n);
+    int sum = 0;
+    for (int q = a; q < b; ++q) sum += v[q];
+    sh[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < SWEEP_NT; o <<= 1) {               // Hillis-Steele inclusive scan of the partials
+        const int x = tid >= o ? sh[tid - o] : 0;
+        __syncthreads();
+        sh[tid] += x;
+        __syncthreads();
+    }
+    int run = sh[tid] - sum;
+    const int total = sh[SWEEP_NT - 1];
+    for (int q = a; q < b; ++q) { const int x = v[q]; v[q] = run; run += x; }
+    __syncthreads();
+    return total;
+}
+
+// y <= x pointwise (same open count; residual bytes stored value+1, zero padded, big-endian in hi/lo)
+__device__ __forceinline__ bool pointwise_le(const SRec& y, const SRec& x) {
+    const unsigned long long yh = y.hi, yl = y.lo, xh = x.hi, xl = x.lo;
+    return __vcmpgeu4((unsigned)xh, (unsigned)yh) == 0xFFFFFFFFu &&
+           __vcmpgeu4((unsigned)(xh >> 32), (unsigned)(yh >> 32)) == 0xFFFFFFFFu &&
+           __vcmpgeu4((unsigned)xl, (unsigned)yl) == 0xFFFFFFFFu &&
+           __vcmpgeu4((unsigned)(xl >> 32), (unsigned)(yl >> 32)) == 0xFFFFFFFFu;
+}
+
+struct CtaSweepWs {
+    SRec* states;     // kept states, level after level
+    SRec* a;          // children / sort ping
+    SRec* b;          // sort pong / filtered list
+    int32_t* i0;      // counts, flags, scan
+    int32_t* i1;      // class buckets
+};
+
+__global__ void __launch_bounds__(SWEEP_NT) exact_sweep_cta_kernel(ss_pool_set P, const int64_t* koff,
+        int32_t* stages, int32_t* members, int32_t* gsize, int32_t* pool_status, int32_t* pool_aux,
+        unsigned char* ws_base, int64_t ws_bytes_per, int fcap, int ccap, const int32_t* exact_list, int n_exact,
+        int32_t* sweep_stats) {
+    __shared__ int sh[SWEEP_NT];
+    __shared__ int level_start[EXACT_LIMIT + 2];
+    __shared__ int found[EXACT_LIMIT + 1];
+    __shared__ int suffix[EXACT_LIMIT + 1];
+    __shared__ int caps_s[EXACT_LIMIT];
+    __shared__ int cls_cnt[(EXACT_LIMIT + 1) * (EXACT_LIMIT + 1)], cls_off[(EXACT_LIMIT + 1) * (EXACT_LIMIT + 1)];
+    __shared__ int s_nfound, s_stop, s_status, s_need, s_stats[4];
+    const int e = blockIdx.x, tid = threadIdx.x;
     if (e >= n_exact) return;
     const int p = exact_list[e];
     if (pool_status[p] != SS_OK) return;
@@ -699,29 +600,185 @@ __global__ void exact_sweep_kernel(ss_pool_set P, const int64_t* koff, int32_t* 
     const int* caps = P.caps + off;
     const int L = P.layers[p], kmax = P.kmax[p];
     const int n = usable_count(caps, n_all);
+    const int kcap = kmax < EXACT_LIMIT ? kmax : EXACT_LIMIT;
     unsigned char* w = ws_base + (int64_t)e * ws_bytes_per;
-    SweepWs ws;
-    ws.states = reinterpret_cast<SRec*>(w);
-    w += (int64_t)fcap * sizeof(SRec);
-    ws.kids = reinterpret_cast<SRec*>(w);
-    w += (int64_t)ccap * sizeof(SRec);
-    ws.idx = reinterpret_cast<int32_t*>(w);
-    w += (int64_t)ccap * 4;
-    ws.tmp = reinterpret_cast<int32_t*>(w);
-    w += (int64_t)ccap * 4;
-    ws.keep = reinterpret_cast<int32_t*>(w);
-    int level_start[EXACT_LIMIT + 2];
-    int found[EXACT_LIMIT + 1];
-    int need = 0;
-    int stats[4];
-    const int st = exact_sweep(caps, n, L, kmax, ws, fcap, ccap, level_start, found, &need, stats);
-    if (sweep_stats) for (int q = 0; q < 4; ++q) sweep_stats[4 * e + q] = stats[q];
-    if (st != SS_OK) { pool_status[p] = st; pool_aux[p] = need; return; }
+    CtaSweepWs ws;
+    ws.states = reinterpret_cast<SRec*>(w);  w += (int64_t)fcap * sizeof(SRec);
+    ws.a = reinterpret_cast<SRec*>(w);       w += (int64_t)ccap * sizeof(SRec);
+    ws.b = reinterpret_cast<SRec*>(w);       w += (int64_t)ccap * sizeof(SRec);
+    ws.i0 = reinterpret_cast<int32_t*>(w);   w += (int64_t)ccap * 4;
+    ws.i1 = reinterpret_cast<int32_t*>(w);
+    if (tid == 0) {
+        suffix[n] = 0;
+        for (int i = n - 1; i >= 0; --i) suffix[i] = suffix[i + 1] + caps[i];
+        for (int i = 0; i < n; ++i) caps_s[i] = caps[i];
+        for (int k = 0; k <= EXACT_LIMIT; ++k) found[k] = 0;
+        SRec root;
+        root.hi = root.lo = 0; root.done = 0; root.m = 0; root.action = 0; root.pad = 0; root.aux = -1;
+        ws.states[0] = root;
+        level_start[0] = 0;
+        level_start[1] = 1;
+        s_nfound = 0; s_stop = 0; s_status = SS_OK; s_need = 0;
+        s_stats[0] = s_stats[1] = s_stats[2] = s_stats[3] = 0;
+    }
+    __syncthreads();
+    for (int i = 0; i < n; ++i) {
+        const int cap = caps_s[i];
+        const int f0 = level_start[i], f1 = level_start[i + 1], np = f1 - f0;
+        // ---- expand: counts, scan, children in producer order -> a[] ----------
+        if (np > ccap) { if (tid == 0) { s_status = SS_WORKSPACE; s_need = np + 1; } break; }
+        for (int q = tid; q < np; q += SWEEP_NT) {
+            const SRec st = ws.states[f0 + q];
+            uint8_t res[EXACT_LIMIT + 1];
+            unpack(st, res);
+            int cnt = 0;
+            for (int slot = 0; slot < st.m; ++slot) cnt += !(slot > 0 && res[slot] == res[slot - 1]);
+            cnt += st.done + st.m < kmax;
+            ws.i0[q] = cnt;
+        }
+        __syncthreads();
+        const int nk = block_scan_excl(ws.i0, np, sh);
+        if (nk > ccap) { if (tid == 0) { s_status = SS_WORKSPACE; s_need = nk + 1; } break; }
+        for (int q = tid; q < np; q += SWEEP_NT) {
+            const SRec st = ws.states[f0 + q];
+            uint8_t res[EXACT_LIMIT + 1], child[EXACT_LIMIT + 1];
+            unpack(st, res);
+            const int m = st.m;
+            int o = ws.i0[q];
+            for (int slot = 0; slot <= m; ++slot) {
+                const bool start = slot == m;
+                if (!start && slot > 0 && res[slot] == res[slot - 1]) continue;
+                if (start && !(st.done + m < kmax)) continue;
+                int cm = 0, left;
+                if (start) {
+                    for (int t = 0; t < m; ++t) child[cm++] = res[t];
+                    left = L - cap;
+                } else {
+                    for (int t = 0; t < m; ++t) if (t != slot) child[cm++] = res[t];
+                    left = (int)res[slot] - cap;
+                }
+                SRec c;
+                c.done = st.done;
+                if (left <= 0) c.done = st.done + 1;
+                else insert_sorted(child, cm, (uint8_t)left);
+                pack(c, child, cm);
+                c.action = start ? 0xFF : (uint8_t)slot;
+                c.pad = 0;
+                c.aux = q;                                   // parent index within the level
+                ws.a[o++] = c;
+            }
+        }
+        __syncthreads();
+        // ---- stable merge sort of a[0..nk) by (key, done) ------------------------
+        SRec* src = ws.a;
+        SRec* dst = ws.b;
+        for (int wd = 1; wd < nk; wd <<= 1) {
+            for (int q = tid; q < nk; q += SWEEP_NT) {
+                const int lo = q / (2 * wd) * (2 * wd), mid = min(lo + wd, nk), hi = min(lo + 2 * wd, nk);
+                const SRec x = src[q];
+                int pos;
+                if (q < mid) {                               // A element: count B elements strictly less
+                    int l = mid, r = hi;
+                    while (l < r) { const int mm = (l + r) >> 1; if (rec_key_less(src[mm], x)) l = mm + 1; else r = mm; }
+                    pos = lo + (q - lo) + (l - mid);
+                } else {                                     // B element: count A elements less or equal
+                    int l = lo, r = mid;
+                    while (l < r) { const int mm = (l + r) >> 1; if (!rec_key_less(x, src[mm])) l = mm + 1; else r = mm; }
+                    pos = lo + (q - mid) + (l - lo);
+                }
+                dst[pos] = x;
+            }
+            __syncthreads();
+            SRec* t = src; src = dst; dst = t;
+        }
+        // ---- first of each key run + feasibility -> flags, scan, compact into dst --
+        const int remaining = n - (i + 1);
+        for (int q = tid; q < nk; q += SWEEP_NT) {
+            const SRec c = src[q];
+            bool keep = q == 0 || !key_eq(src[q - 1], c);
+            if (keep) {
+                uint8_t r[EXACT_LIMIT + 1];
+                unpack(c, r);
+                int sum = 0;
+                for (int t = 0; t < c.m; ++t) sum += r[t];
+                keep = !(c.m > remaining || sum > suffix[i + 1]);
+            }
+            ws.i0[q] = keep;
+        }
+        __syncthreads();
+        const int nf = block_scan_excl(ws.i0, nk, sh);
+        for (int q = tid; q < nk; q += SWEEP_NT) {
+            const int pos = ws.i0[q];
+            const bool keep = (q + 1 < nk ? ws.i0[q + 1] : nf) != pos;
+            if (keep) dst[pos] = src[q];
+        }
+        __syncthreads();
+        SRec* cand = dst;                                    // nf feasible unique children in key order
+        // ---- dominance inside (done, open) classes: bucket, then test each against its bucket --------
+        const int ncls = (EXACT_LIMIT + 1) * (EXACT_LIMIT + 1);
+        for (int q = tid; q < ncls; q += SWEEP_NT) cls_cnt[q] = 0;
+        __syncthreads();
+        for (int q = tid; q < nf; q += SWEEP_NT) atomicAdd(&cls_cnt[cand[q].done * (EXACT_LIMIT + 1) + cand[q].m], 1);
+        __syncthreads();
+        if (tid == 0) {
+            int run = 0;
+            for (int q = 0; q < ncls; ++q) { cls_off[q] = run; run += cls_cnt[q]; cls_cnt[q] = cls_off[q]; }
+        }
+        __syncthreads();
+        for (int q = tid; q < nf; q += SWEEP_NT) {
+            const int cl = cand[q].done * (EXACT_LIMIT + 1) + cand[q].m;
+            ws.i1[atomicAdd(&cls_cnt[cl], 1)] = q;
+        }
+        __syncthreads();
+        for (int q = tid; q < nf; q += SWEEP_NT) {
+            const SRec x = cand[q];
+            const int cl = x.done * (EXACT_LIMIT + 1) + x.m;
+            const int b0 = cls_off[cl], b1 = cls_cnt[cl];    // after the scatter, cls_cnt = bucket end
+            bool dominated = false;
+            for (int t = b0; t < b1 && !dominated; ++t) {
+                const int yq = ws.i1[t];
+                if (yq == q) continue;
+                dominated = pointwise_le(cand[yq], x);
+            }
+            ws.i0[q] = !dominated;
+        }
+        __syncthreads();
+        const int nn = block_scan_excl(ws.i0, nf, sh);
+        const int base = level_start[i + 1];
+        if (base + nn > fcap) { if (tid == 0) { s_status = SS_WORKSPACE; s_need = base + nn + 1; } break; }
+        for (int q = tid; q < nf; q += SWEEP_NT) {
+            const int pos = ws.i0[q];
+            const bool keep = (q + 1 < nf ? ws.i0[q + 1] : nn) != pos;
+            if (keep) {
+                const SRec c = cand[q];
+                ws.states[base + pos] = c;
+                if (c.m == 0 && c.done >= 1 && c.done <= kcap && atomicCAS(&found[c.done], 0, i + 1) == 0)
+                    atomicAdd(&s_nfound, 1);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            level_start[i + 2] = base + nn;
+            s_stats[0] = i + 1;
+            s_stats[1] += np;
+            if (nn > s_stats[2]) s_stats[2] = nn;
+            s_stats[3] += nf - nn;
+            s_stop = s_nfound == kmax || nn == 0;
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    if (sweep_stats) for (int q = 0; q < 4; ++q) sweep_stats[4 * e + q] = s_stats[q];
+    if (s_status != SS_OK) { pool_status[p] = s_status; pool_aux[p] = s_need; return; }
+    int ls[EXACT_LIMIT + 2];
+    for (int q = 0; q < EXACT_LIMIT + 2; ++q) ls[q] = level_start[q];
     for (int k = 1; k <= kmax; ++k) {
         const int64_t ko = koff[p] + k - 1;
         if (k > EXACT_LIMIT || found[k] == 0) { stages[ko] = 0; continue; }
         stages[ko] = found[k];
-        sweep_replay(caps, L, ws.states, level_start, k, found[k], members + P.memb_off[p] + (int64_t)(k - 1) * n_all,
+        sweep_replay(caps, L, ws.states, ls, k, found[k], members + P.memb_off[p] + (int64_t)(k - 1) * n_all,
                      gsize + P.gsz_off[p] + (int64_t)(k - 1) * kmax);
     }
 }
@@ -1128,7 +1185,7 @@ inline int grid_for(int n, int b) { return (n + b - 1) / b; }
 // ---------------------------------------------------------------------------
 extern "C" int64_t ss_stage_counts_workspace(int32_t frontier_cap, int32_t children_cap, int32_t max_levels) {
     (void)max_levels;
-    return (int64_t)frontier_cap * sizeof(SRec) + (int64_t)children_cap * (sizeof(SRec) + 12) + 256;
+    return (int64_t)frontier_cap * sizeof(SRec) + (int64_t)children_cap * (2 * sizeof(SRec) + 8) + 256;
 }
 
 extern "C" int ss_stage_counts_validate(const ss_pool_set* pools, const int64_t* koff, int32_t* stages,
@@ -1145,7 +1202,7 @@ extern "C" int ss_stage_counts_exact(const ss_pool_set* pools, const int64_t* ko
                                      int32_t n_exact, void* workspace, int64_t ws_bytes_per, int32_t frontier_cap,
                                      int32_t children_cap, int32_t* sweep_stats, void* stream) {
     if (n_exact <= 0) return SS_OK;
-    exact_sweep_kernel<<<grid_for(n_exact, 32), 32, 0, ss_stream(stream)>>>(
+    exact_sweep_cta_kernel<<<n_exact, SWEEP_NT, 0, ss_stream(stream)>>>(
         *pools, koff, stages, members, gsize, pool_status, pool_aux, static_cast<unsigned char*>(workspace),
         ws_bytes_per, frontier_cap, children_cap, exact_list, n_exact, sweep_stats);
     SS_CHECK_LAUNCH();

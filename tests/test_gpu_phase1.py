@@ -191,3 +191,18 @@ def test_variant_sweep_vs_oracle(cuda_ready):
                     pos += len(grp)
     bv = int(sw.best_variant.cpu()[0])
     assert bv == int(np.argmax(totals)) and float(sw.best_total.cpu()[0]) == totals.max()
+
+
+def test_sweep_stats_and_s_star_vs_reference(cuda_ready):
+    """exact_sweep_cta_kernel counters (SweepStats, allocator.py:87-94) and s*(k) vs the reference's own sweep on
+    280 exact-path pools, including N=16 / L=80 shapes with ~2k expanded states (tests/golden/sweep_stats_cases.json)."""
+    import json
+    import os
+    from paper_2509_26182_b200 import SweepStats, solve_stage_counts
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sweep_stats_cases.json")) as fh:
+        cases = json.load(fh)
+    for c in cases:
+        st = SweepStats()
+        sols = solve_stage_counts(c["caps"], c["L"], c["kmax"], stats=st)
+        assert [st.levels, st.states_expanded, st.peak_frontier, st.pruned_dominated] == c["stats"], c
+        assert {str(k): v.stages for k, v in sols.items()} == c["s_star"], c
