@@ -37,32 +37,62 @@ def _torch():
     return torch
 
 
+@dataclass
+class PoolArrays:
+    """Many pools as flat arrays (the vectorised alternative to a list of PoolSpec)."""
+    n: np.ndarray                # GPUs per pool
+    caps: np.ndarray             # concatenated, each pool sorted non-increasing
+    flops: np.ndarray            # same order
+    layers: np.ndarray           # per pool
+    kmax: np.ndarray             # per pool
+
+    @staticmethod
+    def from_specs(pools: List[PoolSpec]) -> "PoolArrays":
+        P = len(pools)
+        return PoolArrays(np.array([len(p.caps) for p in pools], dtype=np.int64),
+                          np.concatenate([np.asarray(p.caps, dtype=np.int64) for p in pools]) if P else np.zeros(0, np.int64),
+                          np.concatenate([np.asarray(p.flops, dtype=np.float64) for p in pools]) if P else np.zeros(0),
+                          np.array([p.layers for p in pools], dtype=np.int64),
+                          np.array([max(int(p.kmax), 0) for p in pools], dtype=np.int64))
+
+
+def _ramp(counts: np.ndarray) -> np.ndarray:
+    """1..c for every count c, concatenated."""
+    total = int(counts.sum())
+    if total == 0:
+        return np.zeros(0, dtype=np.int64)
+    starts = np.repeat(np.cumsum(counts) - counts, counts)
+    return np.arange(total, dtype=np.int64) - starts + 1
+
+
 class PoolBatch:
-    def __init__(self, pools: List[PoolSpec], *, stream=None):
+    def __init__(self, pools=None, *, arrays: Optional[PoolArrays] = None, stream=None):
         torch = _torch()
-        self.pools = pools
+        A = arrays if arrays is not None else PoolArrays.from_specs(pools)
         self.stream = stream
         dev = torch.device("cuda")
         self.dev = dev
-        P = len(pools)
-        n = np.array([len(p.caps) for p in pools], dtype=np.int64)
-        km = np.array([max(int(p.kmax), 0) for p in pools], dtype=np.int64)
+        P = int(A.n.size)
+        self.P = P
+        n = A.n.astype(np.int64)
+        km = np.maximum(A.kmax.astype(np.int64), 0)
         self.n, self.km = n, km
         pool_ptr = np.concatenate([[0], np.cumsum(n)])
         koff = np.concatenate([[0], np.cumsum(km)])
         memb = np.concatenate([[0], np.cumsum(km * n)])
         gsz = np.concatenate([[0], np.cumsum(km * km)])
         self.koff_h, self.memb_h, self.gsz_h, self.pool_ptr_h = koff, memb, gsz, pool_ptr
-        caps = np.concatenate([np.asarray(p.caps, dtype=np.int64) for p in pools]) if P else np.zeros(0)
-        flops = np.concatenate([np.asarray(p.flops, dtype=np.float64) for p in pools]) if P else np.zeros(0)
-        usable = np.array([int(np.sum(np.asarray(p.caps) > 0)) for p in pools], dtype=np.int64)
+        caps = A.caps.astype(np.int64)
+        flops = A.flops.astype(np.float64)
+        cpos = np.concatenate([[0], np.cumsum(caps > 0)])
+        usable = cpos[pool_ptr[1:]] - cpos[pool_ptr[:-1]]
         self.usable = usable
         exact = np.nonzero((usable <= EXACT_LIMIT) & (usable > 0) & (km > 0))[0]
         cover_p = np.nonzero(usable > EXACT_LIMIT)[0]
-        cand_pool = np.repeat(cover_p, km[cover_p]) if cover_p.size else np.zeros(0, dtype=np.int64)
-        cand_k = np.concatenate([np.arange(1, km[p] + 1) for p in cover_p]) if cover_p.size else np.zeros(0)
+        cand_pool = np.repeat(cover_p, km[cover_p])
+        cand_k = _ramp(km[cover_p])
         all_pool = np.repeat(np.arange(P), km)
-        all_k = np.concatenate([np.arange(1, k + 1) for k in km]) if km.sum() else np.zeros(0)
+        all_k = _ramp(km)
         # one thread per candidate: order by (k, pool) so a warp's 32 candidates share k (and hence loop
         # trip counts) -- outputs are addressed by (pool, k), so the order is free
         o = np.lexsort((cand_pool, cand_k))
@@ -72,7 +102,7 @@ class PoolBatch:
         self.exact = exact
         self.n_cover = int(cand_pool.size)
         self.n_cand = int(all_pool.size)
-        ints = np.concatenate([pool_ptr, caps, [p.layers for p in pools], km, exact, cand_pool, cand_k, all_pool,
+        ints = np.concatenate([pool_ptr, caps, A.layers, km, exact, cand_pool, cand_k, all_pool,
                                all_k]).astype(np.int32)
         self._ints = torch.from_numpy(ints).to(dev)
         o = 0
@@ -111,7 +141,7 @@ class PoolBatch:
         self.fcap, self.ccap = 4096, 65536
 
     def pool_set(self) -> N.PoolSet:
-        return N.PoolSet(len(self.pools), N.ptr(self.pool_ptr), N.ptr(self.caps), N.ptr(self.flops),
+        return N.PoolSet(self.P, N.ptr(self.pool_ptr), N.ptr(self.caps), N.ptr(self.flops),
                          N.ptr(self.layers), N.ptr(self.kmax), N.ptr(self.memb_off), N.ptr(self.gsz_off))
 
     # -- stage counts ------------------------------------------------------

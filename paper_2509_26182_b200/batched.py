@@ -354,7 +354,8 @@ class ScenarioReplayer:
         info has per-scenario "decision", "rebalanced", "degraded", "changed" (GPU indices), "aborted".
         """
         import dataclasses
-        from ._phase1 import PoolBatch, PoolSpec
+        from ._phase1 import PoolArrays, PoolBatch, _ramp
+        from .errors import SS_OK as SS_OK_STATUS
         torch = self.torch
         sc = self.scen
         S, G, L = self.S, self.G, self.L
@@ -375,44 +376,70 @@ class ScenarioReplayer:
         if sc.slice_order_s is not None:
             order = sc.slice_order_s.copy()
         else:
+            po = np.asarray(sc.plan_order, dtype=np.int64)
+            jn = joined.astype(np.int64)
+            jv = np.where(jn >= 0, jn, 0)
+            rows = np.arange(S)[:, None]
+            cand = np.concatenate([np.broadcast_to(po, (S, po.size)), jn], axis=1)
+            keep = np.concatenate([~absent[:, po], (jn >= 0) & (lo[rows, jv] <= hi[rows, jv])], axis=1)
+            first = np.argsort(~keep, axis=1, kind="stable")          # kept entries first, in list order
             order = np.full((S, G), -1, dtype=np.int32)
-            for s in range(S):
-                cur = [g for g in sc.plan_order if not absent[s, g]] + [g for g in joined[s] if g >= 0
-                                                                        and lo[s, g] <= hi[s, g]]
-                order[s, :len(cur)] = cur
-        pools, items, item_seed, owners = [], [], [], []
-        for s in sel:
-            present = ~absent[s]
-            for r in range(len(sc.region_names)):
-                idx = np.nonzero(present & (sc.region_idx == r))[0]        # cluster_snapshot(): id order
-                if idx.size == 0:
-                    continue
-                caps = sc.layer_cap[idx].astype(np.int64)
-                limit = min(int(idx.size), int(caps.sum()) // L)
-                if limit < 1:
-                    continue
-                o = np.lexsort((idx, -caps))                                # (-capacity, id) (allocator.py:570)
-                pools.append(PoolSpec(caps[o].tolist(), sc.flops[idx][o].tolist(), L, limit))
-                items.append(idx)
-                item_seed.append(int(sc.seeds[s]))
-                owners.append((int(s), idx[o]))
+            packed_o = np.take_along_axis(cand, first, axis=1)[:, :G]
+            cnt = keep.sum(axis=1)
+            order[:, :packed_o.shape[1]] = np.where(np.arange(packed_o.shape[1])[None, :] < cnt[:, None], packed_o, -1)
+        # the churned pools, vectorised over scenarios: region by region (sorted names), the present GPUs of each
+        # selected scenario in (-capacity, id) order (allocator.py:570); id order for the objective items
+        sel = np.asarray(sel, dtype=np.int64)
+        pres = ~absent[sel]
+        P_n, P_caps, P_flops, P_km, P_scen, P_owner, I_gpu = [], [], [], [], [], [], []
+        for r in range(len(sc.region_names)):
+            gr = np.nonzero(sc.region_idx == r)[0]
+            if gr.size == 0 or sel.size == 0:
+                continue
+            capr = sc.layer_cap[gr].astype(np.int64)
+            o_r = np.lexsort((gr, -capr))
+            pr_id = pres[:, gr]
+            cnt = pr_id.sum(axis=1)
+            limit = np.minimum(cnt, (pr_id * capr).sum(axis=1) // L)
+            ok = (cnt > 0) & (limit >= 1)
+            rows = np.nonzero(ok)[0]
+            if rows.size == 0:
+                continue
+            pr_o = pr_id[rows][:, o_r]
+            P_n.append(cnt[rows])
+            P_km.append(limit[rows])
+            P_scen.append(sel[rows])
+            P_caps.append(np.broadcast_to(capr[o_r], pr_o.shape)[pr_o])
+            P_flops.append(np.broadcast_to(sc.flops[gr][o_r], pr_o.shape)[pr_o])
+            P_owner.append(np.broadcast_to(gr[o_r], pr_o.shape)[pr_o])
+            I_gpu.append(np.broadcast_to(gr, (rows.size, gr.size))[pr_id[rows]])
         info = {"decision": dec, "rebalanced": np.zeros(S, dtype=bool), "degraded": np.zeros(S, dtype=bool),
                 "changed": [[] for _ in range(S)], "aborted": np.zeros(S, dtype=np.int32)}
         new_lo, new_hi = lo.copy(), hi.copy()
-        if pools:
-            batch = PoolBatch(pools, stream=self.stream)
+        if P_n:
+            # pools in (scenario, region) order, as the per-scenario allocate() calls would see them
+            cat = lambda xs: np.concatenate(xs)
+            pn, pkm, pscen = cat(P_n), cat(P_km), cat(P_scen)
+            ptr0 = np.concatenate([[0], np.cumsum(pn)])
+            perm = np.argsort(pscen, kind="stable")
+            pn, pkm, pscen = pn[perm], pkm[perm], pscen[perm]
+            gath = np.repeat(ptr0[perm], pn) + _ramp(pn) - 1                # pool-major gather in the new order
+            caps_f, flops_f, owner_f = cat(P_caps)[gath], cat(P_flops)[gath], cat(P_owner)[gath]
+            igpu_f = cat(I_gpu)[gath]                       # objective items: id order, same pool sizes
+            n_it = int(pn.size)
+            batch = PoolBatch(arrays=PoolArrays(pn, caps_f, flops_f, np.full(n_it, L, dtype=np.int64), pkm),
+                              stream=self.stream)
             batch.stage_counts()
             # estimate_objective_params per churned region, gathered from the pool on device (no dense copies)
-            n_it = len(items)
-            iptr = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int32)
+            iptr = np.concatenate([[0], np.cumsum(pn)]).astype(np.int32)
             up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=self.dev, dtype=dt)
             if not hasattr(self, "_pool_flops"):
                 self._pool_flops = up(sc.flops, torch.float64)
             t = torch.empty(n_it, dtype=torch.float64, device=self.dev)
             r = torch.empty(n_it, dtype=torch.float64, device=self.dev)
-            ip_d, g_d = up(iptr, torch.int32), up(np.concatenate(items), torch.int32)
+            ip_d, g_d = up(iptr, torch.int32), up(igpu_f, torch.int32)
             lay_d = torch.full((n_it,), L, dtype=torch.int32, device=self.dev)
-            seed_d = up(np.array(item_seed, dtype=np.int64), torch.int64) if sc.jitter else None
+            seed_d = up(sc.seeds[pscen].astype(np.int64), torch.int64) if sc.jitter else None
             N.check(N.lib().ss_objective_pool(n_it, N.ptr(ip_d), N.ptr(g_d), N.ptr(self._pool_flops),
                                               N.ptr(self.base_rtt), G, N.ptr(seed_d) if seed_d is not None else None,
                                               float(sc.fpl), N.ptr(lay_d), float(tokens), N.ptr(t), N.ptr(r),
@@ -420,36 +447,39 @@ class ScenarioReplayer:
             km = int(batch.km.max())
             batch.score_and_best(t, r, np.array([0.0] + [float(k ** alpha) for k in range(1, km + 1)]))
             res = batch.fetch()
-            by_s = {}
-            for p, (s, og) in enumerate(owners):
-                by_s.setdefault(s, []).append((p, og))
-            for s in sel:
-                s = int(s)
-                gs, starts, ends = [], [], []
-                for p, og in by_s.get(s, []):
-                    res.raise_pool(p)
-                    bg = res.best_groups(p)
-                    if bg is None:
-                        continue
-                    members, sizes, counts = bg
-                    # contiguous slices from layer 1 inside every group (allocator.py:595-606)
-                    ends_all = np.cumsum(counts)
-                    grp_start = np.repeat(np.concatenate([[0], np.cumsum(sizes)[:-1]]), sizes)
-                    before = np.concatenate([[0], ends_all])[grp_start]
-                    e = ends_all - before
-                    gs.append(og[members])
-                    starts.append(e - counts + 1)
-                    ends.append(e)
-                if not gs:                                           # NoFeasiblePipeline: keep the slices
-                    info["degraded"][s] = True
-                    continue
-                g_all = np.concatenate(gs)
-                new_lo[s], new_hi[s] = 0, -1
-                new_lo[s, g_all] = np.concatenate(starts)
-                new_hi[s, g_all] = np.concatenate(ends)
-                order[s] = -1
-                order[s, :g_all.size] = g_all
-                info["rebalanced"][s] = True
+            bad = np.nonzero(res.status != SS_OK_STATUS)[0]
+            if bad.size:
+                res.raise_pool(int(bad[0]))
+            # best-k groups of every pool, flattened: member -> (pool, group, layer count)
+            bk = res.best_k.astype(np.int64)
+            kidx = batch.koff_h[:-1] + np.maximum(bk, 1) - 1
+            total = np.where(bk >= 1, res.stages[kidx], 0).astype(np.int64)
+            mbase = batch.memb_h[:-1] + (np.maximum(bk, 1) - 1) * pn
+            midx = np.repeat(mbase, total) + _ramp(total) - 1
+            members, counts = res.members[midx].astype(np.int64), res.counts[midx].astype(np.int64)
+            kk = np.where(total > 0, bk, 0)
+            gidx = np.repeat(batch.gsz_h[:-1] + (np.maximum(bk, 1) - 1) * pkm, kk) + _ramp(kk) - 1
+            sizes = res.gsize[gidx].astype(np.int64)
+            # contiguous slices from layer 1 inside every group (allocator.py:595-606)
+            ends_all = np.cumsum(counts)
+            gstart = np.repeat(np.cumsum(sizes) - sizes, sizes)            # first member of each member's group
+            before = np.concatenate([[0], ends_all])[gstart]
+            e = ends_all - before
+            mpool = np.repeat(np.arange(n_it), total)
+            g_all = owner_f[np.repeat(np.concatenate([[0], np.cumsum(pn)])[:-1], total) + members]
+            m_scen = pscen[mpool]
+            ok_s = np.zeros(S, dtype=bool)
+            ok_s[m_scen] = True
+            for s_ in sel[~ok_s[sel]]:                                   # NoFeasiblePipeline: keep the slices
+                info["degraded"][int(s_)] = True
+            done_s = np.nonzero(ok_s)[0]
+            new_lo[done_s], new_hi[done_s] = 0, -1
+            new_lo[m_scen, g_all] = e - counts + 1
+            new_hi[m_scen, g_all] = e
+            order[done_s] = -1
+            rank = np.arange(m_scen.size) - np.searchsorted(m_scen, m_scen, side="left")
+            order[m_scen, rank] = g_all
+            info["rebalanced"][done_s] = True
         key0 = np.where(lo <= hi, lo.astype(np.int64) * 100000 + hi, -1)
         key1 = np.where(new_lo <= new_hi, new_lo.astype(np.int64) * 100000 + new_hi, -1)
         changed = key0 != key1
