@@ -128,16 +128,16 @@ def min_stages(capacities: Sequence[int], layer_count: int, k: int) -> Optional[
 
 def _region_items(cluster: ClusterSnapshot, regions_gpus: List[Sequence[GpuNode]]):
     """(flops, links) per region in cluster order; links resolved direct>reverse on device."""
-    items = []
-    for rg in regions_gpus:
-        pos = {g.id: i for i, g in enumerate(rg)}
-        links = []
-        for (a, b), v in cluster.links.items():
-            ia, ib = pos.get(a), pos.get(b)
-            if ia is not None and ib is not None and ia != ib:
-                links.append((ia, ib, float(v)))
-        items.append(([g.flops for g in rg], links))
-    return items
+    where = {}                                   # gpu id -> (region item, position); one pass over the links
+    for ri, rg in enumerate(regions_gpus):
+        for i, g in enumerate(rg):
+            where[g.id] = (ri, i)
+    links = [[] for _ in regions_gpus]
+    for (a, b), v in cluster.links.items():
+        wa, wb = where.get(a), where.get(b)
+        if wa is not None and wb is not None and wa[0] == wb[0] and wa[1] != wb[1]:
+            links[wa[0]].append((wa[1], wb[1], float(v)))
+    return [([g.flops for g in rg], lk) for rg, lk in zip(regions_gpus, links)]
 
 
 def estimate_objective_params(region_gpus: Sequence[GpuNode], cluster: ClusterSnapshot, model: ModelSpec,
