@@ -367,6 +367,10 @@ int ss_set_slot_staging(int32_t stage_bytes, int32_t n_buffers);
 
 /* Kernel tuning knobs (0 = default); returns previous values via *_h. */
 int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
+/* Constructive stage counts: batches of at most max_candidates (pool, k) candidates try every group count in
+ * parallel (cover_try_kernel), larger ones keep the serial m loop (cover_kernel); both give the same result.
+ * < 0 leaves the limit unchanged; returns the previous limit (default 2048). */
+int32_t ss_set_cover_parallel_limit(int32_t max_candidates);
 
 #ifdef __cplusplus
 }

@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(SWEEP_NT) exact_sweep_cta_kernel(ss_pool_set P
 }
 
 constexpr int COVER_UNSET = 0x7f7f7f7f;
+int g_cover_parallel_limit = 2048;      // candidates up to which the group counts are searched in parallel
 
 // Constructive path of one (pool, k) candidate (allocator.py:426-470): m runs from m0 upward and the first m
 // whose best-fit or (failing that) peel succeeds gives the groups.  Split into setup / one attempt so the m
@@ -1218,7 +1219,8 @@ extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* ko
     // succeeded (peel polls best_m), and the smallest success is the reference's first-success m.  A large sweep
     // keeps the work-efficient serial m loop of cover_kernel.
     int32_t* best_m = nullptr;
-    if (n_cand > 0 && n_cand <= 2048 && cudaMallocAsync(&best_m, sizeof(int32_t) * n_cand, s) == cudaSuccess) {
+    if (n_cand > 0 && n_cand <= g_cover_parallel_limit &&
+        cudaMallocAsync(&best_m, sizeof(int32_t) * n_cand, s) == cudaSuccess) {
         cudaMemsetAsync(best_m, 0x7f, sizeof(int32_t) * n_cand, s);          // COVER_UNSET
         int m_off = 0;
         for (int span : {NMAX}) {                                             // m0 .. m0 + NMAX - 1 >= n
@@ -1329,4 +1331,10 @@ extern "C" int ss_score(int32_t n, const int32_t* k, const int32_t* s_star, cons
     score_kernel<<<grid_for(n, 128), 128, 0, ss_stream(stream)>>>(n, k, s_star, kpow, t_comp, rtt, z, status);
     SS_CHECK_LAUNCH();
     return SS_OK;
+}
+
+extern "C" int32_t ss_set_cover_parallel_limit(int32_t max_candidates) {
+    const int32_t old = g_cover_parallel_limit;
+    if (max_candidates >= 0) g_cover_parallel_limit = max_candidates;
+    return old;
 }

@@ -206,3 +206,36 @@ def test_sweep_stats_and_s_star_vs_reference(cuda_ready):
         sols = solve_stage_counts(c["caps"], c["L"], c["kmax"], stats=st)
         assert [st.levels, st.states_expanded, st.peak_frontier, st.pruned_dominated] == c["stats"], c
         assert {str(k): v.stages for k, v in sols.items()} == c["s_star"], c
+
+
+@pytest.mark.parametrize("L", [64, 80])
+def test_cover_serial_and_parallel_m_paths_agree(cuda_ready, L):
+    """ss_stage_counts_cover has two schedules -- the serial group-count loop (large batches) and the parallel
+    group-count search with cancellation (small batches).  Forced through each on the same C3-shaped pools, the
+    stage totals, groups, water-fill counts and scores must be identical, and the serial run must match the
+    oracle (the parallel one is what allocate() and the golden tests exercise)."""
+    from paper_2509_26182_b200 import _native as N
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import VariantSweep
+    lib = N.lib()
+    packed, _ = scen.bench_variants(8, 256, L, seed0=70)
+    out = []
+    old = lib.ss_set_cover_parallel_limit(-1)
+    try:
+        for limit in (0, 1 << 30):
+            lib.ss_set_cover_parallel_limit(limit)
+            sw = VariantSweep(packed, fill_all=True)
+            sw.run()
+            res = sw.batch.fetch()
+            out.append((res.stages.copy(), res.members.copy(), res.gsize.copy(), res.counts.copy(), res.z.copy(),
+                        sw.total.cpu().numpy().copy()))
+    finally:
+        lib.ss_set_cover_parallel_limit(old)
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+    stages, koff = out[0][0], sw.batch.koff_h
+    for p in range(0, len(packed.pools), 3):
+        pool = packed.pools[p]
+        want = alloc_ref.stage_counts(pool.caps, L, pool.kmax)
+        got = {k: int(stages[koff[p] + k - 1]) for k in range(1, pool.kmax + 1) if int(stages[koff[p] + k - 1]) > 0}
+        assert {k: s for k, (s, _) in want.items()} == got, p
