@@ -289,24 +289,6 @@ struct Bits {
     uint64_t w[BWORDS];
 };
 
-__device__ __forceinline__ void bits_shl_or(Bits& dst, const Bits& src, int s, int nbits) {
-    // dst = src | ((src << s) & (2^nbits - 1))
-    const int ws = s >> 6, bs = s & 63;
-#pragma unroll
-    for (int q = BWORDS - 1; q >= 0; --q) {
-        uint64_t v = 0;
-        const int from = q - ws;
-        if (from >= 0) {
-            v = src.w[from] << bs;
-            if (bs && from - 1 >= 0) v |= src.w[from - 1] >> (64 - bs);
-        }
-        const int lo = q * 64;
-        if (lo >= nbits) v = 0;
-        else if (nbits - lo < 64) v &= (1ull << (nbits - lo)) - 1ull;
-        dst.w[q] = src.w[q] | v;
-    }
-}
-
 __device__ __forceinline__ bool bits_test(const Bits& b, int i) { return (b.w[i >> 6] >> (i & 63)) & 1ull; }
 
 struct Frame {          // one peel() activation; its pool = range(m) minus the picks of frames above it
@@ -317,22 +299,51 @@ struct Frame {          // one peel() activation; its pool = range(m) minus the 
 };
 
 __device__ void frame_pool(const Frame* fr, int d, int m, Mask& pool) {
-    pool.clear();
-    for (int i = 0; i < m; ++i) pool.set(i);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {                            // range(m) word by word
+        const int lo = w * 64;
+        pool.w[w] = m >= lo + 64 ? ~0ull : (m > lo ? (1ull << (m - lo)) - 1ull : 0ull);
+    }
     for (int q = 0; q < d; ++q)
+#pragma unroll
         for (int w = 0; w < 4; ++w) pool.w[w] &= ~fr[q].picked.w[w];
 }
 
 __device__ int pool_items(const Mask& pool, int m, uint16_t* items) {
-    int n = 0;
-    for (int i = 0; i < m; ++i) if (pool.test(i)) items[n++] = (uint16_t)i;
+    int n = 0;                                               // set bits in ascending order
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+        for (uint64_t x = pool.w[w]; x; x &= x - 1) items[n++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
+    (void)m;
     return n;
 }
 
+// reach[p + 1] = reach[p] | ((reach[p] << v_p) & (2^(2L) - 1)) with the running set kept in registers
 __device__ void compute_reach(const int* caps, int L, const uint16_t* items, int n, Bits* reach) {
-    for (int q = 0; q < BWORDS; ++q) reach[0].w[q] = 0;
-    reach[0].w[0] = 1;
-    for (int p = 0; p < n; ++p) bits_shl_or(reach[p + 1], reach[p], cval(caps, items[p], L), 2 * L);
+    static_assert(BWORDS == 4, "compute_reach is written for 4 words");
+    const int nbits = 2 * L;
+    uint64_t lim[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int lo = q * 64;
+        lim[q] = lo >= nbits ? 0ull : (nbits - lo >= 64 ? ~0ull : (1ull << (nbits - lo)) - 1ull);
+    }
+    uint64_t r0 = 1, r1 = 0, r2 = 0, r3 = 0;
+    reach[0].w[0] = r0; reach[0].w[1] = 0; reach[0].w[2] = 0; reach[0].w[3] = 0;
+    for (int p = 0; p < n; ++p) {
+        const int s = cval(caps, items[p], L);
+        const int ws = s >> 6, bs = s & 63;
+        const uint64_t w0 = ws == 0 ? r0 : 0ull;
+        const uint64_t w1 = ws == 0 ? r1 : (ws == 1 ? r0 : 0ull);
+        const uint64_t w2 = ws == 0 ? r2 : (ws == 1 ? r1 : (ws == 2 ? r0 : 0ull));
+        const uint64_t w3 = ws == 0 ? r3 : (ws == 1 ? r2 : (ws == 2 ? r1 : (ws == 3 ? r0 : 0ull)));
+        // (lo >> 1) >> (63 - bs) == lo >> (64 - bs) for bs >= 1 and 0 for bs == 0 (no 64-bit shift by 64)
+        r0 |= (w0 << bs) & lim[0];
+        r1 |= ((w1 << bs) | ((w0 >> 1) >> (63 - bs))) & lim[1];
+        r2 |= ((w2 << bs) | ((w1 >> 1) >> (63 - bs))) & lim[2];
+        r3 |= ((w3 << bs) | ((w2 >> 1) >> (63 - bs))) & lim[3];
+        reach[p + 1].w[0] = r0; reach[p + 1].w[1] = r1; reach[p + 1].w[2] = r2; reach[p + 1].w[3] = r3;
+    }
 }
 
 // returns true on success; the k groups are then fr[0..k-1].picked, in peel order
