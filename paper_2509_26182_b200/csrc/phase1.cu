@@ -1225,6 +1225,18 @@ extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* ko
                                      int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool,
                                      const int32_t* cand_k, int32_t n_cand, int32_t* stall, void* stream) {
     cudaStream_t s = ss_stream(stream);
+    // The cover kernels keep their peel frames / reach bitsets on the thread stack (~28 KB).  Reserving that
+    // stack size once stops the driver from resizing the device's local-memory pool between launches of
+    // kernels with different stack needs (measured: sporadic 0.4-1.7 s stalls on a single allocate() call).
+    static bool stack_reserved = false;
+    if (!stack_reserved) {
+        size_t cur = 0;
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, cover_kernel) == cudaSuccess && cudaDeviceGetLimit(&cur, cudaLimitStackSize) ==
+                cudaSuccess && cur < fa.localSizeBytes)
+            cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes);
+        stack_reserved = true;
+    }
     // A batch too small to fill the GPU (one allocate() call: ~4 regions x k_max candidates) tries every group
     // count m of every candidate in parallel; an attempt gives up as soon as a smaller m of its candidate has
     // succeeded (peel polls best_m), and the smallest success is the reference's first-success m.  A large sweep
