@@ -312,10 +312,15 @@ __device__ __forceinline__ long long request_tokens(uint64_t mix, int i, int lo,
            (long long)(ss_splitmix64(mix ^ (0x70ull << 40) ^ (uint64_t)i) % (uint64_t)(hi - lo + 1));
 }
 
-__global__ void __launch_bounds__(32) admission_warp_kernel(ss_dag_set D, WarpLayout A, AdmissionArgs Q) {
+// NWD as in replay_warp_kernel: the chain DP of every admission attempt spreads its destinations over NWD warps
+template <int NWD>
+__global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, WarpLayout A, AdmissionArgs Q) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NT = NWD * 32;
     const int dag = blockIdx.x;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double vshare;
+    __shared__ int flag[3];
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     const int l0 = D.layer_ptr[dag];
     const int nl = D.layer_ptr[dag + 1] - l0;
@@ -335,22 +340,24 @@ __global__ void __launch_bounds__(32) admission_warp_kernel(ss_dag_set D, WarpLa
     double* costs = reinterpret_cast<double*>(smem + A.off_cost);
     long long* kv = reinterpret_cast<long long*>(smem + A.off_kv);
     long long* tcap = reinterpret_cast<long long*>(smem + A.off_tcap);
-    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane)) {
-        if (lane == 0) Q.status[dag] = SS_BAD_INPUT;
+    if (warp == 0) flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? 0 : 1;
+    __syncthreads();
+    if (flag[0]) {
+        if (tid == 0) Q.status[dag] = SS_BAD_INPUT;
         return;
     }
     const int gbase = Q.gpu_ptr[dag];
     const int ng = Q.gpu_ptr[dag + 1] - gbase;
-    for (int g = lane; g < ng; g += 32) {
+    for (int g = tid; g < ng; g += NT) {
         occ[g] = 0;
         kv[g] = 0;
         stamp[g] = 0;
         base[g] = Q.base_tau[gbase + g];
         tcap[g] = Q.token_cap[gbase + g];
     }
-    for (int o = lane; o < A.pow_len; o += 32) pw[o] = Q.occpow[o];
-    if (lane < 8) { costs[32 + lane] = INF; costs[72 + lane] = INF; }
-    __syncwarp();
+    for (int o = tid; o < A.pow_len; o += NT) pw[o] = Q.occpow[o];
+    if (tid < 8) { costs[32 + tid] = INF; costs[72 + tid] = INF; }
+    __syncthreads();
     const uint64_t mix = ss_splitmix64((uint64_t)Q.seeds[dag]);
     const int steps = Q.steps, W = Q.window;
     const int stride = D.max_layers + 1;
@@ -363,37 +370,41 @@ __global__ void __launch_bounds__(32) admission_warp_kernel(ss_dag_set D, WarpLa
             const int32_t* slot = adm + (int64_t)done_head * stride;
             const int cnt = slot[0];
             const long long tok = request_tokens(mix, done_head, Q.tok_lo, Q.tok_hi);
-            for (int k = lane; k < cnt; k += 32) {
+            for (int k = tid; k < cnt; k += NT) {
                 occ[slot[1 + k]] -= 1;
                 kv[slot[1 + k]] -= tok;
             }
-            __syncwarp();
+            __syncthreads();
             ++done_head;
         }
         // request t arrived: drain the queue [head, t] strictly FIFO (sim.py:345-351, 361-366)
         while (head <= t) {
             const long long tok = request_tokens(mix, head, Q.tok_lo, Q.tok_hi);
-            int err = 0, errg = 0;
-            for (int g = lane; g < ng; g += 32) {
+            if (tid == 0) flag[1] = 0;
+            __syncthreads();
+            for (int g = tid; g < ng; g += NT) {
                 const int o = occ[g];
-                if (o >= Q.occpow_len) { err = SS_BAD_INPUT; errg = g; }
+                if (o >= Q.occpow_len) { flag[1] = SS_BAD_INPUT; flag[2] = g; }
                 const int oc = o >= Q.occpow_len ? Q.occpow_len - 1 : o;
                 const double live = base[g] * (oc < A.pow_len ? pw[oc] : Q.occpow[oc]);
                 tau[g] = tcap[g] - kv[g] < tok ? INF : live;      // KV-blocked GPUs are excluded (sim.py:321-325)
             }
-            const unsigned em = __ballot_sync(FULL, err != 0);
-            if (em) {
-                status = __shfl_sync(FULL, err, __ffs(em) - 1);
-                aux = __shfl_sync(FULL, errg, __ffs(em) - 1);
+            __syncthreads();
+            if (flag[1]) {
+                status = flag[1];
+                aux = flag[2];
                 break;
             }
-            __syncwarp();
-            const double v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+            double v;
+            if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+            else v = mw_route<NWD>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
             if (!(v <= DBL_MAX)) break;                          // UncoveredLayer / NoPath: the head waits
+            __syncthreads();
             // admit: reserve the tokens and +1 occupancy on the chain's distinct GPUs (sim.py:330-331)
             int32_t* slot = adm + (int64_t)head * stride;
             const int tag = head + 1;
             int cnt = 0;
+            if (warp == 0) {
             for (int c0 = 0; c0 < nl; c0 += 32) {
                 const int l = c0 + lane;
                 int g = 0;
@@ -416,19 +427,21 @@ __global__ void __launch_bounds__(32) admission_warp_kernel(ss_dag_set D, WarpLa
                 step_out[head] = t;
                 Q.cost_out[(int64_t)dag * steps + head] = v;
             }
-            __syncwarp();
+            }
+            __syncthreads();
             ++head;
         }
     }
-    for (int i = head + lane; i < steps; i += 32) {              // still queued at the end
+    __syncthreads();
+    for (int i = head + tid; i < steps; i += NT) {               // still queued at the end
         step_out[i] = -1;
         Q.cost_out[(int64_t)dag * steps + i] = INF;
     }
-    for (int g = lane; g < ng; g += 32) {
+    for (int g = tid; g < ng; g += NT) {
         Q.kv_out[gbase + g] = kv[g];
         Q.occ_out[gbase + g] = occ[g];
     }
-    if (lane == 0) {
+    if (tid == 0) {
         Q.status[dag] = status;
         Q.aux[dag] = aux;
     }
@@ -506,10 +519,19 @@ extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr,
     if (!warp_layout(D, 0, occpow_len, A)) return SS_BAD_INPUT;
     AdmissionArgs Q{gpu_ptr, base_tau, token_cap, occpow, occpow_len, seeds, tok_lo, tok_hi, steps, window,
                     adm_gpus, step_out, cost_out, gpus_out, kv_out, occ_out, status, aux};
-    if (cudaFuncSetAttribute(admission_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) !=
-        cudaSuccess)
-        return SS_CUDA_ERROR;
-    admission_warp_kernel<<<D.n_dags, 32, A.total, ss_stream(stream_h)>>>(D, A, Q);
+    cudaStream_t s = ss_stream(stream_h);
+    auto run = [&](auto kern, int threads) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
+            return SS_CUDA_ERROR;
+        kern<<<D.n_dags, threads, A.total, s>>>(D, A, Q);
+        return SS_OK;
+    };
+    int rc;
+    if (D.max_hosts <= 8) rc = run(admission_warp_kernel<1>, 32);
+    else if (D.max_hosts <= 16) rc = run(admission_warp_kernel<2>, 64);
+    else if (D.max_hosts <= 24) rc = run(admission_warp_kernel<3>, 96);
+    else rc = run(admission_warp_kernel<4>, 128);
+    if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
     return SS_OK;
 }
