@@ -109,3 +109,19 @@ def test_dropin_release_without_select_underflows(cuda_ready):
     with pytest.raises(OccupancyUnderflow):
         router.release(PipelineChain(hops=(LayerSlice("a", 1, 1), LayerSlice("b", 2, 2)), cost_s=0.0), 0.0)
     assert pm.occupancy("a") == 0 and pm.occupancy("b") == 0
+
+
+@pytest.mark.parametrize("n", [12, 20, 29])
+def test_multiwarp_route_single_layer_and_ties(cuda_ready, n):
+    """replay_warp_kernel<NWD> (NWD = 2, 3, 4 for 12 / 20 / 29 hosts): a one-layer model (no boundary: only the
+    final first-index argmin) and a tie-quantised 6-layer pool where equal candidates meet across the four source
+    phases and warps -- both vs the oracle's strict-< numpy argmin."""
+    rng = np.random.default_rng(50 + n)
+    rtt, tau = random_pool(rng, n)
+    check_vs_oracle(manual_set(1, [1] * n, [1] * n, rtt, np.full(n, 2e-4)), "warp")
+    q = rng.choice([0.001, 0.002], size=(n, n))
+    q = np.triu(q, 1) + np.triu(q, 1).T
+    lo = rng.integers(1, 4, size=n)
+    hi = np.minimum(lo + rng.integers(2, 5, size=n), 6)
+    lo[:3], hi[:3] = 1, 6                                      # every layer covered
+    check_vs_oracle(manual_set(6, lo, hi, q, np.full(n, 1e-4)), "warp", n_req=16, window=5)
