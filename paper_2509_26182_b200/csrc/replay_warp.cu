@@ -46,6 +46,7 @@ struct MwBoundary {
     double td;
 };
 
+template <int SPL>
 __device__ __forceinline__ void mw_fetch(MwBoundary& m, const double* E, const int* node, const int* cl,
                                          const int* noff, const int* eoff, const double* tau, int b, int j, int q) {
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -54,14 +55,15 @@ __device__ __forceinline__ void mw_fetch(MwBoundary& m, const double* E, const i
     const bool act = j < m.rd;
     const double* ep = E + eoff[b] + j;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < SPL; ++k) {
         const int i = q + 4 * k;
         m.e[k] = (act && i < m.rs) ? ep[i * m.rd] : INF;
     }
     m.td = act ? tau[node[noff[b + 1] + j]] : 0.0;
 }
 
-template <int NWD>
+// SPL = ceil(widest column / 4): source slots per lane (the tree and the prefetch shrink with the column)
+template <int NWD, int SPL>
 __device__ double mw_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
                            int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, double* vshare,
                            int tid) {
@@ -74,22 +76,22 @@ __device__ double mw_route(const double* E, const int* node, const int* cl, cons
     double* nxt = costs + 40;
     for (int p = tid; p < 32; p += NT) cur[p] = p < cl[0] ? tau[node[p]] : INF;
     MwBoundary m;
-    if (nblk > 0) mw_fetch(m, E, node, cl, noff, eoff, tau, 0, j, q);
+    if (nblk > 0) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, 0, j, q);
     __syncthreads();
     for (int b = 0; b < nblk; ++b) {
-        double a[8];
+        double a[SPL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(cur[q + 4 * k], m.e[k]);
+        for (int k = 0; k < SPL; ++k) a[k] = __dadd_rn(cur[q + 4 * k], m.e[k]);
         const int rd = m.rd;
         const double td = m.td;
         // in-lane tree: left operands always carry the smaller source index -> take the right one on `<`
-        int ix[8];
+        int ix[SPL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) ix[k] = k;
+        for (int k = 0; k < SPL; ++k) ix[k] = k;
 #pragma unroll
-        for (int w = 1; w < 8; w <<= 1)
+        for (int w = 1; w < SPL; w <<= 1)
 #pragma unroll
-            for (int k = 0; k < 8; k += 2 * w)
+            for (int k = 0; k + w < SPL; k += 2 * w)
                 if (a[k + w] < a[k]) { a[k] = a[k + w]; ix[k] = ix[k + w]; }
         double best = a[0];
         int bi = q + 4 * ix[0];
@@ -104,7 +106,7 @@ __device__ double mw_route(const double* E, const int* node, const int* cl, cons
             nxt[j] = __dadd_rn(best, td);
         }
         // next boundary's operands: issued behind the shuffles (shared LSU queue), landing during the barrier
-        if (b + 1 < nblk) mw_fetch(m, E, node, cl, noff, eoff, tau, b + 1, j, q);
+        if (b + 1 < nblk) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, b + 1, j, q);
         __syncthreads();
         double* t = cur; cur = nxt; nxt = t;
     }
@@ -135,7 +137,7 @@ __device__ double mw_route(const double* E, const int* node, const int* cl, cons
 
 // NWD = 1: one warp owns the scenario (<= 8 hosts per column, warp_route).  NWD = 2..4: the destinations of
 // every boundary are spread over NWD warps (mw_route); the rest of the request stays on warp 0.
-template <int NWD>
+template <int NWD, int SPL>
 __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
         // ---- DP over the layer columns + final argmin / backtrack ------------------
         double v;
         if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
-        else v = mw_route<NWD>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+        else v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
         mark(1);
         if (tid == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         if (!(v <= DBL_MAX)) {
@@ -313,7 +315,7 @@ __device__ __forceinline__ long long request_tokens(uint64_t mix, int i, int lo,
 }
 
 // NWD as in replay_warp_kernel: the chain DP of every admission attempt spreads its destinations over NWD warps
-template <int NWD>
+template <int NWD, int SPL>
 __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, WarpLayout A, AdmissionArgs Q) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
             }
             double v;
             if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
-            else v = mw_route<NWD>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+            else v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
             if (!(v <= DBL_MAX)) break;                          // UncoveredLayer / NoPath: the head waits
             __syncthreads();
             // admit: reserve the tokens and +1 occupancy on the chain's distinct GPUs (sim.py:330-331)
@@ -485,10 +487,15 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
     };
     // destinations per boundary over ceil(hosts / 8) warps (latency: C2's 17 hosts -> 3 warps)
     int rc;
-    if (D.max_hosts <= 8) rc = run(replay_warp_kernel<1>, 32);
-    else if (D.max_hosts <= 16) rc = run(replay_warp_kernel<2>, 64);
-    else if (D.max_hosts <= 24) rc = run(replay_warp_kernel<3>, 96);
-    else rc = run(replay_warp_kernel<4>, 128);
+    switch ((D.max_hosts + 3) / 4) {                             // source slots per lane
+        case 0: case 1: case 2: rc = run(replay_warp_kernel<1, 8>, 32); break;
+        case 3: rc = run(replay_warp_kernel<2, 3>, 64); break;
+        case 4: rc = run(replay_warp_kernel<2, 4>, 64); break;
+        case 5: rc = run(replay_warp_kernel<3, 5>, 96); break;
+        case 6: rc = run(replay_warp_kernel<3, 6>, 96); break;
+        case 7: rc = run(replay_warp_kernel<4, 7>, 128); break;
+        default: rc = run(replay_warp_kernel<4, 8>, 128); break;
+    }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
     if (R.prof) {
@@ -527,10 +534,15 @@ extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr,
         return SS_OK;
     };
     int rc;
-    if (D.max_hosts <= 8) rc = run(admission_warp_kernel<1>, 32);
-    else if (D.max_hosts <= 16) rc = run(admission_warp_kernel<2>, 64);
-    else if (D.max_hosts <= 24) rc = run(admission_warp_kernel<3>, 96);
-    else rc = run(admission_warp_kernel<4>, 128);
+    switch ((D.max_hosts + 3) / 4) {                             // source slots per lane
+        case 0: case 1: case 2: rc = run(admission_warp_kernel<1, 8>, 32); break;
+        case 3: rc = run(admission_warp_kernel<2, 3>, 64); break;
+        case 4: rc = run(admission_warp_kernel<2, 4>, 64); break;
+        case 5: rc = run(admission_warp_kernel<3, 5>, 96); break;
+        case 6: rc = run(admission_warp_kernel<3, 6>, 96); break;
+        case 7: rc = run(admission_warp_kernel<4, 7>, 128); break;
+        default: rc = run(admission_warp_kernel<4, 8>, 128); break;
+    }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
     return SS_OK;
