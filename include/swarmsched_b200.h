@@ -67,6 +67,10 @@ typedef struct ss_dag_set {
     const double*  edge_val;    /* row-major R_l x R_{l+1}: row = source host, col = destination */
 } ss_dag_set;
 
+/* Per-scenario RTT matrices on device: out[s] = base_rtt (n_gpus x n_gpus, row-major) times the exact dyadic
+ * pair jitter of seed s (replaces scenarios.py ScenarioSet.scenario_rtt + an H2D copy of S x N x N doubles). */
+int ss_scenario_rtt(int32_t n_scen, int32_t n_gpus, const double* base_rtt, const int64_t* seeds, double* out,
+                    void* stream);
 /* Dense RTT matrices, one per item (router.py:118-143 rtt_matrix and
  * topology.py:133-142 rtt_s share one rule): out[a][b] = direct (a,b) entry if
  * given, else the (b,a) entry, else `default_value`; diagonal 0; self-links

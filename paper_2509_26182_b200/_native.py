@@ -46,6 +46,7 @@ _SIGS = {
     "ss_status_str": (C.c_char_p, [C.c_int]),
     "ss_version": (C.c_int, []),
     "ss_limits": (C.c_int, [i32p, i32p, i32p]),
+    "ss_scenario_rtt": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_rtt_fill": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_dag_columns": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

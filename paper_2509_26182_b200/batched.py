@@ -562,8 +562,6 @@ class ScenarioReplayer:
         pow_len = max_live + 2
         pub = np.array([float((1 + o) ** contention) for o in range(pow_len)])
         exe = np.array([float(max(1, o) ** contention) for o in range(pow_len)])
-        rtt = np.stack([self.scen.scenario_rtt(s) for s in range(S)]) if self.scen.jitter else \
-            np.broadcast_to(self.scen.base_rtt, (S, G, G)).copy()
         up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=self.dev, dtype=dt)
         if not hasattr(self, "_tokcap"):
             self._tokcap = torch.from_numpy(np.tile(self.scen.token_cap, S)).to(self.dev)
@@ -575,7 +573,14 @@ class ScenarioReplayer:
         peak = torch.zeros(S, dtype=torch.int32, device=self.dev)
         nev = torch.zeros(S, dtype=torch.int64, device=self.dev)
         ptr_d, arr_d, pr_d, ou_d = up(ptr, torch.int32), up(arr, torch.float64), up(pr, torch.int32), up(ou, torch.int32)
-        rtt_d, pub_d, exe_d = up(rtt, torch.float64), up(pub, torch.float64), up(exe, torch.float64)
+        pub_d, exe_d = up(pub, torch.float64), up(exe, torch.float64)
+        # per-scenario RTT matrices (scenario_rtt) built on device from the pool matrix and the jitter seeds
+        if self.scen.jitter:
+            rtt_d = torch.empty(S * G * G, dtype=torch.float64, device=self.dev)
+            N.check(N.lib().ss_scenario_rtt(S, G, N.ptr(self.base_rtt), N.ptr(self.seeds), N.ptr(rtt_d),
+                                            N.stream_handle(self.stream)), "ss_scenario_rtt")
+        else:
+            rtt_d = self.base_rtt.reshape(-1).repeat(S)
         fn = N.lib().ss_sim_warp if self.mode == "warp" else N.lib().ss_sim_cta
         N.check(fn(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self._tokcap),
                                     N.ptr(rtt_d), N.ptr(pub_d), N.ptr(exe_d), pow_len, N.ptr(ptr_d), N.ptr(arr_d),
@@ -590,18 +595,27 @@ class ScenarioReplayer:
         self.raise_first_failure()
         done_t, done_r = done_t.cpu().numpy(), done_r.cpu().numpy()
         dur, comp, peak, nev = dur.cpu().numpy(), comp.cpu().numpy(), peak.cpu().numpy(), nev.cpu().numpy()
+        # latencies in completion order per scenario (sim.py:397), vectorised: sort completed requests by
+        # (scenario, completion rank); float64 subtraction is the reference's float subtraction
+        total_n = int(ptr[-1])
+        scen_of = np.repeat(np.arange(S), n)
+        lat_all = done_t[:total_n] - arr[:total_n]
+        fin = np.nonzero(done_r[:total_n] >= 0)[0]
+        fin = fin[np.lexsort((done_r[fin], scen_of[fin]))]
+        cut = np.searchsorted(scen_of[fin], np.arange(S + 1))
+        lat_sorted = lat_all[fin]
+        by_value = lat_sorted.copy()
+        for s_ in range(S):                                          # per-scenario ascending copy for percentiles
+            by_value[cut[s_]:cut[s_ + 1]].sort()
         reports = []
         for s in range(S):
             a, b = int(ptr[s]), int(ptr[s + 1])
-            ranks = done_r[a:b]
-            done = np.nonzero(ranks >= 0)[0]
-            order = done[np.argsort(ranks[done], kind="stable")]
-            lat = [float(done_t[a + i]) - float(arr[a + i]) for i in order]     # completion order (sim.py:397)
+            lat = lat_sorted[cut[s]:cut[s + 1]].tolist()
             mean = p50 = p95 = p99 = 0.0
             if lat:
                 mean = sum(lat) / len(lat)                                     # CPython 3.12 sum, as sim.py:457
-                srt = sorted(lat)
-                rank = lambda q: srt[max(1, math.ceil(q * len(srt) / 100.0)) - 1]
+                srt = by_value[cut[s]:cut[s + 1]]
+                rank = lambda q: float(srt[max(1, math.ceil(q * len(lat) / 100.0)) - 1])
                 p50, p95, p99 = rank(50), rank(95), rank(99)
             d = float(dur[s])
             reports.append({"submitted": b - a, "completed": int(comp[s]), "unserved": b - a - int(comp[s]),

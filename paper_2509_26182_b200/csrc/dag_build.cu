@@ -146,6 +146,20 @@ __global__ void dag_edges_kernel(ss_dag_set D, const int64_t* rtt_off, const int
     }
 }
 
+// out[s][a][b] = base[a][b] * jitter(seed_s, a, b) (scenarios.py:ScenarioSet.scenario_rtt: the pool matrix times the
+// scenario's exact dyadic pair jitter, diagonal untouched)
+__global__ void scenario_rtt_kernel(int32_t n_gpus, const double* base, const int64_t* seeds, double* out) {
+    const int s = blockIdx.y;
+    const uint64_t mix = ss_splitmix64((uint64_t)seeds[s]);
+    const int64_t nn = (int64_t)n_gpus * n_gpus;
+    double* o = out + (int64_t)s * nn;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(e / n_gpus), b = (int)(e - (int64_t)a * n_gpus);
+        const double v = base[e];
+        o[e] = a == b ? v : v * ss_jitter(mix, (uint32_t)a, (uint32_t)b);
+    }
+}
+
 }  // namespace
 
 extern "C" int ss_rtt_fill(int32_t n_items, const int64_t* mat_off, const int32_t* mat_dim, double* out,
@@ -197,6 +211,17 @@ extern "C" int ss_dag_edges(const ss_dag_set* dags, const int64_t* rtt_off, cons
     dim3 grid(dags->max_layers - 1, dags->n_dags);
     dag_edges_kernel<<<grid, 256, 0, ss_stream(stream)>>>(*dags, rtt_off, rtt_dim, rtt, jitter_seed, n_pool_gpus,
                                                           edge_val);
+    SS_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_scenario_rtt(int32_t n_scen, int32_t n_gpus, const double* base_rtt, const int64_t* seeds,
+                               double* out, void* stream) {
+    if (n_scen <= 0) return SS_OK;
+    if (n_gpus < 1 || !base_rtt || !seeds || !out || n_scen > 65535) return SS_BAD_INPUT;
+    const int64_t nn = (int64_t)n_gpus * n_gpus;
+    dim3 grid((unsigned)((nn + 255) / 256 < 64 ? (nn + 255) / 256 : 64), n_scen);
+    scenario_rtt_kernel<<<grid, 256, 0, ss_stream(stream)>>>(n_gpus, base_rtt, seeds, out);
     SS_CHECK_LAUNCH();
     return SS_OK;
 }

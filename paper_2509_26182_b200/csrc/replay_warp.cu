@@ -32,109 +32,6 @@ struct WarpReplay {
     unsigned long long* prof;   // diagnostics (env SS_WARP_PROF=1): cycles per phase, else NULL
 };
 
-// Chain DP spread over NWD warps (9..32 hosts per column): warp w owns destinations [8w, 8w+8); lane
-// (d, q) = (lane & 7, lane >> 3) takes the sources q, q+4, ..., q+28 of destination 8w+d.  The argmin is a
-// lexicographic (value, index) minimum -- identical to numpy's first-index argmin with a strict `<` scan
-// (all-+inf resolves to index 0, as np.argmin does) -- formed as an in-lane tree plus two shuffle rounds, so
-// every merge stays inside the warp and a boundary costs one CTA barrier.  The boundary's edge entries,
-// column lengths and destination latencies do not depend on the running costs: they are fetched into
-// registers one boundary ahead, leaving only cur[] loads -> DADD -> tree -> shuffles -> store on the
-// critical path.  Same contract as warp_route (picks valid when the returned cost is finite).
-struct MwBoundary {
-    int rs, rd;
-    double e[8];
-    double td;
-};
-
-template <int SPL>
-__device__ __forceinline__ void mw_fetch(MwBoundary& m, const double* E, const int* node, const int* cl,
-                                         const int* noff, const int* eoff, const double* tau, int b, int j, int q) {
-    const double INF = __longlong_as_double(0x7ff0000000000000ll);
-    m.rs = cl[b];
-    m.rd = cl[b + 1];
-    const bool act = j < m.rd;
-    const double* ep = E + eoff[b] + j;
-#pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-        const int i = q + 4 * k;
-        m.e[k] = (act && i < m.rs) ? ep[i * m.rd] : INF;
-    }
-    m.td = act ? tau[node[noff[b + 1] + j]] : 0.0;
-}
-
-// SPL = ceil(widest column / 4): source slots per lane (the tree and the prefetch shrink with the column)
-template <int NWD, int SPL>
-__device__ double mw_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
-                           int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, double* vshare,
-                           int tid) {
-    const double INF = __longlong_as_double(0x7ff0000000000000ll);
-    constexpr int NT = NWD * 32;
-    const int warp = tid >> 5, lane = tid & 31, d = lane & 7, q = lane >> 3;
-    const int j = warp * 8 + d;
-    const uint32_t bp_s = (uint32_t)__cvta_generic_to_shared(bp);   // hoisted: no per-boundary window lookup
-    double* cur = costs;                                     // [40]: 32 hosts + 8 pad (+inf)
-    double* nxt = costs + 40;
-    for (int p = tid; p < 32; p += NT) cur[p] = p < cl[0] ? tau[node[p]] : INF;
-    MwBoundary m;
-    if (nblk > 0) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, 0, j, q);
-    __syncthreads();
-    for (int b = 0; b < nblk; ++b) {
-        double a[SPL];
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) a[k] = __dadd_rn(cur[q + 4 * k], m.e[k]);
-        const int rd = m.rd;
-        const double td = m.td;
-        // in-lane tree: left operands always carry the smaller source index -> take the right one on `<`
-        int ix[SPL];
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) ix[k] = k;
-#pragma unroll
-        for (int w = 1; w < SPL; w <<= 1)
-#pragma unroll
-            for (int k = 0; k + w < SPL; k += 2 * w)
-                if (a[k + w] < a[k]) { a[k] = a[k + w]; ix[k] = ix[k + w]; }
-        double best = a[0];
-        int bi = q + 4 * ix[0];
-#pragma unroll
-        for (int o = 8; o <= 16; o <<= 1) {
-            const double v2 = __shfl_xor_sync(FULL, best, o);
-            const int i2 = __shfl_xor_sync(FULL, bi, o);
-            lexmin(best, bi, v2, i2);
-        }
-        if (q == 0 && j < rd) {
-            asm volatile("st.shared.u8 [%0], %1;" ::"r"(bp_s + b * 32 + j), "r"(bi));
-            nxt[j] = __dadd_rn(best, td);
-        }
-        // next boundary's operands: issued behind the shuffles (shared LSU queue), landing during the barrier
-        if (b + 1 < nblk) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, b + 1, j, q);
-        __syncthreads();
-        double* t = cur; cur = nxt; nxt = t;
-    }
-    if (warp == 0) {
-        double v = lane < cl[nblk] ? cur[lane] : INF;
-        int idx = lane < cl[nblk] ? lane : NONE;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double v2 = __shfl_xor_sync(FULL, v, o);
-            const int i2 = __shfl_xor_sync(FULL, idx, o);
-            lexmin(v, idx, v2, i2);
-        }
-        if (lane == 0) {
-            *vshare = v;
-            if (v <= DBL_MAX) {
-                int p = idx;
-                picks[nblk] = p;
-                for (int b = nblk - 1; b >= 0; --b) {
-                    p = bp[b * 32 + p];
-                    picks[b] = p;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    return *vshare;
-}
-
 // NWD = 1: one warp owns the scenario (<= 8 hosts per column, warp_route).  NWD = 2..4: the destinations of
 // every boundary are spread over NWD warps (mw_route); the rest of the request stays on warp 0.
 template <int NWD, int SPL>

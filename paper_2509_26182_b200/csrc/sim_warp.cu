@@ -589,6 +589,243 @@ __global__ void __launch_bounds__(NT) sim_cta_kernel(ss_dag_set D, CtaLayout B, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// 9..32 hosts per layer: the warp-resident layout of sim_warp_kernel (edges staged in shared memory), the
+// lockstep event loop of sim_cta_kernel over NWD warps, and the destination-split chain DP (mw_route) for
+// every admission attempt -- the route is most of a request's cost at C2 shape.
+// ---------------------------------------------------------------------------
+template <int NWD, int SPL>
+__global__ void __launch_bounds__(NWD * 32) sim_mw_kernel(ss_dag_set D, WarpLayout A, SimLayout B, SimArgs P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NT = NWD * 32;
+    const int dag = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const int l0 = D.layer_ptr[dag];
+    const int nl = D.layer_ptr[dag + 1] - l0;
+    const int nblk = nl - 1;
+    __shared__ double vshare;
+    __shared__ int misc[2];                                     // [0] status / staging flag, [1] finish
+    double* E = reinterpret_cast<double*>(smem + A.off_E);
+    int* node = reinterpret_cast<int*>(smem + A.off_node);
+    int* cl = reinterpret_cast<int*>(smem + A.off_cl);
+    int* noff = reinterpret_cast<int*>(smem + A.off_noff);
+    int* eoff = reinterpret_cast<int*>(smem + A.off_eoff);
+    uint8_t* bp = smem + A.off_bp;
+    int* picks = reinterpret_cast<int*>(smem + A.off_picks);
+    double* tau = reinterpret_cast<double*>(smem + A.off_tau);
+    double* base = reinterpret_cast<double*>(smem + A.off_base);
+    int* occ = reinterpret_cast<int*>(smem + A.off_occ);
+    int* stamp = reinterpret_cast<int*>(smem + A.off_stamp);
+    double* ppw = reinterpret_cast<double*>(smem + A.off_pow);
+    double* costs = reinterpret_cast<double*>(smem + A.off_cost);
+    long long* kv = reinterpret_cast<long long*>(smem + A.off_kv);
+    long long* tcap = reinterpret_cast<long long*>(smem + A.off_tcap);
+    double* ev_time = reinterpret_cast<double*>(smem + B.off_time);
+    int* ev_seq = reinterpret_cast<int*>(smem + B.off_seq);
+    int* ev_req = reinterpret_cast<int*>(smem + B.off_req);
+    int* ev_rem = reinterpret_cast<int*>(smem + B.off_rem);
+    uint8_t* ev_kind = smem + B.off_kind;
+    uint8_t* ev_nh = smem + B.off_nh;
+    double* ev_crtt = reinterpret_cast<double*>(smem + B.off_crtt);
+    long long* ev_tok = reinterpret_cast<long long*>(smem + B.off_tok);
+    short2* ev_hops = reinterpret_cast<short2*>(smem + B.off_hops);
+    double* xpw = reinterpret_cast<double*>(smem + B.off_xpw);
+
+    if (warp == 0) misc[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? SS_OK : SS_BAD_INPUT;
+    __syncthreads();
+    if (misc[0] != SS_OK) {
+        if (tid == 0) P.status[dag] = SS_BAD_INPUT;
+        return;
+    }
+    const int gbase = P.gpu_ptr[dag];
+    const int ng = P.gpu_ptr[dag + 1] - gbase;
+    for (int g = tid; g < ng; g += NT) {
+        occ[g] = 0;
+        kv[g] = 0;
+        stamp[g] = 0;
+        base[g] = P.base_tau[gbase + g];
+        tcap[g] = P.token_cap[gbase + g];
+    }
+    for (int o = tid; o < B.pow_len; o += NT) { ppw[o] = P.pub_pow[o]; xpw[o] = P.exec_pow[o]; }
+    for (int e = tid; e < B.max_live; e += NT) ev_kind[e] = 0xFF;
+    if (tid < 8) { costs[32 + tid] = INF; costs[72 + tid] = INF; }
+    __syncthreads();
+    const double* rtt = P.rtt + (int64_t)dag * D.max_gpus * D.max_gpus;
+    const int r0 = P.trace_ptr[dag], n = P.trace_ptr[dag + 1] - r0;
+    const double* arr = P.arrival + r0;
+    const int32_t* prm = P.prompt + r0;
+    const int32_t* outp = P.output + r0;
+
+    int ap = 0, adm = 0, live_n = 0, live_hw = 0, next_seq = n + 1, completed = 0, peak = 0, status = SS_OK;
+    bool tick = n > 0;                          // sim.py:264-265: first tick only if work remains
+    double tick_t = P.publish_interval, now = 0.0;
+    int tick_seq = n;
+    long long events = 0;
+
+    auto try_admit = [&](int i, double t) -> bool {
+        const long long tok = (long long)prm[i] + outp[i];
+        for (int g = tid; g < ng; g += NT) {
+            const int o = occ[g];
+            tau[g] = tcap[g] - kv[g] < tok ? INF : base[g] * (o < B.pow_len ? ppw[o] : P.pub_pow[o]);  // KV-blocked excluded
+        }
+        __syncthreads();
+        const double v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+        if (!(v <= DBL_MAX)) return false;
+        int slot = -1;                                           // same result in every warp
+        for (int e0 = 0; e0 < B.max_live && slot < 0; e0 += 32) {
+            const unsigned m = __ballot_sync(FULL, e0 + lane < B.max_live && ev_kind[e0 + lane] == 0xFF);
+            if (m) slot = e0 + __ffs(m) - 1;
+        }
+        if (slot < 0) { status = SS_BAD_INPUT; return false; }
+        const int tag = i + 1;
+        for (int l = tid; l < nl; l += NT) {
+            const int g = node[noff[l] + picks[l]];
+            if (atomicExch(&stamp[g], tag) != tag) { atomicAdd(&occ[g], 1); atomicAdd((unsigned long long*)&kv[g], (unsigned long long)tok); }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // merged hops, chain RTT, prefill = CPython sum(base_s * length) * prompt + chain RTT
+            int nh = 0, prev = -1;
+            short2* hp = ev_hops + slot * HMAX;
+            for (int l = 0; l < nl; ++l) {
+                const int g = node[noff[l] + picks[l]];
+                if (g == prev) { hp[nh - 1].y += 1; continue; }
+                if (nh == HMAX) { nh = HMAX + 1; break; }
+                hp[nh].x = (short)g;
+                hp[nh].y = 1;
+                ++nh;
+                prev = g;
+            }
+            if (nh > HMAX) {
+                misc[0] = SS_BAD_INPUT;
+            } else {
+                double crtt = 0.0;
+                for (int h = 0; h + 1 < nh; ++h) crtt = __dadd_rn(crtt, rtt[(int64_t)hp[h].x * D.max_gpus + hp[h + 1].x]);
+                PySum compute;
+                compute.init();
+                for (int h = 0; h < nh; ++h) compute.add_float(__dmul_rn(base[hp[h].x], (double)hp[h].y));
+                const double pre = __dadd_rn(__dmul_rn(compute.value(), (double)prm[i]), crtt);
+                ev_time[slot] = __dadd_rn(t, pre);
+                ev_seq[slot] = next_seq;
+                ev_req[slot] = i;
+                ev_rem[slot] = outp[i];
+                ev_kind[slot] = K_PREFILL;
+                ev_nh[slot] = (uint8_t)nh;
+                ev_crtt[slot] = crtt;
+                ev_tok[slot] = tok;
+            }
+        }
+        __syncthreads();
+        status = misc[0];
+        ++next_seq;
+        ++live_n;
+        if (slot + 1 > live_hw) live_hw = slot + 1;
+        return status == SS_OK;
+    };
+
+    int rank = 0;
+    while (status == SS_OK) {
+        // next event: lexicographic (time, seq) over live chains, the next arrival and the pending tick
+        double bt = INF;
+        int bs = 0x7fffffff, bk = -1;
+        for (int e = lane; e < live_hw; e += 32) {               // every warp reduces all entries
+            if (ev_kind[e] == 0xFF) continue;
+            const double t = ev_time[e];
+            const int q = ev_seq[e];
+            if (t < bt || (t == bt && q < bs)) { bt = t; bs = q; bk = e; }
+        }
+        if (lane == 0) {
+            if (ap < n && (arr[ap] < bt || (arr[ap] == bt && ap < bs))) { bt = arr[ap]; bs = ap; bk = -2; }
+            if (tick && (tick_t < bt || (tick_t == bt && tick_seq < bs))) { bt = tick_t; bs = tick_seq; bk = -3; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double t2 = __shfl_xor_sync(FULL, bt, o);
+            const int s2 = __shfl_xor_sync(FULL, bs, o);
+            const int k2 = __shfl_xor_sync(FULL, bk, o);
+            if (t2 < bt || (t2 == bt && s2 < bs)) { bt = t2; bs = s2; bk = k2; }
+        }
+        if (bk == -1) break;                                     // heap empty
+        now = bt;
+        ++events;
+        if (bk == -3) {                                          // publish tick (sim.py:432-436)
+            if (live_n > 0 || ap < n) { tick_t = __dadd_rn(now, P.publish_interval); tick_seq = next_seq++; }
+            else tick = false;
+            continue;
+        }
+        if (bk == -2) {                                          // arrival (sim.py:361-366)
+            const int i = ap++;
+            if (adm < i || !try_admit(i, now)) {
+                if (status != SS_OK) break;
+                peak = max(peak, ap - adm);
+            } else {
+                ++adm;
+            }
+            continue;
+        }
+        // prefill / step of live chain bk (sim.py:375-392)
+        const int e = bk;
+        if (tid == 0) {
+            if (ev_kind[e] == K_STEP) ev_rem[e] -= 1;
+            const bool finish = ev_rem[e] == 0;
+            misc[1] = finish;
+            if (!finish) {
+                const short2* hp = ev_hops + e * HMAX;
+                double total = 0.0;
+                for (int h = 0; h < ev_nh[e]; ++h) {
+                    const int g = hp[h].x;
+                    const int o = occ[g];
+                    const double xp = o < B.pow_len ? xpw[o] : P.exec_pow[o];
+                    total = __dadd_rn(total, __dmul_rn(__dmul_rn(base[g], xp), (double)hp[h].y));
+                }
+                if (!P.amortize_rtt) total = __dadd_rn(total, ev_crtt[e]);
+                ev_time[e] = __dadd_rn(now, total);
+                ev_seq[e] = next_seq;
+                ev_kind[e] = K_STEP;
+            }
+        }
+        __syncthreads();
+        const bool finish = misc[1] != 0;
+        __syncthreads();                                         // misc[1] is rewritten by the next step event
+        if (!finish) { ++next_seq; continue; }
+        // completion: release (sim.py:353-357), record, strict FIFO drain (sim.py:345-351)
+        {
+            const int i = ev_req[e];
+            const short2* hp = ev_hops + e * HMAX;
+            const long long tok = ev_tok[e];
+            const int tag = -(i + 1);
+            for (int h = tid; h < ev_nh[e]; h += NT) {
+                const int g = hp[h].x;
+                if (atomicExch(&stamp[g], tag) != tag) { atomicSub(&occ[g], 1); atomicAdd((unsigned long long*)&kv[g], (unsigned long long)(-tok)); }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                P.done_time[r0 + i] = now;
+                P.done_rank[r0 + i] = rank;
+                ev_kind[e] = 0xFF;
+            }
+            ++rank;
+            --live_n;
+            ++completed;
+            __syncthreads();
+            while (adm < ap) {
+                if (!try_admit(adm, now)) break;
+                ++adm;
+            }
+        }
+    }
+    // requests never completed keep the caller's NaN / -1 (done_time / done_rank are written on completion)
+    if (tid == 0) {
+        P.duration[dag] = now;
+        P.completed[dag] = completed;
+        P.queue_peak[dag] = peak;
+        P.n_events[dag] = events;
+        P.status[dag] = status;
+        P.aux[dag] = 0;
+    }
+}
+
 inline int align16s(int x) { return (x + 15) / 16 * 16; }
 
 }  // namespace
@@ -633,9 +870,24 @@ extern "C" int ss_sim_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const
     SimArgs P{gpu_ptr, base_tau, token_cap, rtt, pub_pow, exec_pow, pow_len, trace_ptr, arrival, prompt, output,
               publish_interval, amortize_rtt, done_time, done_rank, duration, completed, queue_peak, n_events,
               status, aux};
-    if (cudaFuncSetAttribute(sim_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B.total) != cudaSuccess)
-        return SS_CUDA_ERROR;
-    sim_warp_kernel<<<D.n_dags, 32, B.total, ss_stream(stream)>>>(D, A, B, P);
+    cudaStream_t st = ss_stream(stream);
+    auto run = [&](auto kern, int threads) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B.total) != cudaSuccess)
+            return SS_CUDA_ERROR;
+        kern<<<D.n_dags, threads, B.total, st>>>(D, A, B, P);
+        return SS_OK;
+    };
+    int rc;
+    switch ((D.max_hosts + 3) / 4) {                         // as ss_replay_warp: warps x source slots per lane
+        case 0: case 1: case 2: rc = run(sim_warp_kernel, 32); break;
+        case 3: rc = run(sim_mw_kernel<2, 3>, 64); break;
+        case 4: rc = run(sim_mw_kernel<2, 4>, 64); break;
+        case 5: rc = run(sim_mw_kernel<3, 5>, 96); break;
+        case 6: rc = run(sim_mw_kernel<3, 6>, 96); break;
+        case 7: rc = run(sim_mw_kernel<4, 7>, 128); break;
+        default: rc = run(sim_mw_kernel<4, 8>, 128); break;
+    }
+    if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
     return SS_OK;
 }

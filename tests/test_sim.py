@@ -127,3 +127,37 @@ def test_run_simulation_dropin_matches_reference(cuda_ready, sim_cases, name):
     rep = run_simulation(cl, model, plan, trace[::-1], amortize_rtt=c["amortize"],
                          contention_exponent=c["contention"])
     assert report_hex(rep.to_dict()) == c["report"]
+
+
+@pytest.mark.gpu
+def test_device_simulator_on_jittered_scenarios(cuda_ready):
+    """Jittered C2-shaped scenarios: the per-scenario RTT matrices come from ss_scenario_rtt on device; they must
+    equal ScenarioSet.scenario_rtt bit for bit, and each scenario's MetricsReport must match the oracle event loop."""
+    import torch
+    from paper_2509_26182_b200 import _native as N, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    d = alloc_ref.allocate(cl, model)
+    d["objective"] = d["objective"].hex()
+    d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+    plan = plan_from_golden(d)
+    S = 3
+    ss = scen.build_scenarios(cl, model, plan, S, seeds=[11, 12, 13], churn=0.0, jitter=True)
+    rp = ScenarioReplayer(ss, window=1, mode="warp")
+    G = ss.n_gpus
+    out = torch.empty(S * G * G, dtype=torch.float64, device="cuda")
+    N.check(N.lib().ss_scenario_rtt(S, G, N.ptr(rp.base_rtt), N.ptr(rp.seeds), N.ptr(out), None), "ss_scenario_rtt")
+    got = out.cpu().numpy().reshape(S, G, G)
+    for s in range(S):
+        assert np.array_equal(got[s], ss.scenario_rtt(s))
+    traces = [scen.generate_trace(120.0, 1.0, seed=s, prompt_tokens=(500, 20000), output_tokens=(8, 32))
+              for s in (11, 12, 13)]
+    reps = rp.simulate(traces)
+    for s in range(S):
+        tr = traces[s]
+        rep, lat, _ = sim_ref.simulate(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap,
+                                       list(zip(tr[0].tolist(), tr[1].tolist(), tr[2].tolist())))
+        mine = dict(reps[s])
+        assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
+        mine.pop("events")
+        assert report_hex(mine) == report_hex(rep), s
