@@ -1,17 +1,18 @@
 // Warp-resident replay: Phase-2 route / release(i - W) for DAGs whose layer
 // columns hold <= 32 hosts (C1 / C2 shapes).
 //
-// One warp owns one scenario for the whole launch.  Its edge blocks, host
+// One CTA owns one scenario for the whole launch.  Its edge blocks, host
 // columns, occupancy, release ring and backpointers are copied into shared
-// memory once; every request then runs without a single CTA barrier:
-//   * boundary b: lane j forms the candidates c_i + E_b[i][j] eight sources at a
-//     time (column costs broadcast from shared memory, independent loads and
-//     DADDs), then a tournament whose left operand always holds the lower source
-//     index and loses only to a strictly smaller right value == numpy first-index argmin
-//     (router.py:171); cost = (c_i + r_ij) + tau_j exactly (router.py:170-174);
+// memory once; every request then runs the chain DP on NWD warps:
+//   * <= 8 hosts (NWD = 1, warp_route): lane j forms the candidates c_i + E_b[i][j]
+//     eight sources at a time, then a tournament whose left operand always holds the
+//     lower source index and loses only to a strictly smaller right value == numpy
+//     first-index argmin (router.py:171); no CTA barrier;
+//   * 9..32 hosts (NWD = ceil(hosts / 8), mw_route in warp_dag.cuh): warps own eight
+//     destinations each, lanes split the sources four ways, one CTA barrier per boundary;
+//   * cost = (c_i + r_ij) + tau_j exactly (router.py:170-174);
 //   * load update as perfmap.py:353-382 with tau = base(g) * (1 + occ)^e
 //     (sim.py:182-183) and the distinct GPUs of each chain kept in the ring.
-// Latency per boundary: ceil(R_b / 8) groups of (loads, DADDs, 3-level tournament).
 #include <float.h>
 #include <stdio.h>
 #include <stdlib.h>

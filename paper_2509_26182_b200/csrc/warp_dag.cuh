@@ -1,8 +1,8 @@
 // Warp-resident DAG helpers shared by the warp replay, admission and simulator kernels.
 //
-// One warp owns one scenario: its host columns, node ids and edge blocks (the ss_dag_edges layout, <= 32
-// hosts per column) live in shared memory, and warp_route() runs one chain DP (router.py:163-197) without a
-// CTA barrier.
+// One CTA owns one scenario: its host columns, node ids and edge blocks (the ss_dag_edges layout, <= 32
+// hosts per column) live in shared memory.  warp_route() runs one chain DP (router.py:163-197) on a single
+// warp without a CTA barrier; mw_route() spreads the destinations over NWD warps (one barrier per boundary).
 #pragma once
 
 #include <float.h>
