@@ -1,7 +1,8 @@
 // Serving simulator on device (the admission path with occupancy-dependent step time).
 //
-// One warp runs one scenario's discrete-event simulation of pkg/src/swarmsched/sim.py:_Simulation (no
-// membership events), with the scenario's DAG warp-resident (<= 32 hosts per layer, warp_dag.cuh):
+// One warp (<= 8 hosts per layer) or a lockstep CTA of NWD warps (9..32 hosts, sim_mw_kernel) runs one scenario's
+// discrete-event simulation of pkg/src/swarmsched/sim.py:_Simulation (no membership events), with the scenario's
+// DAG resident in shared memory (warp_dag.cuh); ss_sim_cta covers wider pools with streamed edges:
 //   * events are ordered by (time, seq) exactly like the reference heap: arrivals take seq 0..n-1 in trace
 //     order, the first publish tick seq n, every later push the next number (sim.py:238-265);
 //   * a publish tick re-arms while work remains (sim.py:432-436) and changes nothing the router reads, but it
