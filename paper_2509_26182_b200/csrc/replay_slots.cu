@@ -547,7 +547,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
 #pragma unroll
             for (int d = 0; d < DPL; ++d) { v[d] = INF; ix[d] = PART_NONE; }
             const char* Tb = reinterpret_cast<const char*>(T + lane);
-#pragma unroll 2
+#pragma unroll 4
             for (int k = 0; k < n; k += 4) {
                 const double2 c01 = *reinterpret_cast<const double2*>(cw + k);
                 const double2 c23 = *reinterpret_cast<const double2*>(cw + k + 2);

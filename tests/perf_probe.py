@@ -30,9 +30,12 @@ def main():
     ap.add_argument("--mode", default="slots")
     ap.add_argument("--stage", type=int, default=0)
     ap.add_argument("--sbuf", type=int, default=0)
+    ap.add_argument("--lib", default="", help="alternative libswarmsched_b200.so (A/B builds)")
     args = ap.parse_args()
     import torch
     from paper_2509_26182_b200 import _native as N, scenarios as scen
+    if args.lib:
+        N.load_library(args.lib)
     from paper_2509_26182_b200.batched import ScenarioReplayer
     from helpers_golden import plan_from_golden
     from oracle import alloc_ref
