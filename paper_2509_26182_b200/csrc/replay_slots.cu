@@ -500,18 +500,24 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         pacc[k] += (unsigned long long)(_t - tp);                    \
         tp = _t;                                                     \
     }
+    auto issue_initial_rows = [&]() {
+        const BlkMeta m = bm[0];
+        const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
+        for (int u = warp; u < m.n_ins; u += NW) {
+            const int slot = ins[2 * (m.ins_start + u)];
+            const double* su = s0 + (int64_t)u * Wp;
+            for (int t = lane; t < tw; t += 32) cp_async8(T + slot * W + t, su + t);
+        }
+    };
     for (int r = 0; r < n_req; ++r) {
         const int64_t req = req0 + r;
         SS_PROF(4)
-        // apply(0): the initial frontier's rows, straight from L2 with cp.async (all copies in flight at once)
+        // apply(0): the initial frontier's rows, straight from L2 with cp.async (all copies in flight at once).
+        // From the second request on they were issued as soon as the previous request's last boundary had
+        // released T, so they land during that request's epilogue.
+        if (r == 0) issue_initial_rows();
         {
             const BlkMeta m = bm[0];
-            const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
-            for (int u = warp; u < m.n_ins; u += NW) {
-                const int slot = ins[2 * (m.ins_start + u)];
-                const double* su = s0 + (int64_t)u * Wp;
-                for (int t = lane; t < tw; t += 32) cp_async8(T + slot * W + t, su + t);
-            }
             for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
         }
         cp_async_wait_all();                                    // also lands the prefetched release slot
@@ -574,6 +580,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
             SS_PROF(3)
         }
 
+        if (r + 1 < n_req) issue_initial_rows();               // T is no longer read by this request
         // ---- last column: costs, argmin (first index), backtrack ----------------
         {
             const int rs = col_len[nblk];
