@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--c5-scenarios", type=int, default=4096, help="C5 scenarios per sub-pool (whole job)")
     ap.add_argument("--c5-steps", type=int, default=8)
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-admission", action="store_true")
     ap.add_argument("--no-sim", action="store_true")
@@ -320,6 +321,7 @@ def run_ours(args):
 
     c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
+    c1 = None if (args.no_c1 or rank != 0) else run_c1(args, stream)
     reb = None if args.no_rebalance else run_rebalance(args, rank, world, stream, barrier, reduce_max)
     adm = None if args.no_admission else run_admission(args, rank, world, stream, barrier, reduce_max)
     simr = None if args.no_sim else run_sim(args, rank, world, stream, barrier, reduce_max)
@@ -361,6 +363,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "phase1": p1,
             "c5": c5,
+            "c1": c1,
             "c2": c2,
             "rebalance": reb,
             "admission": adm,
@@ -596,6 +599,65 @@ def _sim_wide(args, rank, world, stream, barrier, reduce_max):
             "wall_ms": 1e3 * t, "kernel": "sim_cta_kernel (ss_sim_cta)",
             "workload": "C4 pool (k=%d), %d scenarios, Poisson traces at 60 req/s for 1.5 s"
                         % (plan.replication_count, len(seeds) * world)}
+
+
+def run_c1(args, stream):
+    """C1 (BASELINE configs[0]): L=32 over 8 GPUs -- one allocate() plus 1,000 routes with
+    accumulate semantics (W = inf, `cli route`), through the drop-in API a user calls (ChainRouter over a PerfMap)
+    and through the replay kernel; both checked against the reference's own 1,000 chains (router_replays.json)."""
+    import torch
+    from paper_2509_26182_b200 import ChainRouter, PerfMap, allocate, scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    cl, model = scen.synthetic_cluster(8, seed=0, model=scen.bench_model(32))
+    allocate(cl, model)
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        plan = allocate(cl, model)
+        ts.append(time.perf_counter() - t0)
+    by = {g.id: g for g in cl.gpus}
+    ids = sorted(by)
+    pm = PerfMap(ttl_s=4.5, latency_fn=lambda g, l, occ: model.flops_per_layer_per_token / by[g].flops * (1 + occ))
+    for g in ids:
+        pm.register_gpu(g)
+    pm.publish_link_rtts({(a, b): cl.rtt_s(a, b) for i, a in enumerate(ids) for b in ids[i + 1:]}, 0.0)
+    for g, sl in plan.gpu_slices().items():
+        pm.sync_gpu_layers(g, range(sl.start_layer, sl.end_layer + 1), 0.0)
+    router = ChainRouter(pm, model.layer_count)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    chains = [router.route(0.0) for _ in range(1000)]
+    t_dropin = time.perf_counter() - t0
+    ss = scen.build_scenarios(cl, model, plan, 1, churn=0.0, jitter=False)
+    rp = ScenarioReplayer(ss, window=-1, max_requests=1004, stream=stream)
+    with torch.cuda.stream(stream):
+        rp.run(4)
+        torch.cuda.synchronize()
+        rp.reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = rp.run(1000, gpus=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    rp.raise_first_failure()
+    t_replay = e0.elapsed_time(e1) / 1e3
+    res = {"metric": "C1: allocate() latency and 1,000-route throughput (one scenario, W = inf)",
+           "allocate_ms_median": 1e3 * sorted(ts)[len(ts) // 2], "k": plan.replication_count,
+           "dropin_routes_per_s": 1000 / t_dropin, "replay_sel_per_s": 1000 / t_replay, "replay_kernel": rp.mode}
+    gold = os.path.join(ROOT, "tests", "golden", "router_replays.json")
+    if os.path.exists(gold):
+        with open(gold) as fh:
+            want = json.load(fh)["c1"]["routes"]
+        pos = {g: i for i, g in enumerate(ids)}
+        dropin = [{"hops": [[pos[h.gpu_id], h.start_layer, h.end_layer] for h in c.hops], "cost": c.cost_s.hex()}
+                  for c in chains]
+        g_rows, costs = out.gpus.cpu().numpy()[0], out.cost.cpu().numpy()[0]
+        replay_ok = True
+        for r, w in enumerate(want):
+            layer_gpu = [h[0] for h in w["hops"] for _ in range(h[1], h[2] + 1)]
+            replay_ok &= g_rows[r].tolist() == layer_gpu and float(costs[r]).hex() == w["cost"]
+        res["matches_reference"] = {"dropin": dropin == want, "replay": bool(replay_ok), "routes": len(want)}
+    return res
 
 
 def run_c2(args, stream):
