@@ -148,11 +148,17 @@ def load_library(path: str = LIB_PATH):
         return lib
 
 
+_device_checked = False
+
+
 def lib():
-    """The loaded library, after checking that a CUDA device is usable."""
-    import torch
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("no CUDA device visible: the scheduler kernels need a B200 (sm_100a)")
+    """The loaded library, after checking (once) that a CUDA device is usable."""
+    global _device_checked
+    if not _device_checked:
+        import torch
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible: the scheduler kernels need a B200 (sm_100a)")
+        _device_checked = True
     return load_library()
 
 
@@ -169,5 +175,9 @@ def ptr(t) -> C.c_void_p:
 
 def stream_handle(stream=None) -> C.c_void_p:
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)    # the current stream without a Stream object
+    if raw is not None:
+        return C.c_void_p(raw(torch._C._cuda_getDevice()))
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
