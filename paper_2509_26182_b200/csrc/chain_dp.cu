@@ -61,6 +61,10 @@ struct Tiling {
 inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
 Tiling make_tiling(const ss_dag_set& D, bool replay, int cw) {
+    // A batch that cannot fill the GPU (one drop-in select_chain / route: a single DAG) gets one CTA per SM
+    // anyway, so it takes most of the SM's shared memory as TMA ring: more edge bytes in flight per boundary.
+    const bool small = D.n_dags <= 64;
+    const int budget = small ? 200 * 1024 : g_smem_budget;
     Tiling t{};
     t.rmaxp = 32 * cw;
     t.lmax = D.max_layers;
@@ -68,8 +72,8 @@ Tiling make_tiling(const ss_dag_set& D, bool replay, int cw) {
     const int fixed = 2 * 8 * 8 /*bars*/ + 2 * t.rmaxp * 8 + align_up(t.lmax * t.rmaxp, 16) +
                       align_up(t.lmax * 4, 16) + align_up(t.lmax * 16, 16) + align_up(t.lmax * 8, 16) +
                       t.gmax * 16 + 64 + cw * 16 + 256;
-    const int nbuf = g_nbuf;
-    int tile = (g_smem_budget - fixed) / nbuf / 128 * 128;
+    const int nbuf = small ? 8 : g_nbuf;
+    int tile = (budget - fixed) / nbuf / 128 * 128;
     const int max_block = align_up(t.rmaxp * t.rmaxp * 8 + 32, 128);
     if (tile > max_block) tile = max_block;
     const int min_tile = align_up(4 * t.rmaxp * 8 + 32, 128);     // at least 4 rows of the widest block

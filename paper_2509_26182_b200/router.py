@@ -349,7 +349,7 @@ class ChainRouter:
         c = self._cache
         excl = frozenset(exclude)
         if (c is not None and c.keys_version == keys_version and c.exclude == excl
-                and c.rtt_key == (pm._rtt_version, c.dag.gpu_ids()) and now <= self._valid_until
+                and c.rtt_key[0] == pm._rtt_version and now <= self._valid_until   # the cached DAG fixes the ids
                 and now - c.min_pub <= pm.ttl_s):
             return self._route_cached(c, dirty, now)
         snapshot = pm.snapshot(now)
