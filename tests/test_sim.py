@@ -161,3 +161,30 @@ def test_device_simulator_on_jittered_scenarios(cuda_ready):
         assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
         mine.pop("events")
         assert report_hex(mine) == report_hex(rep), s
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,L", [(24, 32), (36, 24), (48, 24)])
+def test_multiwarp_simulator_widths_vs_oracle(cuda_ready, n, L):
+    """sim_mw_kernel at 2 / 3 / 4 warps (12, 23, 30 hosts per column) vs the oracle event loop, report and
+    per-request latencies bit for bit (jittered RTT, KV pressure from long prompts)."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    cl, model = scen.synthetic_cluster(n, seed=0, model=scen.bench_model(L))
+    d = alloc_ref.allocate(cl, model)
+    d["objective"] = d["objective"].hex()
+    d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+    plan = plan_from_golden(d)
+    ss = scen.build_scenarios(cl, model, plan, 2, seeds=[5, 6], churn=0.0, jitter=True)
+    rp = ScenarioReplayer(ss, window=1, mode="warp")
+    traces = [scen.generate_trace(200.0, 0.8, seed=s, prompt_tokens=(1000, 40000), output_tokens=(4, 24))
+              for s in (5, 6)]
+    reps = rp.simulate(traces)
+    for s in range(2):
+        tr = traces[s]
+        rep, lat, _ = sim_ref.simulate(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap,
+                                       list(zip(tr[0].tolist(), tr[1].tolist(), tr[2].tolist())))
+        mine = dict(reps[s])
+        assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
+        mine.pop("events")
+        assert report_hex(mine) == report_hex(rep), s
