@@ -90,3 +90,30 @@ def test_device_admission_matches_reference(cuda_ready, admission_cases, name):
                     for i in range(case["steps"])]
         queue_left = [i for i in range(case["steps"]) if step[s, i] < 0]
         check(case, want, admitted, queue_left, kv[s], occ[s])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,L", [(24, 32), (36, 24), (48, 24)])
+def test_device_admission_widths_vs_oracle(cuda_ready, n, L):
+    """admission_warp_kernel at 2 / 3 / 4 warps (12, 23, 30 hosts per column) vs the oracle, under KV pressure."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    case = {"n": n, "L": L}
+    seeds, steps, window, lo, hi = [3, 4], 64, 12, 30000, 90000
+    ss = scenario_set(case, seeds)
+    rp = ScenarioReplayer(ss, window=window, mode="warp")
+    out = rp.admit(steps, tok_lo=lo, tok_hi=hi, gpus=True)
+    rp.raise_first_failure()
+    step, cost, gpus = out["step"].cpu().numpy(), out["cost"].cpu().numpy(), out["gpus"].cpu().numpy()
+    kv, occ = out["kv"].cpu().numpy(), out["occ"].cpu().numpy()
+    for s, seed in enumerate(seeds):
+        toks = [scen.request_tokens(seed, i, lo, hi) for i in range(steps)]
+        want_adm, want_q, want_kv, want_occ = admission_ref.admission_replay(
+            ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap, toks, steps, window,
+            chain_ref.occ_power_table(steps + 4))
+        got = [None if step[s, i] < 0 else (int(step[s, i]), gpus[s, i].tolist(), float(cost[s, i]))
+               for i in range(steps)]
+        assert got == want_adm, s
+        assert [i for i in range(steps) if step[s, i] < 0] == list(want_q)
+        assert [int(x) for x in kv[s]] == [int(x) for x in want_kv]
+        assert [int(x) for x in occ[s]] == [int(x) for x in want_occ]
