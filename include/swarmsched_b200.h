@@ -200,7 +200,7 @@ int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const doub
                       const double* occpow, int32_t occpow_len, const int64_t* seeds, int32_t tok_lo, int32_t tok_hi,
                       int32_t steps, int32_t window, int32_t* adm_gpus, int32_t* step_out, double* cost_out,
                       int16_t* gpus_out, int64_t* kv_out, int32_t* occ_out, int32_t* status, int32_t* aux,
-                      void* stream);
+                      const double* mat, int32_t mat_dim, void* stream);
 
 /* Serving simulator on device (sim.py:_Simulation without membership events):
  * one warp per scenario runs the discrete-event loop -- arrivals, KV-gated
@@ -240,10 +240,17 @@ int ss_sim_cta(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* bas
  * request path.  Same state / outputs / op script as ss_replay (ring entries
  * of a chain are stored in layer order).  ss_replay_warp_smem returns the
  * dynamic shared memory one scenario needs, or -1 when the DAG set does not
- * qualify (hosts > 32, or edges + ring exceed 227 KB). */
-int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len);
+ * qualify (hosts > 32, or edges + ring exceed 227 KB).
+ * Matrix mode (ss_replay_warp, ss_admission_warp; mat may be NULL): mat holds
+ * each scenario's RTT matrix [n_dags][mat_dim][mat_dim] over its pool GPUs
+ * (ss_scenario_rtt); when mat_dim^2 is smaller than the edge blocks the kernel
+ * stages the matrix instead and gathers E_b[i][j] = M[node_i][node_j] -- the
+ * same fp64 values in less shared memory, so more scenarios fit per SM.
+ * ss_sim_warp always offers its rtt input this way. */
+int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len, int32_t mat_dim);
 int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
-                   int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
+                   int32_t window, int32_t n_req, const ss_replay_out* out, const double* mat, int32_t mat_dim,
+                   void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Phase-1                                      */

@@ -70,7 +70,7 @@ _SIGS = {
                                   C.POINTER(ReplayOut), C.c_void_p]),
     "ss_set_slot_staging": (C.c_int, [C.c_int32, C.c_int32]),
     "ss_set_cover_parallel_limit": (C.c_int32, [C.c_int32]),
-    "ss_replay_warp_smem": (C.c_int64, [C.POINTER(DagSet), C.c_int32, C.c_int32]),
+    "ss_replay_warp_smem": (C.c_int64, [C.POINTER(DagSet), C.c_int32, C.c_int32, C.c_int32]),
     "ss_sim_warp": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                               C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -82,7 +82,7 @@ _SIGS = {
     "ss_admission_warp": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                     C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p]),
+                                    C.c_void_p, C.c_int32, C.c_void_p]),
     "ss_objective_pool": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                     C.c_double, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_ring_abort": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -96,7 +96,7 @@ _SIGS = {
                                          C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_replay_warp": (C.c_int, [C.POINTER(DagSet), C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
-                                 C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
+                                 C.c_int32, C.POINTER(ReplayOut), C.c_void_p, C.c_int32, C.c_void_p]),
 }
 
 class PoolSet(C.Structure):

@@ -63,7 +63,8 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
     s_cap = int(max(32, -(-int(held.max()) // 32) * 32))
     occ_len = window + 2 if window > 0 else (max_requests or 1 << 16) + 2
     probe = N.DagSet(scen.n_scenarios, int(cap.max()), L, scen.n_gpus, None, None, None, None, None, None, None)
-    warp_ok = int(cap.max()) <= 32 and int(N.load_library().ss_replay_warp_smem(probe, window, occ_len)) > 0
+    warp_ok = int(cap.max()) <= 32 and int(N.load_library().ss_replay_warp_smem(probe, window, occ_len,
+                                                                                scen.n_gpus)) > 0
     if mode == "auto":
         mode = "warp" if warp_ok else ("slots" if s_cap <= 96 else "blocks")
     if mode == "warp" and not warp_ok:
@@ -246,6 +247,25 @@ class ScenarioReplayer:
         self.ring.zero_()
         self.next_req.zero_()
 
+    def _scenario_mats(self):
+        """Per-scenario RTT matrices [S, G, G] on device (ScenarioSet.scenario_rtt), built once."""
+        torch = self.torch
+        if getattr(self, "_mats", None) is None:
+            S, G = self.S, self.G
+            if self.scen.jitter:
+                self._mats = torch.empty(S * G * G, dtype=torch.float64, device=self.dev)
+                N.check(N.lib().ss_scenario_rtt(S, G, N.ptr(self.base_rtt), N.ptr(self.seeds), N.ptr(self._mats),
+                                                N.stream_handle(self.stream)), "ss_scenario_rtt")
+            else:
+                self._mats = self.base_rtt.reshape(-1).repeat(S)
+        return self._mats
+
+    def _warp_mats(self):
+        """The matrices for the warp kernels' matrix mode, or None when the edge blocks are smaller."""
+        if self.G * self.G >= (self.L - 1) * self.max_hosts * self.max_hosts or self.S <= 148:
+            return None                                  # warp_layout would stage the edge blocks anyway
+        return self._scenario_mats()
+
     def run(self, n_req: int, *, cost: bool = True, hashes: bool = True, gpus: bool = False,
             out: Optional[ReplayResult] = None) -> ReplayResult:
         torch = self.torch
@@ -267,8 +287,10 @@ class ScenarioReplayer:
                                             self.occpow_len, self.window, n_req, ro, N.stream_handle(self.stream)),
                     "ss_replay_slots")
         elif self.mode == "warp":
+            mat = self._warp_mats()
             N.check(N.lib().ss_replay_warp(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window,
-                                           n_req, ro, N.stream_handle(self.stream)), "ss_replay_warp")
+                                           n_req, ro, N.ptr(mat), self.G, N.stream_handle(self.stream)),
+                    "ss_replay_warp")
         else:
             N.check(N.lib().ss_replay(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window, n_req,
                                       ro, N.stream_handle(self.stream)), "ss_replay")
@@ -531,7 +553,8 @@ class ScenarioReplayer:
                                           int(tok_lo), int(tok_hi), int(steps), self.window, N.ptr(adm),
                                           N.ptr(out["step"]), N.ptr(out["cost"]), N.ptr(out["gpus"]), N.ptr(out["kv"]),
                                           N.ptr(out["occ"]), N.ptr(self.status), N.ptr(self.aux),
-                                          N.stream_handle(self.stream)), "ss_admission_warp")
+                                          N.ptr(self._warp_mats()), self.G, N.stream_handle(self.stream)),
+                "ss_admission_warp")
         return out
 
     def simulate(self, traces, *, publish_interval: float = 1.5, amortize_rtt: bool = False,
@@ -575,12 +598,7 @@ class ScenarioReplayer:
         ptr_d, arr_d, pr_d, ou_d = up(ptr, torch.int32), up(arr, torch.float64), up(pr, torch.int32), up(ou, torch.int32)
         pub_d, exe_d = up(pub, torch.float64), up(exe, torch.float64)
         # per-scenario RTT matrices (scenario_rtt) built on device from the pool matrix and the jitter seeds
-        if self.scen.jitter:
-            rtt_d = torch.empty(S * G * G, dtype=torch.float64, device=self.dev)
-            N.check(N.lib().ss_scenario_rtt(S, G, N.ptr(self.base_rtt), N.ptr(self.seeds), N.ptr(rtt_d),
-                                            N.stream_handle(self.stream)), "ss_scenario_rtt")
-        else:
-            rtt_d = self.base_rtt.reshape(-1).repeat(S)
+        rtt_d = self._scenario_mats()
         fn = N.lib().ss_sim_warp if self.mode == "warp" else N.lib().ss_sim_cta
         N.check(fn(self.dag_set(), N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self._tokcap),
                                     N.ptr(rtt_d), N.ptr(pub_d), N.ptr(exe_d), pow_len, N.ptr(ptr_d), N.ptr(arr_d),

@@ -31,11 +31,12 @@ struct WarpReplay {
     int32_t window;
     int32_t n_req;
     unsigned long long* prof;   // diagnostics (env SS_WARP_PROF=1): cycles per phase, else NULL
+    const double* mat;          // matrix mode (A.mat_dim > 0): per-scenario RTT matrices [n_dags][dim][dim]
 };
 
 // NWD = 1: one warp owns the scenario (<= 8 hosts per column, warp_route).  NWD = 2..4: the destinations of
 // every boundary are spread over NWD warps (mw_route); the rest of the request stays on warp 0.
-template <int NWD, int SPL>
+template <int NWD, int SPL, bool MAT = false>
 __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -64,7 +65,9 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
     __shared__ int flag[3];
 
     // ---- one-time staging: columns, edges, per-GPU state, ring --------------
-    if (warp == 0) flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? 0 : 1;
+    if (warp == 0)
+        flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane,
+                            A.mat_dim ? R.mat + (int64_t)dag * A.mat_dim * A.mat_dim : nullptr) ? 0 : 1;
     __syncthreads();
     if (flag[0]) {
         if (tid == 0) R.st.status[dag] = SS_BAD_INPUT;
@@ -126,8 +129,8 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
         mark(0);
         // ---- DP over the layer columns + final argmin / backtrack ------------------
         double v;
-        if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
-        else v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+        if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
+        else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_dim);
         mark(1);
         if (tid == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         if (!(v <= DBL_MAX)) {
@@ -205,6 +208,7 @@ struct AdmissionArgs {
     int32_t* occ_out;
     int32_t* status;
     int32_t* aux;
+    const double* mat;          // matrix mode (A.mat_dim > 0): per-scenario RTT matrices
 };
 
 __device__ __forceinline__ long long request_tokens(uint64_t mix, int i, int lo, int hi) {
@@ -213,7 +217,7 @@ __device__ __forceinline__ long long request_tokens(uint64_t mix, int i, int lo,
 }
 
 // NWD as in replay_warp_kernel: the chain DP of every admission attempt spreads its destinations over NWD warps
-template <int NWD, int SPL>
+template <int NWD, int SPL, bool MAT = false>
 __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, WarpLayout A, AdmissionArgs Q) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -240,7 +244,9 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
     double* costs = reinterpret_cast<double*>(smem + A.off_cost);
     long long* kv = reinterpret_cast<long long*>(smem + A.off_kv);
     long long* tcap = reinterpret_cast<long long*>(smem + A.off_tcap);
-    if (warp == 0) flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? 0 : 1;
+    if (warp == 0)
+        flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane,
+                            A.mat_dim ? Q.mat + (int64_t)dag * A.mat_dim * A.mat_dim : nullptr) ? 0 : 1;
     __syncthreads();
     if (flag[0]) {
         if (tid == 0) Q.status[dag] = SS_BAD_INPUT;
@@ -296,8 +302,8 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
                 break;
             }
             double v;
-            if constexpr (NWD == 1) v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
-            else v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+            if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
+            else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_dim);
             if (!(v <= DBL_MAX)) break;                          // UncoveredLayer / NoPath: the head waits
             __syncthreads();
             // admit: reserve the tokens and +1 occupancy on the chain's distinct GPUs (sim.py:330-331)
@@ -349,22 +355,23 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
 
 }  // namespace
 
-extern "C" int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len) {
+extern "C" int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len, int32_t mat_dim) {
     if (!dags) return -1;
     WarpLayout A{};
-    return warp_layout(*dags, window, occpow_len < 1 ? 1 : occpow_len, A) ? A.total : -1;
+    return warp_layout(*dags, window, occpow_len < 1 ? 1 : occpow_len, A, mat_dim) ? A.total : -1;
 }
 
 extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow,
                               int32_t occpow_len, int32_t window, int32_t n_req, const ss_replay_out* out,
-                              void* stream_h) {
+                              const double* mat, int32_t mat_dim, void* stream_h) {
     if (!dags || !st || !occpow || occpow_len < 1 || n_req < 1) return SS_BAD_INPUT;
     const ss_dag_set& D = *dags;
     if (D.n_dags <= 0) return SS_OK;
     if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
     WarpLayout A{};
-    if (!warp_layout(D, window, occpow_len, A)) return SS_BAD_INPUT;
+    if (!warp_layout(D, window, occpow_len, A, mat ? mat_dim : 0)) return SS_BAD_INPUT;
     WarpReplay R{};
+    R.mat = mat;
     R.st = *st;
     if (out) R.out = *out;
     R.occpow = occpow;
@@ -385,14 +392,15 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
     };
     // destinations per boundary over ceil(hosts / 8) warps (latency: C2's 17 hosts -> 3 warps)
     int rc;
+    const bool mm = A.mat_dim > 0;                               // matrix mode: separate instantiations
     switch ((D.max_hosts + 3) / 4) {                             // source slots per lane
-        case 0: case 1: case 2: rc = run(replay_warp_kernel<1, 8>, 32); break;
-        case 3: rc = run(replay_warp_kernel<2, 3>, 64); break;
-        case 4: rc = run(replay_warp_kernel<2, 4>, 64); break;
-        case 5: rc = run(replay_warp_kernel<3, 5>, 96); break;
-        case 6: rc = run(replay_warp_kernel<3, 6>, 96); break;
-        case 7: rc = run(replay_warp_kernel<4, 7>, 128); break;
-        default: rc = run(replay_warp_kernel<4, 8>, 128); break;
+        case 0: case 1: case 2: rc = mm ? run(replay_warp_kernel<1, 8, true>, 32) : run(replay_warp_kernel<1, 8>, 32); break;
+        case 3: rc = mm ? run(replay_warp_kernel<2, 3, true>, 64) : run(replay_warp_kernel<2, 3>, 64); break;
+        case 4: rc = mm ? run(replay_warp_kernel<2, 4, true>, 64) : run(replay_warp_kernel<2, 4>, 64); break;
+        case 5: rc = mm ? run(replay_warp_kernel<3, 5, true>, 96) : run(replay_warp_kernel<3, 5>, 96); break;
+        case 6: rc = mm ? run(replay_warp_kernel<3, 6, true>, 96) : run(replay_warp_kernel<3, 6>, 96); break;
+        case 7: rc = mm ? run(replay_warp_kernel<4, 7, true>, 128) : run(replay_warp_kernel<4, 7>, 128); break;
+        default: rc = mm ? run(replay_warp_kernel<4, 8, true>, 128) : run(replay_warp_kernel<4, 8>, 128); break;
     }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();
@@ -412,7 +420,8 @@ extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr,
                                  const int64_t* token_cap, const double* occpow, int32_t occpow_len,
                                  const int64_t* seeds, int32_t tok_lo, int32_t tok_hi, int32_t steps, int32_t window,
                                  int32_t* adm_gpus, int32_t* step_out, double* cost_out, int16_t* gpus_out,
-                                 int64_t* kv_out, int32_t* occ_out, int32_t* status, int32_t* aux, void* stream_h) {
+                                 int64_t* kv_out, int32_t* occ_out, int32_t* status, int32_t* aux,
+                                 const double* mat, int32_t mat_dim, void* stream_h) {
     if (!dags || !gpu_ptr || !base_tau || !token_cap || !occpow || occpow_len < 1 || !seeds || !adm_gpus ||
         !step_out || !cost_out || !kv_out || !occ_out || !status || !aux)
         return SS_BAD_INPUT;
@@ -421,9 +430,9 @@ extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr,
     if (D.n_dags <= 0) return SS_OK;
     if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
     WarpLayout A{};
-    if (!warp_layout(D, 0, occpow_len, A)) return SS_BAD_INPUT;
+    if (!warp_layout(D, 0, occpow_len, A, mat ? mat_dim : 0)) return SS_BAD_INPUT;
     AdmissionArgs Q{gpu_ptr, base_tau, token_cap, occpow, occpow_len, seeds, tok_lo, tok_hi, steps, window,
-                    adm_gpus, step_out, cost_out, gpus_out, kv_out, occ_out, status, aux};
+                    adm_gpus, step_out, cost_out, gpus_out, kv_out, occ_out, status, aux, mat};
     cudaStream_t s = ss_stream(stream_h);
     auto run = [&](auto kern, int threads) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
@@ -432,14 +441,15 @@ extern "C" int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr,
         return SS_OK;
     };
     int rc;
+    const bool mm = A.mat_dim > 0;                               // matrix mode: separate instantiations
     switch ((D.max_hosts + 3) / 4) {                             // source slots per lane
-        case 0: case 1: case 2: rc = run(admission_warp_kernel<1, 8>, 32); break;
-        case 3: rc = run(admission_warp_kernel<2, 3>, 64); break;
-        case 4: rc = run(admission_warp_kernel<2, 4>, 64); break;
-        case 5: rc = run(admission_warp_kernel<3, 5>, 96); break;
-        case 6: rc = run(admission_warp_kernel<3, 6>, 96); break;
-        case 7: rc = run(admission_warp_kernel<4, 7>, 128); break;
-        default: rc = run(admission_warp_kernel<4, 8>, 128); break;
+        case 0: case 1: case 2: rc = mm ? run(admission_warp_kernel<1, 8, true>, 32) : run(admission_warp_kernel<1, 8>, 32); break;
+        case 3: rc = mm ? run(admission_warp_kernel<2, 3, true>, 64) : run(admission_warp_kernel<2, 3>, 64); break;
+        case 4: rc = mm ? run(admission_warp_kernel<2, 4, true>, 64) : run(admission_warp_kernel<2, 4>, 64); break;
+        case 5: rc = mm ? run(admission_warp_kernel<3, 5, true>, 96) : run(admission_warp_kernel<3, 5>, 96); break;
+        case 6: rc = mm ? run(admission_warp_kernel<3, 6, true>, 96) : run(admission_warp_kernel<3, 6>, 96); break;
+        case 7: rc = mm ? run(admission_warp_kernel<4, 7, true>, 128) : run(admission_warp_kernel<4, 7>, 128); break;
+        default: rc = mm ? run(admission_warp_kernel<4, 8, true>, 128) : run(admission_warp_kernel<4, 8>, 128); break;
     }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();

@@ -53,6 +53,7 @@ struct SimArgs {
     int32_t* status, *aux;
 };
 
+template <bool MAT = false>
 __global__ void __launch_bounds__(32) sim_warp_kernel(ss_dag_set D, WarpLayout A, SimLayout B, SimArgs P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int dag = blockIdx.x;
@@ -87,7 +88,8 @@ __global__ void __launch_bounds__(32) sim_warp_kernel(ss_dag_set D, WarpLayout A
     short2* ev_hops = reinterpret_cast<short2*>(smem + B.off_hops);     // [max_live][HMAX] (gpu, length)
     double* xpw = reinterpret_cast<double*>(smem + B.off_xpw);
 
-    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane)) {
+    if (!stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane,
+                   A.mat_dim ? P.rtt + (int64_t)dag * A.mat_dim * A.mat_dim : nullptr)) {
         if (lane == 0) P.status[dag] = SS_BAD_INPUT;
         return;
     }
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(32) sim_warp_kernel(ss_dag_set D, WarpLayout A
             tau[g] = tcap[g] - kv[g] < tok ? INF : base[g] * (o < B.pow_len ? ppw[o] : P.pub_pow[o]);  // KV-blocked excluded
         }
         __syncwarp();
-        const double v = warp_route(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane);
+        const double v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
         if (!(v <= DBL_MAX)) return false;
         // a free live slot (warp-uniform search)
         int slot = -1;
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(NT) sim_cta_kernel(ss_dag_set D, CtaLayout B, 
 // lockstep event loop of sim_cta_kernel over NWD warps, and the destination-split chain DP (mw_route) for
 // every admission attempt -- the route is most of a request's cost at C2 shape.
 // ---------------------------------------------------------------------------
-template <int NWD, int SPL>
+template <int NWD, int SPL, bool MAT = false>
 __global__ void __launch_bounds__(NWD * 32) sim_mw_kernel(ss_dag_set D, WarpLayout A, SimLayout B, SimArgs P) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -633,7 +635,9 @@ __global__ void __launch_bounds__(NWD * 32) sim_mw_kernel(ss_dag_set D, WarpLayo
     short2* ev_hops = reinterpret_cast<short2*>(smem + B.off_hops);
     double* xpw = reinterpret_cast<double*>(smem + B.off_xpw);
 
-    if (warp == 0) misc[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane) ? SS_OK : SS_BAD_INPUT;
+    if (warp == 0)
+        misc[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane,
+                            A.mat_dim ? P.rtt + (int64_t)dag * A.mat_dim * A.mat_dim : nullptr) ? SS_OK : SS_BAD_INPUT;
     __syncthreads();
     if (misc[0] != SS_OK) {
         if (tid == 0) P.status[dag] = SS_BAD_INPUT;
@@ -671,7 +675,8 @@ __global__ void __launch_bounds__(NWD * 32) sim_mw_kernel(ss_dag_set D, WarpLayo
             tau[g] = tcap[g] - kv[g] < tok ? INF : base[g] * (o < B.pow_len ? ppw[o] : P.pub_pow[o]);  // KV-blocked excluded
         }
         __syncthreads();
-        const double v = mw_route<NWD, SPL>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid);
+        const double v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare,
+                                                 tid, A.mat_dim);
         if (!(v <= DBL_MAX)) return false;
         int slot = -1;                                           // same result in every warp
         for (int e0 = 0; e0 < B.max_live && slot < 0; e0 += 32) {
@@ -846,7 +851,7 @@ extern "C" int ss_sim_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const
     if (D.n_dags <= 0) return SS_OK;
     if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
     WarpLayout A{};
-    if (!warp_layout(D, 0, pow_len, A)) return SS_BAD_INPUT;
+    if (!warp_layout(D, 0, pow_len, A, D.max_gpus)) return SS_BAD_INPUT;   // rtt doubles as matrix-mode input
     SimLayout B{};
     B.pow_len = A.pow_len;                                   // cached prefix (<= 256); longer tables stay global
     // as many live-chain entries as shared memory holds (a scenario that needs more reports SS_BAD_INPUT)
@@ -879,14 +884,15 @@ extern "C" int ss_sim_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const
         return SS_OK;
     };
     int rc;
+    const bool mm = A.mat_dim > 0;
     switch ((D.max_hosts + 3) / 4) {                         // as ss_replay_warp: warps x source slots per lane
-        case 0: case 1: case 2: rc = run(sim_warp_kernel, 32); break;
-        case 3: rc = run(sim_mw_kernel<2, 3>, 64); break;
-        case 4: rc = run(sim_mw_kernel<2, 4>, 64); break;
-        case 5: rc = run(sim_mw_kernel<3, 5>, 96); break;
-        case 6: rc = run(sim_mw_kernel<3, 6>, 96); break;
-        case 7: rc = run(sim_mw_kernel<4, 7>, 128); break;
-        default: rc = run(sim_mw_kernel<4, 8>, 128); break;
+        case 0: case 1: case 2: rc = mm ? run(sim_warp_kernel<true>, 32) : run(sim_warp_kernel<false>, 32); break;
+        case 3: rc = mm ? run(sim_mw_kernel<2, 3, true>, 64) : run(sim_mw_kernel<2, 3>, 64); break;
+        case 4: rc = mm ? run(sim_mw_kernel<2, 4, true>, 64) : run(sim_mw_kernel<2, 4>, 64); break;
+        case 5: rc = mm ? run(sim_mw_kernel<3, 5, true>, 96) : run(sim_mw_kernel<3, 5>, 96); break;
+        case 6: rc = mm ? run(sim_mw_kernel<3, 6, true>, 96) : run(sim_mw_kernel<3, 6>, 96); break;
+        case 7: rc = mm ? run(sim_mw_kernel<4, 7, true>, 128) : run(sim_mw_kernel<4, 7>, 128); break;
+        default: rc = mm ? run(sim_mw_kernel<4, 8, true>, 128) : run(sim_mw_kernel<4, 8>, 128); break;
     }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();

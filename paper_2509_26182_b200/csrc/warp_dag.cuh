@@ -16,6 +16,7 @@ constexpr unsigned FULL = 0xffffffffu;
 
 struct WarpLayout {
     int e_cap, ring_len, pow_len;
+    int mat_dim;       // > 0: the scenario's whole RTT matrix (mat_dim^2 fp64) replaces the edge blocks in E
     int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
         off_ring, off_pow, off_cost, off_kv, off_tcap, total;
 };
@@ -24,10 +25,13 @@ __device__ __forceinline__ void lexmin(double& v, int& i, double v2, int i2) {
     if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
 }
 
-// Stages one DAG's host columns and edge blocks into shared memory (compact, row-major per boundary).
-// Returns false (warp-uniform) when a column exceeds 32 hosts or the edges exceed the layout.
+// Stages one DAG's host columns and edge blocks into shared memory (compact, row-major per boundary), or --
+// matrix mode, A.mat_dim > 0 -- the scenario's RTT matrix `mat` (mat_dim x mat_dim, the values the edge blocks
+// are gathered from: E_b[i][j] = M[node_i][node_j]), which is smaller whenever the pool has fewer GPUs than
+// sqrt(sum of R_b R_{b+1}).  Returns false (warp-uniform) when a column exceeds 32 hosts or the edges exceed
+// the layout.
 __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l0, int nl, double* E, int* node, int* cl,
-                          int* noff, int* eoff, int lane) {
+                          int* noff, int* eoff, int lane, const double* mat = nullptr) {
     const int nblk = nl - 1;
     for (int l = lane; l < nl; l += 32) cl[l] = D.col_len[l0 + l];
     __syncwarp();
@@ -42,7 +46,7 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
                 e += cl[l] * cl[l + 1];
             }
         }
-        if (e > A.e_cap) bad = 1;
+        if (A.mat_dim == 0 && e > A.e_cap) bad = 1;
         cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
     }
     __syncwarp();
@@ -50,11 +54,15 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
     for (int l = 0; l < nl; ++l) {
         const int len = cl[l];
         if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
-        if (l < nblk) {
+        if (l < nblk && A.mat_dim == 0) {
             const double* src = D.edge_val + D.edge_off[l0 + l];
             const int cnt = len * cl[l + 1];
             for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
         }
+    }
+    if (A.mat_dim > 0) {
+        const int nn = A.mat_dim * A.mat_dim;
+        for (int q = lane; q < nn; q += 32) E[q] = mat[q];
     }
     __syncwarp();
     return true;
@@ -65,8 +73,10 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
 // (left operand = lower positions, loses only to a strictly smaller right value), groups merged in ascending
 // order with the same rule == numpy first-index argmin; cost = (c_i + r_ij) + tau_j.  Returns the chain cost
 // (+inf: no path); when finite, picks[l] (shared memory) holds the chosen position of every layer.
+template <bool MAT = false>
 __device__ inline double warp_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
-                             int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, int lane) {
+                             int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, int lane,
+                             int G = 0) {
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     double* cur = costs;                                     // 32 hosts + 8 pad for the group loop
     double* nxt = costs + 40;
@@ -76,8 +86,10 @@ __device__ inline double warp_route(const double* E, const int* node, const int*
     for (int b = 0; b < nblk; ++b) {
         const int rs = cl[b], rd = cl[b + 1];
         const bool act = lane < rd;
-        const double tdst = act ? tau[node[noff[b + 1] + lane]] : 0.0;
-        const double* ep = E + eoff[b] + lane;
+        const int dn = act ? node[noff[b + 1] + lane] : 0;
+        const double tdst = act ? tau[dn] : 0.0;
+        const double* ep = MAT ? E + dn : E + eoff[b] + lane;      // matrix mode: column dn, rows by source node
+        const int* sn = node + noff[b];
         double best = INF;
         int bi = 0;                                          // +inf everywhere -> 0 == np.argmin
         for (int g0 = 0; g0 < rs; g0 += 8) {
@@ -86,8 +98,8 @@ __device__ inline double warp_route(const double* E, const int* node, const int*
 #pragma unroll
             for (int q = 0; q < 8; q += 2) {
                 const double2 c2 = *reinterpret_cast<const double2*>(cur + g0 + q);
-                const double e0 = (act && g0 + q < rs) ? ep[q * rd] : INF;
-                const double e1 = (act && g0 + q + 1 < rs) ? ep[(q + 1) * rd] : INF;
+                const double e0 = (act && g0 + q < rs) ? (MAT ? ep[sn[g0 + q] * G] : ep[q * rd]) : INF;
+                const double e1 = (act && g0 + q + 1 < rs) ? (MAT ? ep[sn[g0 + q + 1] * G] : ep[(q + 1) * rd]) : INF;
                 a[q] = __dadd_rn(c2.x, e0);
                 a[q + 1] = __dadd_rn(c2.y, e1);
                 ix[q] = g0 + q;
@@ -101,7 +113,7 @@ __device__ inline double warp_route(const double* E, const int* node, const int*
                 }
             }
             if (a[0] < best) { best = a[0]; bi = ix[0]; }
-            ep += 8 * rd;
+            if (!MAT) ep += 8 * rd;
         }
         if (act) bp[b * 32 + lane] = (uint8_t)bi;
         c = act ? __dadd_rn(best, tdst) : INF;
@@ -131,16 +143,33 @@ __device__ inline double warp_route(const double* E, const int* node, const int*
 
 inline int align16(int x) { return (x + 15) / 16 * 16; }
 
-inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A) {
+// mat_dim > 0 offers matrix mode (the caller has per-scenario RTT matrices of that dimension).  It is taken
+// when the matrix is smaller than the edge blocks AND there are more scenarios than SMs: then the smaller
+// footprint puts more CTAs on each SM (C2-shaped batches: 2x replay throughput).  With one CTA per SM anyway
+// the gather M[node_i][node_j] only adds latency (single-scenario C2: 46.8e3 vs 63.2e3 sel/s), so the edge
+// blocks stay.
+inline int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+                cudaSuccess || n <= 0)
+            n = 148;
+    }
+    return n;
+}
+
+inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A, int mat_dim = 0) {
     if (D.max_hosts > 32 || D.max_layers < 1) return false;
     const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * D.max_hosts * D.max_hosts;
+    A.mat_dim = (mat_dim > 0 && (int64_t)mat_dim * mat_dim < e_cap && D.n_dags > sm_count()) ? mat_dim : 0;
     const int64_t ring_len = window > 0 ? (int64_t)window * (D.max_layers + 1) : 0;
     if (e_cap > (1 << 20) || ring_len > (1 << 20)) return false;
     A.e_cap = (int)e_cap;
     A.ring_len = (int)ring_len;
     A.pow_len = occpow_len < 256 ? occpow_len : 256;
     int o = 0;
-    A.off_E = o;      o += align16(A.e_cap * 8);
+    A.off_E = o;      o += align16((A.mat_dim ? A.mat_dim * A.mat_dim : A.e_cap) * 8);
     A.off_node = o;   o += align16(D.max_layers * D.max_hosts * 4);
     A.off_cl = o;     o += align16((D.max_layers + 1) * 4);
     A.off_noff = o;   o += align16(D.max_layers * 4);
@@ -174,27 +203,30 @@ struct MwBoundary {
     double td;
 };
 
-template <int SPL>
+template <int SPL, bool MAT>
 __device__ __forceinline__ void mw_fetch(MwBoundary& m, const double* E, const int* node, const int* cl,
-                                         const int* noff, const int* eoff, const double* tau, int b, int j, int q) {
+                                         const int* noff, const int* eoff, const double* tau, int b, int j, int q,
+                                         int G) {
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     m.rs = cl[b];
     m.rd = cl[b + 1];
     const bool act = j < m.rd;
-    const double* ep = E + eoff[b] + j;
+    const int dn = act ? node[noff[b + 1] + j] : 0;
+    const double* ep = MAT ? E + dn : E + eoff[b] + j;           // matrix mode: column dn, rows by source node
+    const int* sn = node + noff[b];
 #pragma unroll
     for (int k = 0; k < SPL; ++k) {
         const int i = q + 4 * k;
-        m.e[k] = (act && i < m.rs) ? ep[i * m.rd] : INF;
+        m.e[k] = (act && i < m.rs) ? (MAT ? ep[sn[i] * G] : ep[i * m.rd]) : INF;
     }
-    m.td = act ? tau[node[noff[b + 1] + j]] : 0.0;
+    m.td = act ? tau[dn] : 0.0;
 }
 
 // SPL = ceil(widest column / 4): source slots per lane (the tree and the prefetch shrink with the column)
-template <int NWD, int SPL>
+template <int NWD, int SPL, bool MAT = false>
 __device__ double mw_route(const double* E, const int* node, const int* cl, const int* noff, const int* eoff,
                            int nblk, const double* tau, double* costs, uint8_t* bp, int* picks, double* vshare,
-                           int tid) {
+                           int tid, int G = 0) {
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     constexpr int NT = NWD * 32;
     const int warp = tid >> 5, lane = tid & 31, d = lane & 7, q = lane >> 3;
@@ -204,7 +236,7 @@ __device__ double mw_route(const double* E, const int* node, const int* cl, cons
     double* nxt = costs + 40;
     for (int p = tid; p < 32; p += NT) cur[p] = p < cl[0] ? tau[node[p]] : INF;
     MwBoundary m;
-    if (nblk > 0) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, 0, j, q);
+    if (nblk > 0) mw_fetch<SPL, MAT>(m, E, node, cl, noff, eoff, tau, 0, j, q, G);
     __syncthreads();
     for (int b = 0; b < nblk; ++b) {
         double a[SPL];
@@ -234,7 +266,7 @@ __device__ double mw_route(const double* E, const int* node, const int* cl, cons
             nxt[j] = __dadd_rn(best, td);
         }
         // next boundary's operands: issued behind the shuffles (shared LSU queue), landing during the barrier
-        if (b + 1 < nblk) mw_fetch<SPL>(m, E, node, cl, noff, eoff, tau, b + 1, j, q);
+        if (b + 1 < nblk) mw_fetch<SPL, MAT>(m, E, node, cl, noff, eoff, tau, b + 1, j, q, G);
         __syncthreads();
         double* t = cur; cur = nxt; nxt = t;
     }

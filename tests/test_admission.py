@@ -117,3 +117,24 @@ def test_device_admission_widths_vs_oracle(cuda_ready, n, L):
         assert [i for i in range(steps) if step[s, i] < 0] == list(want_q)
         assert [int(x) for x in kv[s]] == [int(x) for x in want_kv]
         assert [int(x) for x in occ[s]] == [int(x) for x in want_occ]
+
+
+@pytest.mark.gpu
+def test_device_admission_matrix_mode_vs_oracle(cuda_ready):
+    """160 C2 scenarios (more than SMs -> matrix mode): a sample vs the oracle."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    seeds, steps, window, lo, hi = list(range(100, 260)), 48, 12, 30000, 90000
+    ss = scenario_set({"n": 64, "L": 64}, seeds)
+    rp = ScenarioReplayer(ss, window=window, mode="warp")
+    out = rp.admit(steps, tok_lo=lo, tok_hi=hi, gpus=True)
+    rp.raise_first_failure()
+    step, cost, gpus = out["step"].cpu().numpy(), out["cost"].cpu().numpy(), out["gpus"].cpu().numpy()
+    for s in range(0, len(seeds), 16):
+        toks = [scen.request_tokens(seeds[s], i, lo, hi) for i in range(steps)]
+        want_adm, want_q, _, _ = admission_ref.admission_replay(
+            ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap, toks, steps, window,
+            chain_ref.occ_power_table(steps + 4))
+        got = [None if step[s, i] < 0 else (int(step[s, i]), gpus[s, i].tolist(), float(cost[s, i]))
+               for i in range(steps)]
+        assert got == want_adm, s

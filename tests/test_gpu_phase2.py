@@ -302,3 +302,31 @@ def test_warp_replay_destination_split_widths_vs_oracle(cuda_ready, n, L, nwd):
         assert gpus[s].tolist() == want_g, s
         assert cost[s].tolist() == want_c, s
         assert rp.occ.view(S, -1)[s].cpu().numpy().tolist() == want_occ.tolist(), s
+
+
+def test_warp_matrix_mode_many_scenarios_vs_oracle(cuda_ready):
+    """More scenarios than SMs: the warp kernel stages each scenario's RTT matrix (ss_scenario_rtt) instead of its
+    edge blocks and gathers E_b[i][j] = M[node_i][node_j].  Every 10th of 160 churned + jittered C2 scenarios vs
+    the oracle, and all 160 against the edge-block run of the same scenarios in groups below the SM count."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from oracle import alloc_ref
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    plan = plan_from_golden(_plan_dict(alloc_ref.allocate(cl, model)))
+    S, n_req, W = 160, 24, 8
+    ss = scen.build_scenarios(cl, model, plan, S, seed0=2000, churn=0.05, jitter=True)
+    rp = ScenarioReplayer(ss, window=W, max_requests=n_req + 4, mode="warp")
+    assert rp._warp_mats() is not None                       # matrix mode offered and taken
+    out = rp.run(n_req, gpus=True)
+    rp.raise_first_failure()
+    gpus, cost = out.gpus.cpu().numpy(), out.cost.cpu().numpy()
+    for s in range(0, S, 10):
+        want_g, want_c, want_occ, _ = chain_ref.replay(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), n_req, W,
+                                                       chain_ref.occ_power_table(n_req + 4))
+        assert gpus[s].tolist() == want_g, s
+        assert cost[s].tolist() == want_c, s
+    half = scen.build_scenarios(cl, model, plan, 80, seed0=2000, churn=0.05, jitter=True)
+    rp2 = ScenarioReplayer(half, window=W, max_requests=n_req + 4, mode="warp")
+    assert rp2._warp_mats() is None                           # 80 <= SMs: edge blocks
+    out2 = rp2.run(n_req, gpus=True)
+    assert np.array_equal(out2.gpus.cpu().numpy(), gpus[:80]) and np.array_equal(out2.cost.cpu().numpy(), cost[:80])

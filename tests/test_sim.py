@@ -188,3 +188,29 @@ def test_multiwarp_simulator_widths_vs_oracle(cuda_ready, n, L):
         assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
         mine.pop("events")
         assert report_hex(mine) == report_hex(rep), s
+
+
+@pytest.mark.gpu
+def test_device_simulator_matrix_mode_vs_oracle(cuda_ready):
+    """160 jittered C2 scenarios (more than SMs -> the simulator stages each RTT matrix): a sample vs the oracle."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    cl, model = scen.synthetic_cluster(64, seed=0, model=scen.bench_model(64))
+    d = alloc_ref.allocate(cl, model)
+    d["objective"] = d["objective"].hex()
+    d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
+    plan = plan_from_golden(d)
+    S = 160
+    ss = scen.build_scenarios(cl, model, plan, S, seeds=list(range(S)), churn=0.0, jitter=True)
+    rp = ScenarioReplayer(ss, window=1, mode="warp")
+    traces = [scen.generate_trace(100.0, 0.6, seed=s, prompt_tokens=(500, 20000), output_tokens=(4, 24))
+              for s in range(S)]
+    reps = rp.simulate(traces)
+    for s in range(0, S, 40):
+        tr = traces[s]
+        rep, lat, _ = sim_ref.simulate(ss.columns(s), ss.base_tau, ss.scenario_rtt(s), ss.token_cap,
+                                       list(zip(tr[0].tolist(), tr[1].tolist(), tr[2].tolist())))
+        mine = dict(reps[s])
+        assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
+        mine.pop("events")
+        assert report_hex(mine) == report_hex(rep), s
