@@ -318,6 +318,16 @@ def run_ours(args):
                                      "fold per variant, global argmax (NCCL all-gather when N>1)",
                          "variants_per_gpu": V, "candidates_per_gpu": n_cand, "pools_with_errors": bad},
               "roofline": {"bound": "issue (integer/bitset DP)", "note": "not HBM-bound; see DESIGN.md"}}
+        # the north-star shape (64-layer model over 256 nodes): the same sweep, a harder constructive path
+        V64 = V
+        packed64, _ = _variants_for_rank(scen, V64, rank, world, layers=64)
+        with torch.cuda.stream(stream):
+            sw64 = VariantSweep(packed64, fill_all=True, stream=stream)
+            t64 = timed(sw64.run, 3, 1, stream, barrier, reduce_max)
+        p1["l64"] = {"value": packed64.n_candidates * world * 3 / t64, "unit": "candidates/s",
+                     "ms_per_step": 1e3 * t64 / 3, "variants_per_gpu": V64,
+                     "candidates_per_gpu": packed64.n_candidates,
+                     "workload": "synthetic_cluster(256, seed=v), L=64: the north star's 64-layer / 256-node shape"}
 
     c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
@@ -702,10 +712,10 @@ def run_c2(args, stream):
     return res
 
 
-def _variants_for_rank(scen, V, rank, world):
+def _variants_for_rank(scen, V, rank, world, layers=80):
     from paper_2509_26182_b200.batched import PackedVariants
     from paper_2509_26182_b200.distributed import shard
-    parts = [scen.bench_variants(1, 256, 80, seed0=int(v)) for v in shard(V, rank, world)]
+    parts = [scen.bench_variants(1, 256, layers, seed0=int(v)) for v in shard(V, rank, world)]
     pools, of, orr, meta, var_ptr = [], [], [], [], [0]
     for pk, mt in parts:
         pools += pk.pools
