@@ -6,6 +6,8 @@ Same names, fields and semantics as the reference for the pieces the hot path fe
   ``load_trace`` / ``save_trace`` (79-115, JSON lines ``{"id", "t", "prompt_tokens", "output_tokens"}``);
 * ``generate_trace`` (118-148): Poisson arrivals from ``random.Random(seed)``, ids ``r00000``...;
 * ``percentile`` (151-159, nearest rank) and ``MetricsReport`` (190-217);
+* ``baseline_plan`` (513-553): the naive placement the simulator is compared against (capacity-sorted first fit,
+  equal-speed water-fill through the device ``solve_lambda`` / ``hamilton_round``);
 * ``run_simulation`` (478-510): the discrete-event serving simulation of one cluster / plan / trace.  The event
   loop runs on the GPU (``ss_sim_warp`` for <= 32 hosts per layer, ``ss_sim_cta`` up to 256) through
   ``ScenarioReplayer.simulate``; this wrapper only packs the pool and unpacks the report.
@@ -24,10 +26,10 @@ from typing import Iterable, List, Sequence, Tuple
 
 import numpy as np
 
-from .errors import EmptySample
+from .errors import EmptySample, NoFeasiblePipeline
 from .perfmap import DEFAULT_PUBLISH_INTERVAL_S, DEFAULT_TTL_MULTIPLIER
-from .plan import AllocationPlan
-from .topology import ClusterSnapshot, ModelSpec
+from .plan import AllocationPlan, Pipeline
+from .topology import ClusterSnapshot, LayerSlice, ModelSpec, layer_capacity
 
 
 @dataclass(frozen=True)
@@ -146,3 +148,34 @@ def run_simulation(cluster: ClusterSnapshot, model: ModelSpec, plan: AllocationP
     rep = rp.simulate([arrays], publish_interval=float(publish_interval_s), amortize_rtt=bool(amortize_rtt),
                       contention=float(contention_exponent))[0]
     return MetricsReport(**{name: rep[name] for name in MetricsReport.__dataclass_fields__})
+
+
+def baseline_plan(cluster: ClusterSnapshot, model: ModelSpec) -> AllocationPlan:
+    """Naive placement (sim.py:513-553): GPUs by (-capacity, id) regardless of region, grouped first-fit until a
+    group can hold the model; each group's layers split by an equal-speed water-fill + Hamilton rounding; GPUs of
+    an unfinished last group stay unused.  objective 0.0, no per-k table."""
+    from .waterfill import hamilton_round, solve_lambda
+    L = model.layer_count
+    caps_of = {g.id: layer_capacity(g, model) for g in cluster.gpus}
+    usable = [g for g in sorted(cluster.gpus, key=lambda g: (-caps_of[g.id], g.id)) if caps_of[g.id] >= 1]
+    pipelines: List[Pipeline] = []
+    group: List[Tuple[str, int]] = []
+    acc = 0
+    for g in usable:
+        group.append((g.id, caps_of[g.id]))
+        acc += caps_of[g.id]
+        if acc < L:
+            continue
+        caps = [c for _, c in group]
+        rounded = hamilton_round(solve_lambda([1.0] * len(group), caps, L), caps, total=L)
+        stages, cursor = [], 1
+        for (gid, _), count in zip(group, rounded.layers):
+            stages.append(LayerSlice(gid, cursor, cursor + count - 1))
+            cursor += count
+        regions = {cluster.gpu(gid).region for gid, _ in group}
+        pipelines.append(Pipeline(stages=tuple(stages), region=regions.pop() if len(regions) == 1 else None))
+        group, acc = [], 0
+    if not pipelines:
+        raise NoFeasiblePipeline()
+    return AllocationPlan(replication_count=len(pipelines), pipelines=tuple(pipelines),
+                          stage_total=sum(p.stage_count for p in pipelines), objective_score=0.0, per_k_table=())

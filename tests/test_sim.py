@@ -214,3 +214,16 @@ def test_device_simulator_matrix_mode_vs_oracle(cuda_ready):
         assert [v.hex() for v in mine.pop("latencies")] == [v.hex() for v in lat], s
         mine.pop("events")
         assert report_hex(mine) == report_hex(rep), s
+
+
+@pytest.mark.gpu
+def test_baseline_plan_matches_reference(cuda_ready):
+    """sim.py:513-553 baseline_plan (water-fill and rounding on device) vs the reference's plans."""
+    from paper_2509_26182_b200 import baseline_plan, plan_to_dict, scenarios as scen
+    with open(os.path.join(HERE, "golden", "baseline_cases.json")) as fh:
+        cases = json.load(fh)
+    for name, c in cases.items():
+        cl, model = scen.synthetic_cluster(c["n"], seed=c["seed"], model=scen.bench_model(c["L"]))
+        d = plan_to_dict(baseline_plan(cl, model))
+        d["objective"] = float(d["objective"]).hex()
+        assert d == c["plan"], name
