@@ -84,3 +84,23 @@ def test_layer_load_helpers_known_values():
     assert layer_load_cov([2.0, 2.0, 2.0]) == 0.0
     assert math.isclose(layer_load_cov([1.0, 2.0, 3.0, 4.0]), math.sqrt(1.25) / 2.5, rel_tol=0, abs_tol=0)
     assert LayerLoad(3, 0.2, 0.6, 0.25).value == 0.25 * 0.2 + 0.75 * 0.6
+
+
+@pytest.mark.parametrize("name,kind", [("io_cluster_bench16.json", "cluster"), ("io_cluster_hand.json", "cluster"),
+                                       ("io_model_bench32.json", "model")])
+def test_cluster_and_model_files_round_trip_reference_text(tmp_path, name, kind):
+    """topology.py:180-288 file formats: reference-written files load through the drop-in and save back to the
+    same text (ms on disk, s in memory; asymmetric links and a custom cross-region RTT included)."""
+    from paper_2509_26182_b200 import load_cluster, load_model, save_cluster, save_model
+    src = os.path.join(os.path.dirname(__file__), "golden", name)
+    out = str(tmp_path / name)
+    if kind == "cluster":
+        snap = load_cluster(src)
+        save_cluster(snap, out)
+        if name == "io_cluster_hand.json":
+            assert snap.rtt_s("a", "b") == 0.0015 and snap.rtt_s("b", "a") == 0.0025
+            assert snap.rtt_s("c", "a") == 0.031 and snap.rtt_s("b", "c") == 0.042
+            assert snap.gpu("a").ram_token_capacity == 50_000 and snap.regions == frozenset({"east", "west"})
+    else:
+        save_model(load_model(src), out)
+    assert open(out).read() == open(src).read()
