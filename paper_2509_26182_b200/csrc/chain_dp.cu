@@ -55,12 +55,12 @@ struct SelectArgs {
 struct Tiling {
     int nbuf, tile_bytes, rmaxp, lmax, gmax;
     int off_full, off_empty, off_cost, off_bp, off_picks, off_blk, off_boff, off_tau, off_occ, off_stamp,
-        off_misc, off_red, total;
+        off_misc, off_red, off_part, total;
 };
 
 inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
-Tiling make_tiling(const ss_dag_set& D, bool replay, int cw) {
+Tiling make_tiling(const ss_dag_set& D, bool replay, int cw, int sg = 1) {
     // A batch that cannot fill the GPU (one drop-in select_chain / route: a single DAG) gets one CTA per SM
     // anyway, so it takes most of the SM's shared memory as TMA ring: more edge bytes in flight per boundary.
     const bool small = D.n_dags <= 64;
@@ -71,7 +71,7 @@ Tiling make_tiling(const ss_dag_set& D, bool replay, int cw) {
     t.gmax = replay ? D.max_gpus : 0;
     const int fixed = 2 * 8 * 8 /*bars*/ + 2 * t.rmaxp * 8 + align_up(t.lmax * t.rmaxp, 16) +
                       align_up(t.lmax * 4, 16) + align_up(t.lmax * 16, 16) + align_up(t.lmax * 8, 16) +
-                      t.gmax * 16 + 64 + cw * 16 + 256;
+                      t.gmax * 16 + 64 + cw * 16 + 256 + (sg > 1 ? sg * t.rmaxp * 12 + 16 : 0);
     const int nbuf = small ? 8 : g_nbuf;
     int tile = (budget - fixed) / nbuf / 128 * 128;
     const int max_block = align_up(t.rmaxp * t.rmaxp * 8 + 32, 128);
@@ -93,6 +93,7 @@ Tiling make_tiling(const ss_dag_set& D, bool replay, int cw) {
     t.off_stamp = o; o += t.gmax * 4;
     t.off_red = o;   o += align_up(cw * 16, 16);
     t.off_misc = o;  o += 64;
+    t.off_part = o;  o += sg > 1 ? align_up(sg * t.rmaxp * 12, 16) : 0;
     t.total = o;
     return t;
 }
@@ -114,11 +115,15 @@ __device__ __forceinline__ void lex_min(double& v, int& i, double v2, int i2) {
     if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
 }
 
-template <int CW, bool REPLAY>
-__global__ void __launch_bounds__((CW + 1) * 32)
+// SG > 1 (batches too small to fill the GPU: one DAG per SM, e.g. a drop-in select_chain / route): every
+// destination group is served by SG warps, each scanning every SG-th group of four source rows; their
+// (value, row) partials meet in shared memory and merge lexicographically (order-free) behind the boundary
+// barrier -- SG times less serial work per warp on the single-DAG latency path.
+template <int CW, bool REPLAY, int SG = 1>
+__global__ void __launch_bounds__((CW * SG + 1) * 32)
 chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int NC = CW * 32;                 // consumer threads
+    constexpr int NC = CW * SG * 32;            // consumer threads
     const int dag = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l0 = D.layer_ptr[dag];
@@ -148,7 +153,7 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
         if (nl < 1 || nl > T.lmax) misc[0] = SS_BAD_INPUT;
         for (int b = 0; b < T.nbuf; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&empty[b], CW);
+            mbar_init(&empty[b], CW * SG);
         }
         fence_mbar_init();
     }
@@ -196,7 +201,7 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
     // =========================================================================
     // producer warp
     // =========================================================================
-    if (warp == CW) {
+    if (warp == CW * SG) {
         if (lane == 0 && nblk > 0) {
             int64_t n = 0;
             for (int r = 0; r < n_req; ++r) {
@@ -240,7 +245,10 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
             stamp[g] = 0;
         }
     }
-    const int j = warp * 32 + lane;          // destination owned by this lane
+    const int dgrp = warp % CW, sgrp = warp / CW;
+    const int j = dgrp * 32 + lane;          // destination owned by this lane
+    double* part_v = reinterpret_cast<double*>(smem + T.off_part);          // [SG][rmaxp] source-group partials
+    int* part_i = reinterpret_cast<int*>(part_v + SG * T.rmaxp);
     int64_t consumed = 0;
     // after a failure the producer still issues every tile: acknowledge them all so
     // no bulk copy is in flight into this CTA's shared memory when it exits
@@ -312,9 +320,9 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
                 const int shift = (int)((base_start + (int64_t)row0 * bk.rd) & 1);
                 const double* tile = reinterpret_cast<const double*>(smem + (size_t)buf * T.tile_bytes) + shift + j;
                 if (active) {
-                    int q = 0;
-                    // rows in groups of 4 -> four independent (value, index) chains
-                    for (; q + 4 <= nr; q += 4) {
+                    int q = 4 * sgrp;
+                    // rows in groups of 4 -> four independent (value, index) chains; SG > 1: every SG-th group
+                    for (; q + 4 <= nr; q += 4 * SG) {
                         const int i = row0 + q;                       // multiple of 4: 16-B aligned pairs
                         const double2 c01 = *reinterpret_cast<const double2*>(cur + i);
                         const double2 c23 = *reinterpret_cast<const double2*>(cur + i + 2);
@@ -328,11 +336,12 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
                         if (a2 < v2) { v2 = a2; i2 = i + 2; }
                         if (a3 < v3) { v3 = a3; i3 = i + 3; }
                     }
-                    for (; q < nr; ++q) {
-                        const int i = row0 + q;
-                        const double a = __dadd_rn(cur[i], tile[q * bk.rd]);
-                        if (a < v0) { v0 = a; i0 = i; }
-                    }
+                    if (q < nr)                              // the tail group (< 4 rows) belongs to its group's warp
+                        for (; q < nr; ++q) {
+                            const int i = row0 + q;
+                            const double a = __dadd_rn(cur[i], tile[q * bk.rd]);
+                            if (a < v0) { v0 = a; i0 = i; }
+                        }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[buf]);
@@ -342,6 +351,15 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
                 lex_min(v0, i0, v1, i1);
                 lex_min(v0, i0, v2, i2);
                 lex_min(v0, i0, v3, i3);
+            }
+            if constexpr (SG > 1) {
+                if (active) { part_v[sgrp * T.rmaxp + j] = v0; part_i[sgrp * T.rmaxp + j] = i0; }
+                consumer_sync(NC);
+                if (sgrp == 0 && active)
+#pragma unroll
+                    for (int g = 1; g < SG; ++g) lex_min(v0, i0, part_v[g * T.rmaxp + j], part_i[g * T.rmaxp + j]);
+            }
+            if (active && sgrp == 0) {
                 if (i0 == IDX_NONE) i0 = 0;                 // all-inf column: numpy argmin -> 0
                 if constexpr (REPLAY) tau_dst = tau_g[g_dst];
                 nxt[j] = __dadd_rn(v0, tau_dst);
@@ -356,14 +374,14 @@ chain_dp_kernel(ss_dag_set D, Tiling T, ReplayArgs R, SelectArgs S) {
             const int len = D.col_len[l0 + nl - 1];
             double v = __longlong_as_double(0x7ff0000000000000ll);
             int idx = IDX_NONE;
-            if (j < len) { v = cur[j]; idx = j; }
+            if (j < len && sgrp == 0) { v = cur[j]; idx = j; }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
                 const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
                 lex_min(v, idx, v2, i2);
             }
-            if (lane == 0) { red_v[warp] = v; red_i[warp] = idx; }
+            if (lane == 0 && sgrp == 0) { red_v[dgrp] = v; red_i[dgrp] = idx; }
         }
         consumer_sync(NC);
         if (tid == 0) {
@@ -437,7 +455,9 @@ int launch(const ss_dag_set& D, const ReplayArgs& R, const SelectArgs& S, cudaSt
         return SS_BAD_INPUT;
     if (REPLAY && (D.max_gpus < 1 || D.max_gpus > SS_MAX_GPUS)) return SS_BAD_INPUT;
     const int cw = (D.max_hosts + 31) / 32;
-    Tiling T = make_tiling(D, REPLAY, cw);
+    // fewer DAGs than SMs: each DAG's CTA is alone on its SM, so split the sources over 4 warp groups
+    const int sg = D.n_dags <= 64 && cw <= 4 ? 4 : 1;
+    Tiling T = make_tiling(D, REPLAY, cw, sg);
     if (T.total > 227 * 1024) return SS_BAD_INPUT;
     auto run = [&](auto kern, int threads) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T.total) != cudaSuccess)
@@ -446,6 +466,14 @@ int launch(const ss_dag_set& D, const ReplayArgs& R, const SelectArgs& S, cudaSt
         SS_CHECK_LAUNCH();
         return SS_OK;
     };
+    if (sg == 4) {
+        switch (cw) {
+            case 1: return run(chain_dp_kernel<1, REPLAY, 4>, 5 * 32);
+            case 2: return run(chain_dp_kernel<2, REPLAY, 4>, 9 * 32);
+            case 3: return run(chain_dp_kernel<3, REPLAY, 4>, 13 * 32);
+            default: return run(chain_dp_kernel<4, REPLAY, 4>, 17 * 32);
+        }
+    }
     switch (cw) {
         case 1: return run(chain_dp_kernel<1, REPLAY>, 64);
         case 2: return run(chain_dp_kernel<2, REPLAY>, 96);
