@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--c5-steps", type=int, default=8)
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
+    ap.add_argument("--full-c4", action="store_true",
+                    help="also run the whole configs[3] job: 10k scenarios x 10k requests, sharded over the ranks")
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-admission", action="store_true")
     ap.add_argument("--no-sim", action="store_true")
@@ -332,6 +334,7 @@ def run_ours(args):
     c5 = None if args.no_c5 else run_c5(args, rank, world, stream, barrier, reduce_max)
     c2 = None if (args.no_c2 or rank != 0) else run_c2(args, stream)
     c1 = None if (args.no_c1 or rank != 0) else run_c1(args, stream)
+    c4_full = run_full_c4(args, rank, world, stream, barrier, reduce_max) if args.full_c4 else None
     reb = None if args.no_rebalance else run_rebalance(args, rank, world, stream, barrier, reduce_max)
     adm = None if args.no_admission else run_admission(args, rank, world, stream, barrier, reduce_max)
     simr = None if args.no_sim else run_sim(args, rank, world, stream, barrier, reduce_max)
@@ -374,6 +377,7 @@ def run_ours(args):
             "phase1": p1,
             "c5": c5,
             "c1": c1,
+            "c4_full": c4_full,
             "c2": c2,
             "rebalance": reb,
             "admission": adm,
@@ -609,6 +613,37 @@ def _sim_wide(args, rank, world, stream, barrier, reduce_max):
             "wall_ms": 1e3 * t, "kernel": "sim_cta_kernel (ss_sim_cta)",
             "workload": "C4 pool (k=%d), %d scenarios, Poisson traces at 60 req/s for 1.5 s"
                         % (plan.replication_count, len(seeds) * world)}
+
+
+def run_full_c4(args, rank, world, stream, barrier, reduce_max):
+    """BASELINE configs[3] as a whole job: 10,000 churn+jitter C4 scenario states x 10,000 requests each (10^8
+    chain selections, W=64), scenario s on rank s mod world, timed on the device as the max over ranks."""
+    import torch
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    n_scen, n_req, chunk = 10_000, 10_000, 100
+    cl, model, plan = base_pool()
+    mine = np.arange(rank, n_scen, world, dtype=np.int64)
+    ss = scen.build_scenarios(cl, model, plan, len(mine), churn=0.05, jitter=True, seeds=mine, host_events=False)
+    with torch.cuda.stream(stream):
+        rp = ScenarioReplayer(ss, window=args.window, stream=stream, mode=args.mode)
+        rp.build()
+        out = rp.run(chunk)
+        torch.cuda.synchronize()
+        rp.reset()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_req // chunk):
+            rp.run(chunk, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    rp.raise_first_failure()
+    t = reduce_max(e0.elapsed_time(e1) / 1e3)
+    return {"metric": "configs[3] whole job: chain selections/sec", "value": n_scen * n_req / t,
+            "unit": "selections/s", "seconds": t, "scenarios": n_scen, "requests_per_scenario": n_req,
+            "scenarios_per_rank": int(len(mine)), "kernel": rp.mode,
+            "note": "10^8 selections; requests of a scenario stay serial (W=64 feedback), launches of %d" % chunk}
 
 
 def run_c1(args, stream):
