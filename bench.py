@@ -63,10 +63,12 @@ def parse():
                     help="Phase-2 kernel of the headline value (the other one is reported as phase2_alt)")
     ap.add_argument("--no-alt", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
-    ap.add_argument("--c5-scenarios", type=int, default=4096, help="C5 scenarios per sub-pool (whole job)")
+    ap.add_argument("--c5-scenarios", type=int, default=4096, help="C5 scenarios per sub-pool per rank")
     ap.add_argument("--c5-steps", type=int, default=8)
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
+    ap.add_argument("--full-c5", action="store_true",
+                    help="run C5 as the whole configs[4] job: 4,096 requests per scenario (default: --c5-steps launches)")
     ap.add_argument("--full-c4", action="store_true",
                     help="also run the whole configs[3] job: 10k scenarios x 10k requests, sharded over the ranks")
     ap.add_argument("--no-rebalance", action="store_true")
@@ -399,7 +401,9 @@ def run_c5(args, rank, world, stream, barrier, reduce_max):
     from paper_2509_26182_b200.distributed import shard
     R, W = args.requests_per_step, args.window
     pools = scen.c5_pools(0)
-    seeds = shard(args.c5_scenarios, rank, world)
+    # default: --c5-scenarios per rank (weak scaling); --full-c5: the fixed configs[4] job, 4,096 scenarios per
+    # sub-pool in total, scenario s on rank s mod world (strong scaling)
+    seeds = np.arange(rank, 4096, world, dtype=np.int64) if args.full_c5 else shard(args.c5_scenarios, rank, world)
     with torch.cuda.stream(stream):
         torch.cuda.synchronize()
         barrier()
@@ -424,11 +428,13 @@ def run_c5(args, rank, world, stream, barrier, reduce_max):
         def step():
             for rp, out in zip(reps, outs):
                 rp.run(R, out=out)
-        t = timed(step, args.c5_steps, args.warmup, stream, barrier, reduce_max)
-    sel = len(seeds) * R * len(reps) * world * args.c5_steps
+        c5_steps = 4096 // R if args.full_c5 else args.c5_steps
+        t = timed(step, c5_steps, args.warmup, stream, barrier, reduce_max)
+    sel = len(seeds) * R * len(reps) * world * c5_steps
     res = {"metric": "C5 two-phase schedule: Phase-2 chain selections/sec (whole job)", "value": sel / t,
-           "unit": "selections/s", "ms_per_step": 1e3 * t / args.c5_steps,
+           "unit": "selections/s", "ms_per_step": 1e3 * t / c5_steps, "requests_per_scenario": R * c5_steps,
            "phase1_ms": 1e3 * t_p1, "scenario_build_ms": 1e3 * t_build,
+           "schedule_seconds": t_p1 + t_build + t,
            "config": {"workload": "C5: 1,024 GPUs in 8 regions (explicit region RTT matrix, intra 1 ms, inter "
                                   "U(5,80) ms) split 256/384/384 into 8B (L=32) / 32B (L=64) / 70B (L=80) "
                                   "sub-pools; device allocate() per sub-pool; %d churn+jitter scenarios per "
