@@ -185,7 +185,8 @@ int ss_ring_abort(int32_t n_scen, int32_t n_gpus, int32_t max_layers, int32_t wi
                   void* stream);
 
 /* Admission path (sim.py:319-366) per scenario on a time-free step schedule,
- * for DAGs with <= 32 hosts per layer (one warp per scenario, edges resident):
+ * for DAGs with <= 32 hosts per layer (one CTA of 1-4 warps per scenario, edges
+ * or the scenario's RTT matrix resident; matrix mode as for ss_replay_warp):
  * at step t the requests admitted at step t - W complete (occupancy -1 and
  * tokens released on their distinct GPUs), request t joins the queue, and the
  * queue drains strictly FIFO: the head (tokens uniform in [tok_lo, tok_hi]
@@ -203,7 +204,8 @@ int ss_admission_warp(const ss_dag_set* dags, const int32_t* gpu_ptr, const doub
                       const double* mat, int32_t mat_dim, void* stream);
 
 /* Serving simulator on device (sim.py:_Simulation without membership events):
- * one warp per scenario runs the discrete-event loop -- arrivals, KV-gated
+ * one warp (<= 8 hosts) or a lockstep CTA of up to 4 warps (<= 32 hosts) per
+ * scenario runs the discrete-event loop -- arrivals, KV-gated
  * strict-FIFO admission (route with KV-blocked GPUs excluded), prefill and
  * decode steps with occupancy-dependent duration, completions, publish ticks --
  * in the reference's (time, seq) order, on a warp-resident DAG (<= 32 hosts per
@@ -235,8 +237,9 @@ int ss_sim_cta(const ss_dag_set* dags, const int32_t* gpu_ptr, const double* bas
                int32_t* aux, void* stream);
 
 /* Warp-resident replay for DAGs whose columns hold <= 32 hosts (C1/C2 shapes):
- * one warp per scenario with its edge blocks (the ss_dag_edges layout), ring
- * and state staged in shared memory once per launch; no CTA barriers on the
+ * one CTA of 1-4 warps per scenario with its edge blocks (the ss_dag_edges
+ * layout), ring and state staged in shared memory once per launch; one CTA
+ * barrier per layer boundary when the destinations span warps (none for one warp) on the
  * request path.  Same state / outputs / op script as ss_replay (ring entries
  * of a chain are stored in layer order).  ss_replay_warp_smem returns the
  * dynamic shared memory one scenario needs, or -1 when the DAG set does not
