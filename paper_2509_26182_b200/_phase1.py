@@ -103,7 +103,11 @@ class PoolBatch:
         self.n_cover = int(cand_pool.size)
         self.n_cand = int(all_pool.size)
         ints = np.concatenate([pool_ptr, caps, A.layers, km, exact, cand_pool, cand_k, all_pool,
-                               all_k]).astype(np.int32)
+                               all_k])
+        if ints.size and (int(ints.max()) > np.iinfo(np.int32).max or int(ints.min()) < np.iinfo(np.int32).min):
+            raise ValueError("layer capacities, k_max or pool sizes exceed the device path's int32 range "
+                             f"(max {int(ints.max())}); a capacity this large means bytes_per_layer is tiny")
+        ints = ints.astype(np.int32)
         self._ints = torch.from_numpy(ints).to(dev)
         o = 0
 

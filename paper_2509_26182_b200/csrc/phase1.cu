@@ -91,7 +91,7 @@ __device__ int hamilton(const double* t, const int* tint, const int* cap, int n,
     int order[NMAX];
     double rem[NMAX];
     for (int i = 0; i < n; ++i) {
-        rem[i] = tint[i] ? 0.0 : __dsub_rn(t[i], (double)out[i]);
+        rem[i] = __dsub_rn(t[i], (double)out[i]);     // t - min(floor(t), c): positive for an int t above its cap
         int j = i;
         while (j > 0 && rem[order[j - 1]] < rem[i]) { order[j] = order[j - 1]; --j; }
         order[j] = i;

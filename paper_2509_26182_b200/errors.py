@@ -112,11 +112,11 @@ SS_WORKSPACE = 10
 SS_ZERO_CAPACITY = 11
 
 
-def raise_for_status(code: int, aux: int = 0, *, names=None, detail: str = "") -> None:
+def raise_for_status(code: int, aux: int = 0, *, names=None, detail: str = "", layer_count: int = -1) -> None:
     """Raise the reference exception matching a device status code.
 
     ``names`` maps an aux node index back to a gpu id when the status carries
-    one (OCC_UNDERFLOW, ZERO_CAPACITY).
+    one (OCC_UNDERFLOW, ZERO_CAPACITY); ``layer_count`` completes InfeasibleCapacity(total_cap, layer_count).
     """
     code = int(code)
     if code == SS_OK:
@@ -130,7 +130,7 @@ def raise_for_status(code: int, aux: int = 0, *, names=None, detail: str = "") -
     if code == SS_NO_FEASIBLE_PIPELINE:
         raise NoFeasiblePipeline(detail or "no feasible pipeline")
     if code == SS_INFEASIBLE_CAPACITY:
-        raise InfeasibleCapacity(int(aux), -1)
+        raise InfeasibleCapacity(int(aux), int(layer_count))
     if code == SS_ROUNDING_OVERFLOW:
         raise RoundingOverflow(detail or "rounding overflow")
     if code == SS_DEGENERATE_OBJECTIVE:

@@ -299,7 +299,7 @@ class _RouteCache:
     """A device DAG kept across routes while the perf map's tau key set, the exclude set and the RTT table are
     unchanged and no entry can have expired: only republished tau values move, host mirror -> device."""
 
-    def __init__(self, keys_version, exclude, rtt_key, min_pub, dag, ddag, index, edges, tau_h, nodes_of):
+    def __init__(self, keys_version, exclude, rtt_key, min_pub, dag, ddag, index, edges, tau_h, nodes_of, hidden):
         self.keys_version = keys_version
         self.exclude = exclude
         self.rtt_key = rtt_key
@@ -310,6 +310,7 @@ class _RouteCache:
         self.edges = edges
         self.tau_h = tau_h              # host mirror of ddag.node_tau
         self.nodes_of = nodes_of        # gpu -> [(node position, layer)]
+        self.hidden = hidden            # GPUs with a tau entry (layers 1..L) left out of the DAG as expired
 
 
 class ChainRouter:
@@ -331,6 +332,7 @@ class ChainRouter:
         self._index: Dict[str, int] = {}
         self._valid_until = -math.inf
         self._cache: Optional[_RouteCache] = None
+        self._tau_seen = 0              # this router's read position in the perf map's tau write log
 
     def _matrix_for(self, snapshot: PerfSnapshot, gpu_ids: Tuple[str, ...]):
         key = (snapshot.rtt_version, gpu_ids)
@@ -345,12 +347,15 @@ class ChainRouter:
 
     def route(self, now: float, *, exclude: AbstractSet[str] = _EMPTY) -> PipelineChain:
         pm = self.perf_map
-        keys_version, dirty = pm._drain_tau_updates()
+        keys_version, seq, dirty = pm._tau_updates_since(self._tau_seen)
+        self._tau_seen = seq
         c = self._cache
         excl = frozenset(exclude)
-        if (c is not None and c.keys_version == keys_version and c.exclude == excl
+        # an entry that was expired when the DAG was built and has since been republished under the same key
+        # changes the live key set without changing the key-set version: rebuild
+        if (c is not None and dirty is not None and c.keys_version == keys_version and c.exclude == excl
                 and c.rtt_key[0] == pm._rtt_version and now <= self._valid_until   # the cached DAG fixes the ids
-                and now - c.min_pub <= pm.ttl_s):
+                and now - c.min_pub <= pm.ttl_s and not (c.hidden and dirty & c.hidden)):
             return self._route_cached(c, dirty, now)
         snapshot = pm.snapshot(now)
         dag = build_dag(snapshot, self.layer_count, exclude=exclude)
@@ -360,9 +365,11 @@ class ChainRouter:
         ddag = _pack_dag(dag, index)
         picks, cost, status, edges = _select_on_device(ddag, matrix, len(ids))
         chain = self._finish(dag, picks, cost, status, edges)
+        L = self.layer_count
         with pm._lock:
             min_pub = min((pm._tau[(g, l + 1)].published_at for l, col in enumerate(dag.hosts) for g in col),
                           default=math.inf)
+            hidden = {g for (g, l), e in pm._tau.items() if 1 <= l <= L and e.expired(now)}
         nodes_of: Dict[str, list] = {}
         pos = 0
         for l, col in enumerate(dag.hosts):
@@ -372,7 +379,7 @@ class ChainRouter:
         tau_h = np.array([dag.latencies[(g, l + 1)] for l, col in enumerate(dag.hosts) for g in col],
                          dtype=np.float64)
         self._cache = _RouteCache(keys_version, excl, (pm._rtt_version, ids), min_pub, dag, ddag, index, edges,
-                                  tau_h, nodes_of)
+                                  tau_h, nodes_of, frozenset(hidden))
         pm.on_chain_event(chain, "select", now)
         return chain
 

@@ -31,6 +31,17 @@ class IntegerAllocation:
     layers: tuple
 
 
+# one device water-fill group holds at most this many entries (phase1.cu NMAX: per-thread arrays); the reference
+# accepts any length, but a pipeline never has more stages than its region has usable GPUs (<= 256 on the device
+# path's constructive cover as well) -- documented in DESIGN.md "Limits of the device path"
+MAX_ENTRIES = 256
+
+
+def _check_len(n, what):
+    if n > MAX_ENTRIES:
+        raise ValueError(f"{what}: the device water-fill takes at most {MAX_ENTRIES} entries per call, got {n}")
+
+
 def _dev():
     import torch
     return torch, torch.device("cuda")
@@ -39,6 +50,7 @@ def _dev():
 def _run_waterfill(flops, caps, layer_count, mode):
     torch, dev = _dev()
     n = len(caps)
+    _check_len(n, ("solve_lambda", "", "rebalance_pipeline")[mode] or "water-fill")
     ints = torch.tensor([0, n, layer_count] + [int(c) for c in caps], dtype=torch.int32, device=dev)
     fl = torch.tensor([float(f) for f in flops], dtype=torch.float64, device=dev)
     targets = torch.zeros(n, dtype=torch.float64, device=dev)
@@ -86,6 +98,7 @@ def hamilton_round(frac: FractionalAllocation, capacities: Sequence[int], total:
         raise ValueError("targets and capacities must be equal-length")
     torch, dev = _dev()
     n = len(targets)
+    _check_len(n, "hamilton_round")
     ints = torch.tensor([0, n, -1 if total is None else int(total)] + [int(c) for c in capacities] +
                         [1 if isinstance(t, int) else 0 for t in targets], dtype=torch.int32, device=dev)
     tv = torch.tensor([float(t) for t in targets], dtype=torch.float64, device=dev)

@@ -66,5 +66,30 @@ def test_cached_routes_equal_fresh_selection(cuda_ready):
     pm.publish_link_rtts(rtt, 2.3)
     route(2.45)                                          # ... e, f expired (ttl 2.0): dropped from the DAG
     route(2.45, exclude={"d"})
+    pm.sync_gpu_layers("e", range(1, 5), 2.5)           # expired entries republished under the SAME keys:
+    pm.sync_gpu_layers("f", range(2, 7), 2.5)           # the key-set version does not move, the DAG must
+    route(2.55)
+    route(2.6)
     assert router.stats.matrix_reuses > 0 and router.stats.dags_built == router.stats.matrix_reuses + \
         router.stats.matrix_rebuilds
+
+
+def test_routers_sharing_one_perf_map(cuda_ready):
+    """Two routers on one PerfMap: each must see every republication (no destructive drain of the changes)."""
+    from paper_2509_26182_b200 import ChainRouter, PerfMap
+    flops = {"a": 1.0, "b": 2.0, "c": 1.5, "d": 0.7}
+    pm = PerfMap(ttl_s=10.0, latency_fn=lambda g, l, occ: 1e-3 / flops[g] * (1 + occ))
+    for g in flops:
+        pm.register_gpu(g)
+    ids = sorted(flops)
+    pm.publish_link_rtts({(x, y): 0.0005 * (1 + (i + j) % 3) for i, x in enumerate(ids)
+                          for j, y in enumerate(ids) if i < j}, 0.0)
+    for g, (s, e) in {"a": (1, 4), "b": (1, 2), "c": (3, 4), "d": (1, 4)}.items():
+        pm.sync_gpu_layers(g, range(s, e + 1), 0.0)
+    L = 4
+    r1, r2 = ChainRouter(pm, L), ChainRouter(pm, L)
+    for step in range(12):
+        for r in ((r1, r2) if step % 3 else (r2, r1)):
+            want = _expected(pm, 0.1, L, frozenset())
+            chain = r.route(0.1)
+            assert _as_tuple(chain) == (want[0], [tuple(h) for h in want[1]], want[2])
