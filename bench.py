@@ -22,8 +22,9 @@ allocations/sec at 1/2/4/8 B200"):
 * ``e2e``: the same Phase-2 metric through ``ScenarioReplayer.run_from_host``:
   pinned host scenario descriptors -> H2D -> device DAG build -> replay ->
   D2H of per-request costs and chain hashes, all inside the timed region.
-* ``cpu_baseline`` / ``--impl reference``: the reference's CPU path (the
-  oracle port, pinned bit-exact to the reference) on this box's host cores.
+* ``cpu_baseline`` / ``--impl reference``: the reference's CPU path on this box's host cores -- the
+  unmodified reference package installed into baseline/_ref (``oracle/bench_ref.py``), with the
+  golden-pinned oracle port beside it (``cpu_baseline_port``).
 """
 
 from __future__ import annotations
@@ -238,6 +239,12 @@ def run_ours(args):
         return rp, first, t_rank, reduce_max(t_rank), clk
 
     rp, first_cost, t_rank, t_max, clk = measure(args.mode, True)
+    ex = None
+    gather = None
+    if dist:
+        from paper_2509_26182_b200.distributed import NcclExchange
+        ex = NcclExchange(stream=stream)
+        gather = chain_gather_check(ex, cl, model, plan, rank, world, stream, R, W, args.mode)
     # gather of the chosen chains: the last step's per-selection chain hashes, summed over ranks
     # on NVLink (all-reduce); gather_chains moves full int16 host[L] records the same way when they are wanted
     from paper_2509_26182_b200.distributed import chain_checksum
@@ -307,9 +314,10 @@ def run_ours(args):
 
             def p1_step():
                 sw.run()
-                if dist:
-                    # global argmax over ranks: (best objective, variant id) all-gathered over NVLink
-                    global_argmax(sw.best_total[0], var_ids[sw.best_variant[0].clamp(min=0).long()])
+                if ex is not None:
+                    # global argmax over ranks: (best objective, variant id) through ss_argmax_allgather
+                    # (ncclAllGather over NVLink + a pick kernel; include/swarmsched_b200_nccl.h)
+                    ex.argmax(sw.best_total[0], var_ids[sw.best_variant[0].clamp(min=0).long()])
             t_p1 = timed(p1_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
         p1_steps = max(2, args.steps // 2)
         n_cand = packed.n_candidates
@@ -342,9 +350,11 @@ def run_ours(args):
     simr = None if args.no_sim else run_sim(args, rank, world, stream, barrier, reduce_max)
 
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, ss, packed if p1 else None)
+        cpu, cpu_port = cpu_baseline(args, ss, packed if p1 else None)
+        if cpu_port is None:                               # reference not installed: the port is the baseline
+            cpu, cpu_port = cpu_port or cpu, None
 
     if rank == 0:
         line = {
@@ -368,6 +378,7 @@ def run_ours(args):
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
             "chain_checksum": "%016x" % checksum,
+            "chain_gather": gather,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": _traffic(traffic_key, sel_per_step_rank), "peak_source": peak_src,
                          "kernel": kernel_name, "note": bound_note,
@@ -376,6 +387,7 @@ def run_ours(args):
             "clocks": clk,
             "phase2_alt": alt,
             "cpu_baseline": cpu,
+            "cpu_baseline_port": cpu_port,
             "phase1": p1,
             "c5": c5,
             "c1": c1,
@@ -386,9 +398,48 @@ def run_ours(args):
             "simulator": simr,
         }
         print(json.dumps(line), flush=True)
+    if ex is not None:
+        ex.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def chain_gather_check(ex, cl, model, plan, rank, world, stream, R, W, mode, per_rank=8):
+    """N > 1: the full chains (int16 host[L] + fp64 cost per selection) of a scenario sample gathered on rank 0
+    through ss_gather_chains (grouped ncclSend / ncclRecv over NVLink), then replayed by rank 0 alone on its own
+    GPU -- the N = 1 run of the same global scenarios -- and compared chain for chain."""
+    import torch
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import ScenarioReplayer
+    from paper_2509_26182_b200.distributed import shard
+    with torch.cuda.stream(stream):
+        ss = scen.build_scenarios(cl, model, plan, per_rank, churn=0.05, jitter=True,
+                                  seeds=shard(per_rank, rank, world), host_events=False)
+        rp = ScenarioReplayer(ss, window=W, stream=stream, mode=mode, max_requests=2 * R)
+        rp.run(R)
+        out = rp.run(R, gpus=True)
+        rp.raise_first_failure()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g, c = ex.gather_chains(out.gpus, out.cost, dst=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rank != 0:
+            return None
+        seeds = np.arange(per_rank * world, dtype=np.int64)
+        ss1 = scen.build_scenarios(cl, model, plan, len(seeds), churn=0.05, jitter=True, seeds=seeds,
+                                   host_events=False)
+        rp1 = ScenarioReplayer(ss1, window=W, stream=stream, mode=mode, max_requests=2 * R)
+        rp1.run(R)
+        o1 = rp1.run(R, gpus=True)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(g, o1.gpus) and torch.equal(c, o1.cost))
+    nbytes = int(out.gpus.numel() * 2 + out.cost.numel() * 8) * world
+    return {"scenarios": int(len(seeds)), "selections": int(len(seeds) * R), "bytes": nbytes,
+            "gather_ms": e0.elapsed_time(e1), "path": "ss_gather_chains (grouped ncclSend/ncclRecv to rank 0)",
+            "matches_single_gpu_run": same}
 
 
 def run_c5(args, rank, world, stream, barrier, reduce_max):
@@ -786,55 +837,94 @@ def _resident_bytes(rp):
 
 
 def cpu_baseline(args, ss_dev, packed):
-    from oracle import bench_cpu
+    """The reference's CPU path on this box's host cores, on a bounded sample of the same workload: the
+    UNMODIFIED reference (baseline/_ref, kind "reference") when installed, and the golden-pinned port
+    (kind "port") beside it."""
+    from oracle import bench_cpu, bench_ref
     from paper_2509_26182_b200 import scenarios as scen
     n_s = min(args.cpu_sample_scenarios, ss_dev.n_scenarios)
     cl, model, plan = base_pool()
     # the sampled scenarios' departures drawn on the host (the same events the device generated)
     ss = scen.build_scenarios(cl, model, plan, n_s, seeds=ss_dev.seeds[:n_s], churn=0.05, jitter=True)
     rate, cores, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), args.cpu_sample_requests, args.window)
-    out = {"value": rate, "unit": "selections/s", "cores": cores, "kind": "port",
-           "sample": f"C4 shape: {n_s} scenarios x {args.cpu_sample_requests} requests (W={args.window}), "
-                     f"{sel} selections in {wall:.1f} s wall on {cores} processes"}
+    port = {"value": rate, "unit": "selections/s", "cores": cores, "kind": "port",
+            "sample": f"C4 shape: {n_s} scenarios x {args.cpu_sample_requests} requests (W={args.window}), "
+                      f"{sel} selections in {wall:.1f} s wall on {cores} processes"}
     if packed is not None:
         r1, c1, cand, w1 = bench_cpu.phase1_rate(packed, args.cpu_sample_pools)
-        out["phase1"] = {"value": r1, "unit": "candidates/s", "cores": c1,
-                         "sample": f"C3 shape: first {args.cpu_sample_pools} pools, {cand} candidates in {w1:.1f} s"}
-    return out
+        port["phase1"] = {"value": r1, "unit": "candidates/s", "cores": c1,
+                          "sample": f"C3 shape: first {args.cpu_sample_pools} pools, {cand} candidates in {w1:.1f} s"}
+    if not bench_ref.available():
+        return port, None
+    n_req = args.window + 64                              # releases run for the last 64 requests
+    cores = len(os.sched_getaffinity(0))
+    p2 = bench_ref.phase2_rate(ss_dev.seeds[:cores], n_req, args.window)
+    out = {"value": p2["value"], "unit": "selections/s", "cores": p2["cores"], "kind": "reference",
+           "per_core": p2["per_core"],
+           "sample": f"C4 shape: the unmodified reference (baseline/_ref) ChainRouter.route/release, "
+                     f"{p2['cores']} scenarios x {n_req} requests (W={args.window}), {p2['selections']} selections, "
+                     f"{p2['route_seconds']:.1f} process-seconds inside the routing loops on {p2['cores']} processes"}
+    p1 = bench_ref.phase1_rate(range(2 * cores), 80)
+    out["phase1"] = {"value": p1["value"], "unit": "candidates/s", "cores": p1["cores"], "kind": "reference",
+                     "per_core": p1["per_core"],
+                     "sample": f"C3 shape: variants 0..{2 * cores - 1}, {p1['candidates']} candidates "
+                               f"(solve_stage_counts + score + rebalance_pipeline per (region, k)) in "
+                               f"{p1['eval_seconds']:.1f} process-seconds"}
+    return out, port
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path on the box's host cores (rank 0 only):
+    the unmodified reference package (baseline/_ref) when installed, else the golden-pinned port."""
     rank, world, local = dist_env()
     if rank != 0:
         return
-    from oracle import alloc_ref, bench_cpu
-    from paper_2509_26182_b200 import scenarios as scen
-    from paper_2509_26182_b200.plan import AllocationPlan, Pipeline
-    from paper_2509_26182_b200.topology import LayerSlice
-    cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
-    d = alloc_ref.allocate(cl, model)
-    pipes = tuple(Pipeline(tuple(LayerSlice(s["gpu_id"], s["start_layer"], s["end_layer"]) for s in p["stages"]),
-                           p["region"]) for p in d["pipelines"])
-    plan = AllocationPlan(d["k"], pipes, sum(p.stage_count for p in pipes), d["objective"], ())
-    n_s = args.cpu_sample_scenarios
-    ss = scen.build_scenarios(cl, model, plan, n_s, seed0=0, churn=0.05, jitter=True)
-    rates, walls = [], []
-    for _ in range(args.warmup):
-        bench_cpu.phase2_rate(ss, list(range(min(8, n_s))), 4, args.window)
-    for _ in range(args.steps):
-        rate, cores, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), args.cpu_sample_requests // 4 or 1,
-                                                       args.window)
-        rates.append(rate)
-        walls.append(wall)
-    value = float(np.median(rates))
+    from oracle import bench_ref
+    cores = len(os.sched_getaffinity(0))
+    n_req = args.window + 64
+    if bench_ref.available():
+        seeds = np.arange(cores, dtype=np.int64)
+        rates, walls = [], []
+        for _ in range(args.warmup):
+            bench_ref.phase2_rate(seeds[:min(cores, 4)], 8, args.window)
+        for _ in range(args.steps):
+            r = bench_ref.phase2_rate(seeds, n_req, args.window)
+            rates.append(r["value"])
+            walls.append(r["wall_seconds"])
+        value = float(np.median(rates))
+        kind, used = "reference", r["cores"]
+        workload = ("C4 shape (L=64, 256-GPU pool, churn+jitter scenarios, W=%d) -- the unmodified reference "
+                    "(baseline/_ref: swarmsched ChainRouter.route/release, MembershipManager-built states)" % args.window)
+        sample = f"{len(seeds)} scenarios x {n_req} requests per step, routing loops only (set-up excluded)"
+    else:
+        from oracle import alloc_ref, bench_cpu
+        from paper_2509_26182_b200 import scenarios as scen
+        from paper_2509_26182_b200.plan import AllocationPlan, Pipeline
+        from paper_2509_26182_b200.topology import LayerSlice
+        cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+        d = alloc_ref.allocate(cl, model)
+        pipes = tuple(Pipeline(tuple(LayerSlice(s["gpu_id"], s["start_layer"], s["end_layer"]) for s in p["stages"]),
+                               p["region"]) for p in d["pipelines"])
+        plan = AllocationPlan(d["k"], pipes, sum(p.stage_count for p in pipes), d["objective"], ())
+        n_s = args.cpu_sample_scenarios
+        ss = scen.build_scenarios(cl, model, plan, n_s, seed0=0, churn=0.05, jitter=True)
+        rates, walls = [], []
+        for _ in range(args.warmup):
+            bench_cpu.phase2_rate(ss, list(range(min(8, n_s))), 4, args.window)
+        for _ in range(args.steps):
+            rate, used, sel, wall = bench_cpu.phase2_rate(ss, list(range(n_s)), n_req, args.window)
+            rates.append(rate)
+            walls.append(wall)
+        value = float(np.median(rates))
+        kind = "port"
+        workload = ("C4 shape (L=64, 256-GPU pool, churn+jitter scenarios, W=%d) -- reference CPU path (oracle "
+                    "port of router.py/perfmap.py, bit-exact to the reference)" % args.window)
+        sample = f"{n_s} scenarios x {n_req} requests per step"
     line = {"metric": METRIC, "value": value, "unit": "selections/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(walls)), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C4 shape (L=64, 256-GPU pool, churn+jitter scenarios, W=%d) -- reference CPU "
-                                   "path (oracle port of router.py/perfmap.py, bit-exact to the reference)"
-                                   % args.window, "parallelism": f"{cores} host processes"},
-            "cpu_baseline": {"value": value, "unit": "selections/s", "cores": cores, "kind": "port",
-                             "sample": f"{n_s} scenarios x {args.cpu_sample_requests // 4 or 1} requests per step"},
+            "config": {"workload": workload, "parallelism": f"{used} host processes"},
+            "cpu_baseline": {"value": value, "unit": "selections/s", "cores": used, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": "selections/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -151,6 +151,44 @@ def load_library(path: str = LIB_PATH):
 _device_checked = False
 
 
+LIB_NCCL_PATH = os.path.join(HERE, "libswarmsched_b200_nccl.so")
+_nccl_lib = None
+
+_SIGS_NCCL = {
+    "ss_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "ss_nccl_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "ss_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "ss_argmax_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]),
+    "ss_gather_chains": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]),
+}
+
+
+def load_nccl_library(path: str = LIB_NCCL_PATH):
+    """dlopen the exchange library (include/swarmsched_b200_nccl.h); torch is imported first so the process
+    shares torch's libnccl.so.2."""
+    global _nccl_lib
+    with _lock:
+        if _nccl_lib is not None:
+            return _nccl_lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(f"{path} is missing; run __graft_entry__.build() (nvcc, sm_100a, NCCL)")
+        import torch  # noqa: F401  (loads libnccl.so.2)
+        lib = C.CDLL(path)
+        for name, (res, args) in _SIGS_NCCL.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _nccl_lib = lib
+        return lib
+
+
+def nccl_lib():
+    lib()                                   # device check
+    return load_nccl_library()
+
+
 def lib():
     """The loaded library, after checking (once) that a CUDA device is usable."""
     global _device_checked
@@ -164,7 +202,7 @@ def lib():
 
 def check(status: int, what: str) -> None:
     if status != SS_OK:
-        msg = load_library().ss_status_str(status).decode()
+        msg = "NCCL error" if status == 12 else load_library().ss_status_str(status).decode()
         raise DeviceError(f"{what}: {msg} (status {status})")
 
 

@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
         mark(0);
         // ---- DP over the layer columns + final argmin / backtrack ------------------
         double v;
-        if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
-        else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_dim);
+        if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_pitch);
+        else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_pitch);
         mark(1);
         if (tid == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         if (!(v <= DBL_MAX)) {
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
                 break;
             }
             double v;
-            if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
-            else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_dim);
+            if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_pitch);
+            else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_pitch);
             if (!(v <= DBL_MAX)) break;                          // UncoveredLayer / NoPath: the head waits
             __syncthreads();
             // admit: reserve the tokens and +1 occupancy on the chain's distinct GPUs (sim.py:330-331)

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(32) sim_warp_kernel(ss_dag_set D, WarpLayout A
             tau[g] = tcap[g] - kv[g] < tok ? INF : base[g] * (o < B.pow_len ? ppw[o] : P.pub_pow[o]);  // KV-blocked excluded
         }
         __syncwarp();
-        const double v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_dim);
+        const double v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_pitch);
         if (!(v <= DBL_MAX)) return false;
         // a free live slot (warp-uniform search)
         int slot = -1;
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(NWD * 32) sim_mw_kernel(ss_dag_set D, WarpLayo
         }
         __syncthreads();
         const double v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare,
-                                                 tid, A.mat_dim);
+                                                 tid, A.mat_pitch);
         if (!(v <= DBL_MAX)) return false;
         int slot = -1;                                           // same result in every warp
         for (int e0 = 0; e0 < B.max_live && slot < 0; e0 += 32) {

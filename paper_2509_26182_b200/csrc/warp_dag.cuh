@@ -17,6 +17,8 @@ constexpr unsigned FULL = 0xffffffffu;
 struct WarpLayout {
     int e_cap, ring_len, pow_len;
     int mat_dim;       // > 0: the scenario's whole RTT matrix (mat_dim^2 fp64) replaces the edge blocks in E
+    int mat_pitch;     // its row pitch in E: odd (mat_dim | 1), so lanes gathering one column from different
+                       // source rows (mw_route: 4 source lanes per destination) hit different banks
     int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
         off_ring, off_pow, off_cost, off_kv, off_tcap, total;
 };
@@ -61,8 +63,11 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
         }
     }
     if (A.mat_dim > 0) {
-        const int nn = A.mat_dim * A.mat_dim;
-        for (int q = lane; q < nn; q += 32) E[q] = mat[q];
+        const int n = A.mat_dim, P = A.mat_pitch;
+        for (int q = lane; q < n * n; q += 32) {
+            const int r = q / n;
+            E[r * P + (q - r * n)] = mat[q];
+        }
     }
     __syncwarp();
     return true;
@@ -162,14 +167,15 @@ inline int sm_count() {
 inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A, int mat_dim = 0) {
     if (D.max_hosts > 32 || D.max_layers < 1) return false;
     const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * D.max_hosts * D.max_hosts;
-    A.mat_dim = (mat_dim > 0 && (int64_t)mat_dim * mat_dim < e_cap && D.n_dags > sm_count()) ? mat_dim : 0;
+    A.mat_dim = (mat_dim > 0 && (int64_t)mat_dim * (mat_dim | 1) < e_cap && D.n_dags > sm_count()) ? mat_dim : 0;
+    A.mat_pitch = A.mat_dim | 1;
     const int64_t ring_len = window > 0 ? (int64_t)window * (D.max_layers + 1) : 0;
     if (e_cap > (1 << 20) || ring_len > (1 << 20)) return false;
     A.e_cap = (int)e_cap;
     A.ring_len = (int)ring_len;
     A.pow_len = occpow_len < 256 ? occpow_len : 256;
     int o = 0;
-    A.off_E = o;      o += align16((A.mat_dim ? A.mat_dim * A.mat_dim : A.e_cap) * 8);
+    A.off_E = o;      o += align16((A.mat_dim ? A.mat_dim * A.mat_pitch : A.e_cap) * 8);
     A.off_node = o;   o += align16(D.max_layers * D.max_hosts * 4);
     A.off_cl = o;     o += align16((D.max_layers + 1) * 4);
     A.off_noff = o;   o += align16(D.max_layers * 4);

@@ -11,8 +11,8 @@ from conftest import hx
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _header_symbols():
-    text = open(os.path.join(ROOT, "include", "swarmsched_b200.h")).read()
+def _header_symbols(name="swarmsched_b200.h"):
+    text = open(os.path.join(ROOT, "include", name)).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(ss_[a-z0-9_]+)\s*\(", text)))
 
@@ -31,6 +31,16 @@ def test_library_builds_and_exports_every_header_symbol():
     h, l, g = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     assert lib.ss_limits(ctypes.byref(h), ctypes.byref(l), ctypes.byref(g)) == 0
     assert h.value == 256
+
+
+def test_nccl_library_builds_and_exports_every_header_symbol():
+    from paper_2509_26182_b200 import _build, _native
+    _build.build_nccl()
+    lib = _native.load_nccl_library()
+    declared = _header_symbols("swarmsched_b200_nccl.h")
+    assert set(declared) == set(_native._SIGS_NCCL), declared
+    for name in declared:
+        assert hasattr(lib, name), name
 
 
 def test_compute_entry_points_refuse_without_gpu():

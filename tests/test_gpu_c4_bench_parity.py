@@ -1,7 +1,8 @@
 """Parity at the bench's own size ("every 97th scenario in full plus 1% random others").
 
 The headline workload exactly as bench.py builds it -- C4 pool (L64/N256, k=73), 1,184 scenarios with
-device-drawn departures + jitter, 64 requests, W=64 -- through both throughput kernels.  Every 97th scenario
+device-drawn departures + jitter, W=64 -- through both throughput kernels, for 320 requests (5 x W): the timed
+region's steady state, with a release before every route from request 64 on and up to 64 live chains.  Every 97th scenario
 plus a seeded 1% random sample is replayed by the oracle on the same (host-drawn, identical) scenario states
 and must match chain for chain, cost for cost, occupancy for occupancy.  The two kernels must agree on all
 1,184 scenarios.
@@ -14,7 +15,7 @@ from oracle import chain_ref
 
 pytestmark = pytest.mark.gpu
 
-S, R, W = 1184, 64, 64
+S, R, W = 1184, 320, 64
 
 
 def test_c4_bench_size_sampled_scenarios_vs_oracle(cuda_ready):
@@ -28,7 +29,7 @@ def test_c4_bench_size_sampled_scenarios_vs_oracle(cuda_ready):
     dev = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=seeds, host_events=False)
     outs = {}
     for mode in ("slots", "blocks"):
-        rp = ScenarioReplayer(dev, window=W, mode=mode)
+        rp = ScenarioReplayer(dev, window=W, mode=mode, max_requests=R)
         out = rp.run(R, gpus=True)
         rp.raise_first_failure()
         outs[mode] = (out.gpus.cpu().numpy(), out.cost.cpu().numpy(), rp.occ.view(S, -1).cpu().numpy())

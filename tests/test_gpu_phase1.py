@@ -75,7 +75,7 @@ def test_allocate_golden(cuda_ready, phase1_cases):
 
 def test_objective_golden(cuda_ready, phase1_cases):
     from paper_2509_26182_b200 import estimate_objective_params, scenarios as scen
-    for rec in phase1_cases["objective"][:6]:
+    for rec in phase1_cases["objective"]:
         cl, m = scen.synthetic_cluster(rec["n"], seed=rec["seed"], model=scen.bench_model(rec["L"]))
         p = estimate_objective_params(cl.gpus_in_region(rec["region"]), cl, m, 1.0, 128.0)
         assert (p.t_comp_seconds.hex(), p.rtt_seconds.hex()) == (rec["t_comp"], rec["rtt"])
@@ -92,6 +92,51 @@ def test_waterfill_golden(cuda_ready, phase1_cases):
         assert list(hamilton_round(frac, rec["caps"], rec["L"]).layers) == rec["layers"], i
         assert list(hamilton_round(frac, rec["caps"]).layers) == list(
             waterfill_ref.largest_remainder(frac.targets, rec["caps"])), i
+
+
+def test_waterfill_golden_all_batched(cuda_ready, phase1_cases):
+    """All 400 golden solve_lambda + hamilton_round cases (total = L and total = None) in batched launches."""
+    import torch
+    from paper_2509_26182_b200 import _native as N
+    recs = phase1_cases["waterfill"]
+    sizes = [len(r["caps"]) for r in recs]
+    ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    dev = torch.device("cuda")
+    n = int(ptr[-1])
+    fl = torch.tensor([hx(f) for r in recs for f in r["flops"]], dtype=torch.float64, device=dev)
+    caps = torch.tensor([c for r in recs for c in r["caps"]], dtype=torch.int32, device=dev)
+    layers = torch.tensor([r["L"] for r in recs], dtype=torch.int32, device=dev)
+    gp = torch.from_numpy(ptr).to(dev)
+    targets = torch.zeros(n, dtype=torch.float64, device=dev)
+    tflag = torch.zeros(n, dtype=torch.int32, device=dev)
+    level = torch.zeros(len(recs), dtype=torch.float64, device=dev)
+    st = torch.zeros(len(recs), dtype=torch.int32, device=dev)
+    aux = torch.zeros(len(recs), dtype=torch.int32, device=dev)
+    N.check(N.lib().ss_waterfill(len(recs), N.ptr(gp), N.ptr(fl), N.ptr(caps), N.ptr(layers), 0, N.ptr(targets),
+                                 N.ptr(tflag), N.ptr(level), None, N.ptr(st), N.ptr(aux), N.stream_handle()),
+            "ss_waterfill")
+    assert not st.any().item()
+    tv, tf, lv = targets.cpu().numpy(), tflag.cpu().numpy(), level.cpu().numpy()
+    for i, rec in enumerate(recs):
+        got = [int(v) if f else float(v) for v, f in zip(tv[ptr[i]:ptr[i + 1]], tf[ptr[i]:ptr[i + 1]])]
+        want = [untag(t) for t in rec["targets"]]
+        assert got == want and [type(t) for t in got] == [type(t) for t in want], i
+        assert float(lv[i]) == hx(rec["level"]), i
+    for total_of in (lambda r: r["L"], lambda r: -1):
+        total = torch.tensor([total_of(r) for r in recs], dtype=torch.int32, device=dev)
+        counts = torch.zeros(n, dtype=torch.int32, device=dev)
+        hs = torch.zeros(len(recs), dtype=torch.int32, device=dev)
+        N.check(N.lib().ss_hamilton(len(recs), N.ptr(gp), N.ptr(targets), N.ptr(tflag), N.ptr(caps), N.ptr(total),
+                                    N.ptr(counts), N.ptr(hs), N.stream_handle()), "ss_hamilton")
+        assert not hs.any().item()
+        cv = counts.cpu().numpy()
+        for i, rec in enumerate(recs):
+            got = cv[ptr[i]:ptr[i + 1]].tolist()
+            if total_of(rec) >= 0:
+                assert got == rec["layers"], i
+            else:
+                tg = [untag(t) for t in rec["targets"]]
+                assert got == list(waterfill_ref.largest_remainder(tg, rec["caps"])), i
 
 
 def test_waterfill_batched_vs_oracle(cuda_ready, phase1_cases):
@@ -239,3 +284,37 @@ def test_cover_serial_and_parallel_m_paths_agree(cuda_ready, L):
         want = alloc_ref.stage_counts(pool.caps, L, pool.kmax)
         got = {k: int(stages[koff[p] + k - 1]) for k in range(1, pool.kmax + 1) if int(stages[koff[p] + k - 1]) > 0}
         assert {k: s for k, (s, _) in want.items()} == got, p
+
+
+@pytest.mark.parametrize("L", [80, 64])
+def test_bench_sweep_every_97th_variant_vs_oracle(cuda_ready, L):
+    """The bench's whole C3 sweep (synthetic_cluster(256, seed=v), v = 0..1811, one launch set) at L=80 (configs[2])
+    and at the north star's L=64: every 97th variant's objective total, stage counts, groups' water-filled layer
+    counts and Z(k) vs the oracle's allocate (allocator.py:541-618), and the sweep's argmax vs the totals."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import VariantSweep
+    V = 1812
+    packed, meta = scen.bench_variants(V, 256, L, seed0=0)
+    sw = VariantSweep(packed, fill_all=True)
+    sw.run()
+    res = sw.batch.fetch()
+    totals = sw.total.cpu().numpy()
+    for v in range(0, V, 97):
+        cl, m = scen.synthetic_cluster(256, seed=v, model=scen.bench_model(L))
+        want = alloc_ref.allocate(cl, m)
+        assert totals[v] == want["objective"], v
+        rows = {(r["region"], r["k"]): (r["s_star"], r["z"]) for r in want["per_k"]}
+        for p in range(packed.var_ptr[v], packed.var_ptr[v + 1]):
+            pool = packed.pools[p]
+            region = meta[p][1]
+            sols = res.solutions(p)
+            assert sols == alloc_ref.stage_counts(pool.caps, L, pool.kmax), (v, region)
+            for k, (s, groups) in sols.items():
+                assert (s, res.z_of(p, k)) == rows[(region, k)], (v, region, k)
+                counts = res.counts_of(p, k)
+                pos = 0
+                for grp in groups:
+                    want_len = waterfill_ref.stage_lengths([pool.flops[i] for i in grp], [pool.caps[i] for i in grp], L)
+                    assert counts[pos:pos + len(grp)] == want_len, (v, region, k)
+                    pos += len(grp)
+    assert int(sw.best_variant.cpu()[0]) == int(np.argmax(totals))
