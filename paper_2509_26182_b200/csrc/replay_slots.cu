@@ -221,7 +221,8 @@ struct SlotArgs {
     int64_t stream_stride;
     int s_rows, w, nbuf, stage_bytes;
     int off_T, off_stage, off_full, off_empty, off_meta, meta_bytes, off_part, off_bp, off_picks, off_tau, off_occ,
-        off_stamp, off_slotgpu, off_cl, off_red, off_misc, off_base, off_pow, pow_len, off_rel, off_coff, off_costw, total;
+        off_stamp, off_slotgpu, off_cl, off_red, off_misc, off_base, off_pow, pow_len, off_rel, off_coff, off_costw, off_seg,
+        total;
     unsigned long long* prof;   // diagnostics (env SS_SLOT_PROF=1): per-warp phase cycle totals, else NULL
 };
 
@@ -240,8 +241,10 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"n"(CONSUMER_BAR), "r"(nthreads) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+constexpr int ALL_BAR = 2;
+// boundary / request-start barrier of the consumers AND the unit-producer warp
+__device__ __forceinline__ void all_sync(int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ALL_BAR), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ void lex_min(double& v, int& i, double v2, int i2) {
@@ -268,23 +271,26 @@ __device__ __forceinline__ void relax_row(const double* row, double c, int p, do
     }
 }
 
-// Warp roles: NW consumer warps, warp NW is the TMA producer of the row/column units.
+// Warp roles: NW consumer warps (the DP), warp NW owns the row/column units: it streams them with 1-D TMA
+// bulk copies through a ring of staging buffers it alone consumes, and writes them into T ("apply").
 //
 // Every layer column is cut into NW contiguous position ranges (warp w owns
-// [w*R/NW, (w+1)*R/NW)).  Per boundary b, ONE named barrier:
-//   merge : warp w finishes the costs of ITS positions of column b -- the
-//           lexicographic (value, position) min over the NW range partials of
-//           boundary b-1 (== numpy first-index argmin), + tau; backpointers;
-//   relax : lanes own DPL destination slots and scan the warp's sources (cost and
-//           slot broadcast by shuffle) -> partial (value, position) per slot;
-//   apply : rows / columns of the GPUs entering at b+1 (slots are reused one
-//           boundary late, so nothing relaxed at b is overwritten).
+// [w*R/NW, (w+1)*R/NW)).  Per boundary b, ONE named barrier over all NW + 1 warps:
+//   consumers: merge -- warp w finishes the costs of ITS positions of column b: the lexicographic
+//              (value, position) min over the NW range partials of boundary b-1 (== numpy first-index
+//              argmin), + tau; backpointers;
+//              relax -- lanes own DPL destination slots and scan the warp's sources -> partial (value,
+//              position) per slot;
+//   producer : apply(b+1) -- rows / columns of the GPUs entering at b+1, concurrently with relax(b): slots are
+//              reused one boundary late, so nothing relaxed at b is overwritten, and the copy is off the
+//              consumers' critical path.
 template <int DPL, int NW>
 __global__ void __launch_bounds__((NW + 1) * 32, 2)
 replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int SC = DPL * 32;
     constexpr int NC = NW * 32;
+    constexpr int NT = NC + 32;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
     const int dag = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -296,7 +302,7 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
 
     double* T = reinterpret_cast<double*>(smem + A.off_T);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + A.off_full);
-    uint64_t* empty = reinterpret_cast<uint64_t*>(smem + A.off_empty);
+    uint64_t* rows_bar = reinterpret_cast<uint64_t*>(smem + A.off_empty);   // the request's initial rows landed
     unsigned char* meta_s = smem + A.off_meta;
     double* part_v = reinterpret_cast<double*>(smem + A.off_part);          // [2][NW][SC]
     int16_t* part_i = reinterpret_cast<int16_t*>(part_v + 2 * NW * SC);     // [2][NW][SC]
@@ -314,7 +320,9 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     double* pow_s = reinterpret_cast<double*>(smem + A.off_pow);     // occpow[0 .. pow_len)
     int* rel = reinterpret_cast<int*>(smem + A.off_rel);             // prefetched ring slot of the next release
     int* coff = reinterpret_cast<int*>(smem + A.off_coff);           // this DAG's column offsets
-    constexpr int CW_LEN = SC / NW + 8;                               // >= ceil(SC / NW) + 3, multiple of 4
+    uint8_t* seg_end = smem + A.off_seg;                              // [NW][SC] backtrack segment ends
+    int* seg_start = reinterpret_cast<int*>(smem + A.off_seg + NW * SC);   // [NW] true segment starts
+    constexpr int CW_LEN = SC / NW + 8;                               // >= ceil(SC / NW) + 1, even
     double* cost_w = reinterpret_cast<double*>(smem + A.off_costw);  // [NW][CW_LEN] each warp's source costs
     int* row_w = reinterpret_cast<int*>(cost_w + NW * CW_LEN);        // [NW][CW_LEN] their T row byte offsets
 
@@ -324,10 +332,8 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         misc[0] = SS_OK;
         misc[1] = 0;
         if (R.st.status[dag] != SS_OK) misc[0] = -1;
-        for (int b = 0; b < A.nbuf; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], NW);
-        }
+        for (int b = 0; b < A.nbuf; ++b) mbar_init(&full[b], 1);
+        mbar_init(rows_bar, 1);
         fence_mbar_init();
     }
     // static program metadata -> shared memory (once per launch, reused by every request)
@@ -364,30 +370,96 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     }
     const int n_req = R.n_req;
     const double* stream_g = A.stream + (int64_t)dag * A.stream_stride;
+    unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // prologue relax apply barrier epilogue argmin+backtrack chain-update initial-rows
 
-    // ========================= producer: units of boundaries 1..nblk-1 =========
+    // ========================= producer: TMA ring + apply(1..nblk-1) ===============
     if (warp == NW) {
-        if (lane == 0) {
-            int buf = 0;
-            uint32_t phase = 0;
-            bool wrapped = false;
-            for (int r = 0; r < n_req; ++r) {
-                for (int b = 1; b < nblk; ++b) {
-                    const BlkMeta m = bm[b];
+        const int64_t total = (int64_t)n_req * misc[3];
+        int64_t issued = 0;
+        int ib = 1, iu0 = 0;                                 // next chunk to issue: boundary, first unit
+        auto issue_next = [&](int buf) {                     // lane 0; buffer `buf` is free
+            while (ib < nblk && iu0 >= 2 * bm[ib].n_ins) { ++ib; iu0 = 0; }
+            if (ib >= nblk) { ib = 1; iu0 = 0; while (ib < nblk && 2 * bm[ib].n_ins == 0) ++ib; }
+            const BlkMeta m = bm[ib];
+            const int nu = min(upc, 2 * m.n_ins - iu0);
+            const uint32_t bytes = (uint32_t)nu * Wp * 8;
+            fence_proxy_async_smem();
+            mbar_expect_tx(&full[buf], bytes);
+            bulk_g2s(smem + A.off_stage + (size_t)buf * A.stage_bytes, stream_g + (int64_t)(m.unit_start + iu0) * Wp,
+                     bytes, &full[buf]);
+            iu0 += nu;
+            ++issued;
+        };
+        // the initial frontier's rows (boundary 0, one unit per GPU of col_0 U col_1) go straight into their T rows:
+        // 1-D bulk copies (T rows are 16-B aligned: even pitch), completing on rows_bar
+        int rows_issued = 0;
+        auto issue_rows = [&]() {
+            const BlkMeta m = bm[0];
+            const uint32_t ub = (uint32_t)Wp * 8;
+            if (lane == 0) mbar_expect_tx(rows_bar, ub * (uint32_t)m.n_ins);
+            __syncwarp();
+            fence_proxy_async_smem();
+            const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
+            for (int u = lane; u < m.n_ins; u += 32)
+                bulk_g2s(T + ins[2 * (m.ins_start + u)] * W, s0 + (int64_t)u * Wp, ub, rows_bar);
+            ++rows_issued;
+        };
+        if (n_req > 0) issue_rows();
+        if (lane == 0)
+            for (int b = 0; b < A.nbuf && issued < total; ++b) issue_next(b);
+        int cbuf = 0;
+        uint32_t cphase = 0;
+        int64_t consumed = 0;
+        for (int r = 0; r < n_req; ++r) {
+            all_sync(NT);                                    // request start: tau ready, initial rows landed
+            if (misc[0] != SS_OK) break;
+            long long tp = A.prof ? clock64() : 0;
+            for (int b = 0; b < nblk; ++b) {
+                if (b + 1 < nblk) {
+                    const BlkMeta m = bm[b + 1];
                     const int units = 2 * m.n_ins;
                     for (int u0 = 0; u0 < units; u0 += upc) {
                         const int nu = min(upc, units - u0);
-                        if (wrapped) mbar_wait_backoff(&empty[buf], phase ^ 1u);
-                        const uint32_t bytes = (uint32_t)nu * Wp * 8;
-                        fence_proxy_async_smem();
-                        mbar_expect_tx(&full[buf], bytes);
-                        bulk_g2s(smem + A.off_stage + (size_t)buf * A.stage_bytes,
-                                 stream_g + (int64_t)(m.unit_start + u0) * Wp, bytes, &full[buf]);
-                        if (++buf == A.nbuf) { buf = 0; phase ^= 1u; wrapped = true; }
+                        mbar_wait(&full[cbuf], cphase);
+                        const double* stg = reinterpret_cast<const double*>(smem + A.off_stage +
+                                                                            (size_t)cbuf * A.stage_bytes);
+                        for (int ul = 0; ul < nu; ++ul) {
+                            const int u = u0 + ul;
+                            const int slot = ins[2 * (m.ins_start + (u >> 1))];
+                            const double* su = stg + ul * Wp;
+                            // tw <= s_rows <= SC: all DPL loads in flight before the stores
+                            double x[DPL];
+#pragma unroll
+                            for (int d = 0; d < DPL; ++d) x[d] = lane + 32 * d < tw ? su[lane + 32 * d] : 0.0;
+                            const int step = (u & 1) ? 32 * W : 32;      // column: stride W; row: contiguous
+                            double* dst = T + ((u & 1) ? lane * W + slot : slot * W + lane);
+#pragma unroll
+                            for (int d = 0; d < DPL; ++d)
+                                if (lane + 32 * d < tw) dst[d * step] = x[d];
+                        }
+                        __syncwarp();                        // the buffer is read: refill it
+                        if (lane == 0 && issued < total) issue_next(cbuf);
+                        ++consumed;
+                        if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
                     }
+                    for (int k = lane; k < m.n_ins; k += 32)
+                        slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
                 }
+                if (A.prof) { const long long t = clock64(); pacc[2] += (unsigned long long)(t - tp); tp = t; }
+                all_sync(NT);                                // boundary b
+                if (A.prof) { const long long t = clock64(); pacc[3] += (unsigned long long)(t - tp); tp = t; }
             }
+            if (r + 1 < n_req) issue_rows();                 // T is no longer read by this request
         }
+        if (rows_issued > 0) mbar_wait(rows_bar, (uint32_t)((rows_issued - 1) & 1));   // earlier phases were awaited
+        // an aborted launch leaves copies in flight: land them before the CTA exits
+        while (consumed < issued) {
+            mbar_wait(&full[cbuf], cphase);
+            ++consumed;
+            if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
+        }
+        if (A.prof && lane == 0)
+            for (int k = 0; k < 8; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
         return;
     }
 
@@ -410,62 +482,13 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         }
     };
     if (n_req > 0) prefetch_release(req0);
-    int cbuf = 0;
-    uint32_t cphase = 0;
-    int64_t consumed = 0;
-    auto release_chunk = [&]() {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[cbuf]);
-        if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
-        ++consumed;
-    };
-    auto drain = [&]() {
-        const int64_t total = (int64_t)n_req * misc[3];
-        while (consumed < total) {
-            mbar_wait(&full[cbuf], cphase);
-            release_chunk();
-        }
-    };
-    // apply(b), b >= 1: row + column of every GPU entering the frontier at b (TMA-staged units)
-    unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};    // prologue, relax, apply, barrier, epilogue, TMA wait
-    auto apply = [&](int b) {
-        const BlkMeta m = bm[b];
-        const int units = 2 * m.n_ins;
-        for (int u0 = 0; u0 < units; u0 += upc) {
-            const int nu = min(upc, units - u0);
-            if (A.prof) {
-                const long long t0 = clock64();
-                mbar_wait(&full[cbuf], cphase);
-                pacc[5] += (unsigned long long)(clock64() - t0);
-            } else {
-                mbar_wait(&full[cbuf], cphase);
-            }
-            const double* stg = reinterpret_cast<const double*>(smem + A.off_stage + (size_t)cbuf * A.stage_bytes);
-            for (int ul = warp; ul < nu; ul += NW) {
-                const int u = u0 + ul;
-                const int slot = ins[2 * (m.ins_start + (u >> 1))];
-                const double* su = stg + ul * Wp;
-                // tw <= s_rows <= SC: all DPL loads in flight before the stores (one LDS latency per unit)
-                double x[DPL];
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) x[d] = lane + 32 * d < tw ? su[lane + 32 * d] : 0.0;
-                const int step = (u & 1) ? 32 * W : 32;                  // column: stride W; row: contiguous
-                double* dst = T + ((u & 1) ? lane * W + slot : slot * W + lane);
-#pragma unroll
-                for (int d = 0; d < DPL; ++d)
-                    if (lane + 32 * d < tw) dst[d * step] = x[d];
-            }
-            release_chunk();
-        }
-        for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
-    };
     // Costs of this warp's positions [p0, p0+n) of column c into cw[], their T row byte offsets into rw[]
-    // (padded with +inf / row 0 to a multiple of 4).  c == 0: tau of the first layer's hosts; c >= 1: the
+    // (padded with +inf / row 0 to an even count).  c == 0: tau of the first layer's hosts; c >= 1: the
     // lexicographic (value, position) min over the NW range partials of boundary c-1 (== numpy first-index
     // argmin) + tau, recording the backpointers of boundary c-1.
     auto stage_sources = [&](int c, int p0, int n, double* cw, int* rw) {
-        const int n4 = (n + 3) & ~3;
-        for (int q = lane; q < n4; q += 32) {
+        const int n2 = (n + 1) & ~1;
+        for (int q = lane; q < n2; q += 32) {
             double cst = INF;
             int sl = 0;
             if (q < n) {
@@ -500,45 +523,35 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         pacc[k] += (unsigned long long)(_t - tp);                    \
         tp = _t;                                                     \
     }
-    auto issue_initial_rows = [&]() {
-        const BlkMeta m = bm[0];
-        const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
-        for (int u = warp; u < m.n_ins; u += NW) {
-            const int slot = ins[2 * (m.ins_start + u)];
-            const double* su = s0 + (int64_t)u * Wp;
-            for (int t = lane; t < tw; t += 32) cp_async8(T + slot * W + t, su + t);
-        }
-    };
     for (int r = 0; r < n_req; ++r) {
         const int64_t req = req0 + r;
         SS_PROF(4)
-        // apply(0): the initial frontier's rows, straight from L2 with cp.async (all copies in flight at once).
-        // From the second request on they were issued as soon as the previous request's last boundary had
-        // released T, so they land during that request's epilogue.
-        if (r == 0) issue_initial_rows();
-        {
+        // apply(0): the initial frontier's rows, bulk-copied into T by the producer warp as soon as the previous
+        // request's last boundary had released T, so they land during that request's epilogue.
+        if (misc[0] == SS_OK) {
             const BlkMeta m = bm[0];
             for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
-        }
-        cp_async_wait_all();                                    // also lands the prefetched release slot
-        consumer_sync(NC);
-        if (window > 0 && req >= window) {
-            const int cnt = rel[0];
-            for (int k = tid; k < cnt; k += NC) occ_s[rel[1 + k]] -= 1;
-        }
-        consumer_sync(NC);
-        for (int g = tid; g < ng; g += NC) {
-            const int o = occ_s[g];
-            if (o < 0 || o >= R.occpow_len) {
-                atomicExch((int*)&misc[0], o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT);
-                misc[1] = g;
+            cp_async_wait_all();                                // the prefetched release slot
+            mbar_wait(rows_bar, (uint32_t)(r & 1));             // the initial rows
+            consumer_sync(NC);
+            if (window > 0 && req >= window) {
+                const int cnt = rel[0];
+                for (int k = tid; k < cnt; k += NC) occ_s[rel[1 + k]] -= 1;
             }
-            const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
-            tau_g[g] = base_s[g] * (oc < A.pow_len ? pow_s[oc] : R.occpow[oc]);
+            consumer_sync(NC);
+            for (int g = tid; g < ng; g += NC) {
+                const int o = occ_s[g];
+                if (o < 0 || o >= R.occpow_len) {
+                    atomicExch((int*)&misc[0], o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT);
+                    misc[1] = g;
+                }
+                const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
+                tau_g[g] = base_s[g] * (oc < A.pow_len ? pow_s[oc] : R.occpow[oc]);
+            }
+            if (tid == 0) misc[2] = 0;
         }
-        if (tid == 0) misc[2] = 0;
-        consumer_sync(NC);
-        if (misc[0] != SS_OK) { drain(); break; }
+        all_sync(NT);                                           // request start (the producer joins)
+        if (misc[0] != SS_OK) break;
 
         SS_PROF(0)
         double* cw = cost_w + warp * CW_LEN;
@@ -547,23 +560,19 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
             const int rs = col_len[b];
             const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
             stage_sources(b, p0, n, cw, rw);
-            // ---- relax boundary b over this warp's sources (4 per step: 2x LDS.128 cost, 1x LDS.128 rows) --
+            // ---- relax boundary b over this warp's sources (2 per step: LDS.128 costs, LDS.64 rows) ------
             double v[DPL];
             int ix[DPL];
 #pragma unroll
             for (int d = 0; d < DPL; ++d) { v[d] = INF; ix[d] = PART_NONE; }
             const char* Tb = reinterpret_cast<const char*>(T + lane);
 #pragma unroll 4
-            for (int k = 0; k < n; k += 4) {
+            for (int k = 0; k < n; k += 2) {
                 const double2 c01 = *reinterpret_cast<const double2*>(cw + k);
-                const double2 c23 = *reinterpret_cast<const double2*>(cw + k + 2);
-                const int4 r4 = *reinterpret_cast<const int4*>(rw + k);
-                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.x), c01.x, p0 + k, v, ix);
-                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.y), c01.y, p0 + k + 1, v, ix);
-                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.z), c23.x, p0 + k + 2, v, ix);
-                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r4.w), c23.y, p0 + k + 3, v, ix);
+                const int2 r2 = *reinterpret_cast<const int2*>(rw + k);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r2.x), c01.x, p0 + k, v, ix);
+                relax_row<DPL>(reinterpret_cast<const double*>(Tb + r2.y), c01.y, p0 + k + 1, v, ix);
             }
-            __syncwarp();
             {
                 double* pv = part_v + (b & 1) * NW * SC + warp * SC;
                 int16_t* pi = part_i + (b & 1) * NW * SC + warp * SC;
@@ -574,13 +583,11 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
                 }
             }
             SS_PROF(1)
-            if (b + 1 < nblk) apply(b + 1);
-            SS_PROF(2)
-            consumer_sync(NC);
+            all_sync(NT);                                       // boundary b (the producer has applied b+1)
             SS_PROF(3)
         }
 
-        if (r + 1 < n_req) issue_initial_rows();               // T is no longer read by this request
+        SS_PROF(7)
         // ---- last column: costs, argmin (first index), backtrack ----------------
         {
             const int rs = col_len[nblk];
@@ -598,6 +605,19 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
             if (lane == 0) { red_v[warp] = v; red_i[warp] = idx; }
         }
         consumer_sync(NC);
+        // backtrack, segment-parallel: warp w owns boundaries [w*nblk/NW, (w+1)*nblk/NW); its lanes walk the
+        // backpointers down from EVERY position of the segment's top layer at once (seg_end[w][start]); then the
+        // true segment starts chain from the final argmin through seg_end (NW lookups), and each warp re-walks
+        // its segment from its true start writing the picks -- ~2 x (nblk / NW) dependent steps instead of nblk
+        {
+            const int blo = warp * nblk / NW, bhi = (warp + 1) * nblk / NW;
+            for (int st = lane; st < SC; st += 32) {
+                int p = st;
+                for (int b = bhi - 1; b >= blo; --b) p = min((int)bp[b * SC + p], SC - 1);   // rows past a column
+                seg_end[warp * SC + st] = (uint8_t)p;                                       // hold stale bytes
+            }
+        }
+        consumer_sync(NC);
         if (tid == 0) {
             double v = red_v[0];
             int idx = red_i[0];
@@ -607,15 +627,25 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
             } else {
                 int p = idx;
                 picks[nl - 1] = p;
-                for (int b = nblk - 1; b >= 0; --b) {
-                    p = bp[b * SC + p];
-                    picks[b] = p;
+                for (int w = NW - 1; w >= 0; --w) {
+                    seg_start[w] = p;
+                    p = seg_end[w * SC + p];
                 }
             }
             if (R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
         }
         consumer_sync(NC);
-        if (misc[0] != SS_OK) { drain(); break; }
+        if (lane == 0 && misc[0] == SS_OK) {
+            const int blo = warp * nblk / NW, bhi = (warp + 1) * nblk / NW;
+            int p = seg_start[warp];
+            for (int b = bhi - 1; b >= blo; --b) {
+                p = bp[b * SC + p];
+                picks[b] = p;
+            }
+        }
+        consumer_sync(NC);
+        SS_PROF(5)
+        if (misc[0] != SS_OK) continue;                        // the next request-start barrier ends the launch
 
         const int tag = (int)(req & 0x3fffffff) + 1;
         int* slot = window > 0 ? ring + (int64_t)(req % window) * ring_stride : nullptr;
@@ -640,13 +670,14 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
         if (tid == 0 && slot) slot[0] = misc[2];
         consumer_sync(NC);
         if (r + 1 < n_req) prefetch_release(req + 1);
+        SS_PROF(6)
         ++done;
     }
     cp_async_wait_all();
     SS_PROF(4)
 #undef SS_PROF
     if (A.prof && lane == 0)
-        for (int k = 0; k < 6; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
+        for (int k = 0; k < 8; ++k) atomicAdd(&A.prof[warp * 8 + k], pacc[k]);
     for (int g = tid; g < ng; g += NC) R.st.occ[gbase + g] = occ_s[g];
     if (tid == 0) {
         R.st.next_req[dag] = req0 + done;
@@ -697,14 +728,24 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
     const int dpl = s_cap / 32;
     // 4 source ranges: measured best on B200 (C4: 2.8e6 sel/s vs 2.65e6 with 8 -- the per-position merge of
     // NW partials and the per-warp fixed costs outgrow the shorter relax loops)
-    const int nw = 4;
+    // 4 source ranges: measured best on B200 with the in-warp apply (C4: 2.8e6 sel/s vs 2.65e6 with 8 -- the
+    // per-position merge of NW partials and the per-warp fixed costs outgrow the shorter relax loops);
+    // SS_SLOT_NW = 6 / 8 selects the wider split at DPL = 3 (experiments)
+    int nw = 4;
+    if (const char* e = getenv("SS_SLOT_NW")) {
+        const int v = atoi(e);
+        if ((v == 6 || v == 8) && dpl == 3) nw = v;
+    }
     SlotArgs A{};
     A.meta = meta;
     A.meta_stride = meta_stride;
     A.stream = stream;
     A.stream_stride = stream_stride;
     A.s_rows = s_rows;
-    A.w = s_rows | 1;                                   // odd row pitch: column writes are conflict-free
+    // row pitch >= s_rows with W = 2 (mod 4): rows are 16-B aligned (bulk copies land the initial rows straight in
+    // T) and the producer's column writes see at most 2-way bank conflicts
+    A.w = s_rows;
+    while (A.w % 4 != 2) ++A.w;
     MetaLayout ml{D.max_layers - 1, s_cap, D.max_gpus};
     A.meta_bytes = ml.bytes();
     auto layout = [&](int nbuf, int stage) {
@@ -732,6 +773,7 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
         A.off_rel = o;     o += align_up((D.max_layers + 1) * 4, 16);
         A.off_coff = o;    o += align_up(D.max_layers * 4, 16);
         A.off_costw = o;   o += nw * (s_cap / nw + 8) * 12;
+        A.off_seg = o;     o += align_up(nw * s_cap + nw * 4, 16);
         A.total = o;
     };
     // two CTAs per SM when the staging ring can shrink to fit (>= 2 buffers of >= one unit);
@@ -770,11 +812,12 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
             cudaStreamSynchronize(s);
             fprintf(stderr, "slot prof: smem=%d nbuf=%d stage=%d s_rows=%d | per CTA-request cycles, by warp:\n",
                     A.total, A.nbuf, A.stage_bytes, A.s_rows);
-            for (int w = 0; w < 9; ++w) {
+            for (int w = 0; w <= nw; ++w) {
                 const double d = (double)D.n_dags * n_req;
-                fprintf(stderr, "  w%d prologue %.0f relax %.0f apply %.0f (of which TMA wait %.0f) barrier %.0f epilogue %.0f\n",
-                        w, h[w * 8 + 0] / d, h[w * 8 + 1] / d, h[w * 8 + 2] / d, h[w * 8 + 5] / d, h[w * 8 + 3] / d,
-                        h[w * 8 + 4] / d);
+                fprintf(stderr, "  w%d prologue %.0f relax %.0f apply %.0f barrier %.0f | epilogue: initial-rows %.0f "
+                        "argmin+backtrack %.0f chain-update %.0f rest %.0f\n",
+                        w, h[w * 8 + 0] / d, h[w * 8 + 1] / d, h[w * 8 + 2] / d, h[w * 8 + 3] / d, h[w * 8 + 7] / d,
+                        h[w * 8 + 5] / d, h[w * 8 + 6] / d, h[w * 8 + 4] / d);
             }
             cudaFree(A.prof);
         }
@@ -783,7 +826,10 @@ extern "C" int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int6
     switch (dpl) {
         case 1: return run(replay_slots_kernel<1, 4>, 5 * 32);
         case 2: return run(replay_slots_kernel<2, 4>, 5 * 32);
-        case 3: return run(replay_slots_kernel<3, 4>, 5 * 32);
+        case 3:
+            if (nw == 6) return run(replay_slots_kernel<3, 6>, 7 * 32);
+            if (nw == 8) return run(replay_slots_kernel<3, 8>, 9 * 32);
+            return run(replay_slots_kernel<3, 4>, 5 * 32);
         case 4: return run(replay_slots_kernel<4, 4>, 5 * 32);
         case 5: return run(replay_slots_kernel<5, 4>, 5 * 32);
         case 6: return run(replay_slots_kernel<6, 4>, 5 * 32);

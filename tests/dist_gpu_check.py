@@ -62,6 +62,8 @@ def main():
         all_ids = np.arange(V)
         want = sweep_best([scen.bench_variants(1, 256, 80, seed0=int(v))[0] for v in all_ids], all_ids)
         report["argmax"] = {"variants": V, "winner": got_abi[1], "objective": got_abi[0].hex(),
+                            "single_gpu": [want[0].hex(), int(want[1])], "torch": [float(got_torch[0]).hex(),
+                                                                                  int(got_torch[1])],
                             "abi_matches_single_gpu": got_abi == want, "torch_matches_single_gpu": got_torch == want}
         ok &= got_abi == want and got_torch == want
 

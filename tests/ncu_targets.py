@@ -1,6 +1,9 @@
 """Ad-hoc ncu targets (not a test): one launch of a chosen kernel family at its bench shape.
 
-    ncu --set full -k regex:<kernel> -c 1 python tests/ncu_targets.py <admission|sim|exact|cover|warp>
+    ncu --set full -k regex:<kernel> -c 1 python tests/ncu_targets.py <admission|sim|exact|cover|warp|slots|blocks|c5>
+
+``slots`` / ``blocks``: bench.py's own headline launch (C4 pool, 1,184 device-churned scenarios, 64 requests, W=64),
+launched twice -- profile the second (``-s 1 -c 1``), whose requests 64..127 run the steady state.
 """
 import os
 import sys
@@ -28,6 +31,23 @@ def main(what):
         else:
             rp = ScenarioReplayer(ss, window=64, mode="warp")
             rp.run(64)
+    elif what in ("slots", "blocks"):
+        cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
+        plan = allocate(cl, model)
+        S = 1184
+        ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=list(range(S)), host_events=False)
+        rp = ScenarioReplayer(ss, window=64, mode=what)
+        out = rp.run(64)
+        rp.run(64, out=out)
+    elif what == "c5":
+        pools = scen.c5_pools(0)
+        name, cl, model = pools[2]                                   # 70B: L=80 over 384 GPUs
+        plan = allocate(cl, model)
+        S = 1184
+        ss = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=list(range(S)), host_events=False)
+        rp = ScenarioReplayer(ss, window=64, mode=os.environ.get("SS_MODE", "auto"))
+        out = rp.run(64)
+        rp.run(64, out=out)
     elif what == "exact":
         packed, _ = scen.bench_variants(256, 64, 64, seed0=0)      # C2-shaped pools: 16 GPUs per region
         VariantSweep(packed, fill_all=True).run()
