@@ -263,24 +263,25 @@ def run_ours(args):
     if args.mode == "slots":
         stream_b = float(rp.stream_bytes_per_selection())
         kernel_name = "replay_slots_kernel<3,4> (ss_replay_slots)"
-        traffic_key = "slots_dram_bytes_per_selection"
-        bound_note = ("algorithmic bytes B2 (the fp64 RTT entries the DP reads) per launch / launch time. The RTT "
-                      "tile is reused from shared memory, so only %.0f KB per selection (entering GPUs' rows and "
-                      "columns) cross L2/HBM; the kernel is issue-bound (DESIGN.md)" % (stream_b / 1e3))
+        bound_note = ("achieved = algorithmic bytes B2 (the fp64 RTT entries the DP reads) per launch / launch time. "
+                      "The kernel reads them from its shared-memory RTT tile: only %.0f KB per selection (entering "
+                      "GPUs' rows and columns) cross L2/HBM, so frac can exceed 1 and HBM is not what binds it. It is "
+                      "bound by instruction issue and shared-memory wavefronts (the ncu block: issue active, smem "
+                      "wavefronts per SM cycle, warp instructions per selection; DESIGN.md)" % (stream_b / 1e3))
     else:
         stream_b = float(b2.mean())
         kernel_name = "chain_dp_kernel<3,true> (ss_replay)"
-        traffic_key = "replay_dram_bytes_per_selection"
         bound_note = "algorithmic bytes B2 per launch / launch time; every edge block streams from HBM once"
 
     # ---- e2e: host descriptors in, host results out ---------------------------
     seeds_h = torch.from_numpy(ss.seeds.copy()).pin_memory()
     cost_h = torch.empty((S, R), dtype=torch.float64).pin_memory()
     hash_h = torch.empty((S, R), dtype=torch.int64).pin_memory()
+    gpus_h = torch.empty((S, R, 64), dtype=torch.int16).pin_memory()     # the chains themselves: int16 host[L]
     rp2 = ScenarioReplayer(ss, window=W, stream=stream, mode=args.mode)
     with torch.cuda.stream(stream):
         def e2e_step():
-            rp2.run_from_host(None, seeds_h, R, cost_h, hash_h)
+            rp2.run_from_host(None, seeds_h, R, cost_h, hash_h, gpus_h)
         t_e2e = timed(e2e_step, max(2, args.steps // 2), args.warmup, stream, barrier, reduce_max)
     e2e_steps = max(2, args.steps // 2)
     torch.cuda.synchronize()
@@ -372,18 +373,17 @@ def run_ours(args):
                        "bytes_per_selection_B2": float(b2.mean())},
             "e2e": {"value": e2e_value, "unit": "selections/s",
                     "h2d_bytes_per_step": int(seeds_h.numel() * 8),
-                    "d2h_bytes_per_step": int(cost_h.numel() * 8 + hash_h.numel() * 8),
-                    "path": "ScenarioReplayer.run_from_host: H2D scenario seeds, device membership events + DAG "
-                            "build, replay, D2H results",
+                    "d2h_bytes_per_step": int(cost_h.numel() * 8 + hash_h.numel() * 8 + gpus_h.numel() * 2 +
+                                              (S * 8 if args.mode == "slots" else 0)),
+                    "path": "ScenarioReplayer.run_from_host: H2D scenario seeds, ss_replay_reset (cudaMemsetAsync), "
+                            "device membership events + DAG build (+ the slot program's used-slot count, D2H), "
+                            "replay, D2H of every selection's cost, chain hash and chain (int16 host[L])",
                     "matches_device_run": e2e_ok},
             "gpu_launches": args.steps,
             "chain_checksum": "%016x" % checksum,
             "chain_gather": gather,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": _traffic(traffic_key, sel_per_step_rank), "peak_source": peak_src,
-                         "kernel": kernel_name, "note": bound_note,
-                         "l2_hbm_bytes_per_selection": stream_b,
-                         "algorithmic_bytes_per_launch": float(b2.mean()) * sel_per_step_rank},
+            "roofline": _roofline(args.mode, S, R, achieved, hbm, peak_src, kernel_name, bound_note, stream_b,
+                                  float(b2.mean()) * sel_per_step_rank, launch_s),
             "clocks": clk,
             "phase2_alt": alt,
             "cpu_baseline": cpu,
@@ -819,14 +819,41 @@ def _variants_for_rank(scen, V, rank, world, layers=80):
     return PackedVariants(pools, of, orr, np.array(var_ptr), p0.fpl, p0.layers, p0.tokens, p0.alpha), meta
 
 
-def _traffic(key, selections_per_launch):
-    """DRAM bytes per launch from the committed ncu capture (per selection x selections per launch)."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def _ncu_launch(mode, S, R):
+    """The committed ncu --set full capture of THIS launch shape (profiles/ncu_bench_launch.json, written by
+    profiles/ncu_to_json.py from `ncu ... python tests/ncu_targets.py <mode>`), or None if the shapes differ."""
+    path = os.path.join(ROOT, "profiles", "ncu_bench_launch.json")
     try:
         with open(path) as fh:
-            return json.load(fh)[key] * selections_per_launch
+            rec = json.load(fh)[mode]
     except Exception:
         return None
+    return rec if (rec["scenarios"], rec["requests"]) == (S, R) else None
+
+
+def _roofline(mode, S, R, achieved, hbm, peak_src, kernel_name, note, stream_b, algo_bytes, launch_s):
+    nc = _ncu_launch(mode, S, R)
+    out = {"bound": "issue" if mode == "slots" else "hbm",
+           "achieved": achieved, "achieved_kind": "algorithmic bytes B2 per launch / CUDA-event launch time",
+           "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+           "frac_kind": "algorithmic-byte fraction of the measured HBM copy bandwidth",
+           "traffic": nc["traffic_bytes"] if nc else None,
+           "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this "
+                              "launch shape (%d scenarios x %d requests), %s" % (S, R, nc["summary"])) if nc else None,
+           "peak_source": peak_src, "kernel": kernel_name, "note": note,
+           "l2_hbm_bytes_per_selection": stream_b, "algorithmic_bytes_per_launch": algo_bytes,
+           "launch_ms": 1e3 * launch_s}
+    if nc:
+        out["ncu"] = {"issue_active_pct": nc["issue_active_pct"],
+                      "warp_execution_efficiency": nc["warp_execution_efficiency"],
+                      "smem_bank_conflicts_per_launch": nc["smem_bank_conflicts"],
+                      "smem_wavefronts_per_sm_cycle": nc["smem_wavefronts_per_sm_cycle"],
+                      "warp_instructions_per_selection": nc["per_selection"]["warp_instructions"],
+                      "smem_wavefronts_per_selection": nc["per_selection"]["smem_wavefronts"],
+                      "dram_bytes_per_selection": nc["per_selection"]["dram_bytes"],
+                      "l2_hit_pct": nc["l2_hit_pct"], "fp64_pipe_pct": nc["fp64_pipe_pct"],
+                      "duration_ms_under_ncu": nc["duration_ms"]}
+    return out
 
 
 def _resident_bytes(rp):

@@ -134,6 +134,11 @@ typedef struct ss_replay_out {
 int ss_replay(const ss_dag_set* dags, const ss_replay_state* st, const double* occpow, int32_t occpow_len,
               int32_t window, int32_t n_req, const ss_replay_out* out, void* stream);
 
+/* Fresh replay state (stream-ordered cudaMemsetAsync, no kernel): occupancy [n_gpus_total], release ring
+ * [ring_ints], next_req / status / aux [n_dags] -- what a new batch of scenario states starts from (the e2e call
+ * of the reference-facing path re-uses one allocation for every batch). */
+int ss_replay_reset(const ss_replay_state* st, int32_t n_dags, int64_t n_gpus_total, int64_t ring_ints, void* stream);
+
 /* Membership churn on device (membership.py:303-357).
  * One CTA per scenario replays the scenario's events on the base placement:
  *   1. on_leave of want_leave plan GPUs present at the start, visited in

@@ -60,6 +60,7 @@ _SIGS = {
     "ss_select": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ss_replay": (C.c_int, [C.POINTER(DagSet), C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
                             C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
+    "ss_replay_reset": (C.c_int, [C.POINTER(ReplayState), C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
     "ss_set_tiling": (C.c_int, [C.c_int32, C.c_int32, i32p, i32p]),
     "ss_slot_meta_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "ss_slot_program": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,

@@ -65,8 +65,45 @@ def _ramp(counts: np.ndarray) -> np.ndarray:
     return np.arange(total, dtype=np.int64) - starts + 1
 
 
+class Upload:
+    """Host arrays packed into ONE pinned staging buffer and copied with ONE H2D (stream-ordered, non-blocking);
+    device views by name.  Small single calls (allocate() on a handful of GPUs) are launch/copy-latency bound,
+    so every input of the call travels together."""
+
+    def __init__(self):
+        self.parts = []
+        self.size = 0
+
+    def add(self, name: str, arr) -> None:
+        arr = np.ascontiguousarray(arr)
+        off = (self.size + 15) // 16 * 16
+        self.parts.append((name, off, arr))
+        self.size = off + arr.nbytes
+
+    def upload(self, dev, stream=None) -> dict:
+        torch = _torch()
+        host = torch.empty(max(self.size, 16), dtype=torch.uint8, pin_memory=True)   # caching host allocator
+        hv = host.numpy()
+        for _, off, arr in self.parts:
+            hv[off:off + arr.nbytes] = arr.view(np.uint8).reshape(-1)
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                dbuf = host.to(dev, non_blocking=True)
+        else:
+            dbuf = host.to(dev, non_blocking=True)
+        tmap = {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
+                np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8}
+        return {name: dbuf[off:off + arr.nbytes].view(tmap[arr.dtype]) for name, off, arr in self.parts}
+
+
 class PoolBatch:
-    def __init__(self, pools=None, *, arrays: Optional[PoolArrays] = None, stream=None):
+    def __init__(self, pools=None, *, arrays: Optional[PoolArrays] = None, stream=None, extra: Optional[dict] = None,
+                 defer_workspace_check: bool = False):
+        """``extra``: further host arrays (name -> ndarray) that ride along in the batch's single H2D copy; their
+        device views are ``self.extra[name]``.  ``defer_workspace_check``: the exact sweep's workspace overflow
+        (SS_WORKSPACE) is detected by fetch(), which grows the caps and replays the logged launches -- no host
+        sync inside stage_counts(); only for callers that always fetch() (allocate())."""
+        self.defer = defer_workspace_check
         torch = _torch()
         A = arrays if arrays is not None else PoolArrays.from_specs(pools)
         self.stream = stream
@@ -108,7 +145,15 @@ class PoolBatch:
             raise ValueError("layer capacities, k_max or pool sizes exceed the device path's int32 range "
                              f"(max {int(ints.max())}); a capacity this large means bytes_per_layer is tiny")
         ints = ints.astype(np.int32)
-        self._ints = torch.from_numpy(ints).to(dev)
+        up = Upload()
+        up.add("ints", ints)
+        up.add("i64", np.concatenate([koff[:-1], memb[:-1], gsz[:-1]]).astype(np.int64))
+        up.add("flops", flops)
+        for name, arr in (extra or {}).items():
+            up.add(name, arr)
+        dv = up.upload(dev, stream)
+        self.extra = {name: dv[name] for name in (extra or {})}
+        self._ints = dv["ints"]
         o = 0
 
         def take(cnt):
@@ -126,22 +171,27 @@ class PoolBatch:
         self.cand_k = take(cand_k.size)
         self.all_pool = take(all_pool.size)
         self.all_k = take(all_k.size)
-        i64 = torch.from_numpy(np.concatenate([koff[:-1], memb[:-1], gsz[:-1]]).astype(np.int64)).to(dev)
+        i64 = dv["i64"]
         self.koff, self.memb_off, self.gsz_off = i64[:P], i64[P:2 * P], i64[2 * P:]
-        self.flops = torch.from_numpy(flops).to(dev)
+        self.flops = dv["flops"]
         K, M, G = int(koff[-1]), int(memb[-1]), int(gsz[-1])
-        # outputs: one zeroed int32 block + one fp64 block (two allocations, two D2H copies in fetch())
+        # outputs: ONE zeroed allocation -- an fp64 block then an int32 block -- read back by ONE D2H in fetch()
         sizes = [("stages", max(K, 1)), ("stall", max(K, 1)), ("kstatus", max(K, 1)), ("fstatus", max(K, 1)),
                  ("members", max(M, 1)), ("counts", max(M, 1)), ("gsize", max(G, 1)), ("status", max(P, 1)),
-                 ("aux", max(P, 1)), ("best_k", max(P, 1)), ("sweep_stats", max(exact.size, 1) * 4)]
-        self._iblock = torch.zeros(sum(c for _, c in sizes), dtype=torch.int32, device=dev)
+                 ("aux", max(P, 1)), ("best_k", max(P, 1)), ("sweep_stats", max(exact.size, 1) * 4),
+                 ("feasible", 1)]
+        nf = max(K, 1) + 1
+        ni = sum(c for _, c in sizes)
+        self._oblock = torch.zeros(nf * 8 + ni * 4, dtype=torch.uint8, device=dev)
+        self._fblock = self._oblock[:nf * 8].view(torch.float64)
+        self._iblock = self._oblock[nf * 8:].view(torch.int32)
         o = 0
         for name, cnt in sizes:
             setattr(self, name, self._iblock[o:o + cnt])
             o += cnt
-        self._fblock = torch.zeros(max(K, 1) + 1, dtype=torch.float64, device=dev)
         self.z = self._fblock[:max(K, 1)]
         self.total = self._fblock[max(K, 1):]              # spare slot: allocate()'s objective_total
+        self._ops = []                                     # launch log: replayed when the exact sweep needs more room
         self.fcap, self.ccap = 4096, 65536
 
     def pool_set(self) -> N.PoolSet:
@@ -150,6 +200,10 @@ class PoolBatch:
 
     # -- stage counts ------------------------------------------------------
     def stage_counts(self) -> None:
+        self._ops = [self._stage_counts]                   # a new launch sequence starts here
+        self._stage_counts()
+
+    def _stage_counts(self) -> None:
         lib = N.lib()
         st = N.stream_handle(self.stream)
         ps = self.pool_set()
@@ -163,36 +217,54 @@ class PoolBatch:
                 "ss_stage_counts_cover")
 
     def _run_exact(self, lib, ps, st) -> None:
+        # a pool whose frontier outgrows the workspace reports SS_WORKSPACE (aux = the size it needed): grow and
+        # rerun here (one host sync), or -- deferred -- in fetch(), which replays the whole launch log
         torch = _torch()
         while True:
             per = int(lib.ss_stage_counts_workspace(self.fcap, self.ccap, 17))
             per = (per + 255) // 256 * 256
-            ws = torch.empty(per * self.exact.size, dtype=torch.uint8, device=self.dev)
+            self._ws = torch.empty(per * self.exact.size, dtype=torch.uint8, device=self.dev)
             N.check(lib.ss_stage_counts_exact(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members),
                                               N.ptr(self.gsize), N.ptr(self.status), N.ptr(self.aux),
-                                              N.ptr(self.exact_list), int(self.exact.size), N.ptr(ws), per,
+                                              N.ptr(self.exact_list), int(self.exact.size), N.ptr(self._ws), per,
                                               self.fcap, self.ccap, N.ptr(self.sweep_stats), st),
                     "ss_stage_counts_exact")
+            if self.defer:
+                return
             status = self.status.cpu().numpy()[self.exact]
             if not (status == SS_WORKSPACE).any():
                 return
             need = int(self.aux.cpu().numpy()[self.exact].max())
-            self.fcap = max(self.fcap * 4, need * 2)
-            self.ccap = max(self.ccap * 4, need * 2)
+            self._grow(need)
             bad = self.exact[status == SS_WORKSPACE]
             self.status[torch.from_numpy(bad).to(self.dev)] = SS_OK
-            if self.ccap > 1 << 24:
-                raise MemoryError("exact sweep frontier exceeds 16M children")
+
+    def _grow(self, need: int) -> None:
+        self.fcap = max(self.fcap * 4, need * 2)
+        self.ccap = max(self.ccap * 4, need * 2)
+        if self.ccap > 1 << 24:
+            raise MemoryError("exact sweep frontier exceeds 16M children")
 
     # -- objective + score + best -----------------------------------------
-    def score_and_best(self, t_comp, rtt, kpow: np.ndarray, fill_all: bool = False) -> None:
+    def score_and_best(self, t_comp, rtt, kpow, fill_all: bool = False) -> None:
         torch = _torch()
+        self._t = t_comp if torch.is_tensor(t_comp) else torch.as_tensor(np.asarray(t_comp, dtype=np.float64)).to(self.dev)
+        self._r = rtt if torch.is_tensor(rtt) else torch.as_tensor(np.asarray(rtt, dtype=np.float64)).to(self.dev)
+        self._kpow = kpow if torch.is_tensor(kpow) else torch.from_numpy(np.asarray(kpow, dtype=np.float64)).to(self.dev)
+        self._fill_all = fill_all
+        self._ops.append(self._score_and_best)
+        self._score_and_best()
+
+    def log_op(self, fn) -> None:
+        """Run a further launch on this batch's outputs and record it for fetch()'s replay."""
+        self._ops.append(fn)
+        fn()
+
+    def _score_and_best(self) -> None:
         lib = N.lib()
         st = N.stream_handle(self.stream)
         ps = self.pool_set()
-        self._t = t_comp if torch.is_tensor(t_comp) else torch.as_tensor(np.asarray(t_comp, dtype=np.float64)).to(self.dev)
-        self._r = rtt if torch.is_tensor(rtt) else torch.as_tensor(np.asarray(rtt, dtype=np.float64)).to(self.dev)
-        self._kpow = torch.from_numpy(np.asarray(kpow, dtype=np.float64)).to(self.dev)
+        fill_all = self._fill_all
         N.check(lib.ss_phase1_score(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members), N.ptr(self.gsize),
                                     N.ptr(self._t), N.ptr(self._r), N.ptr(self._kpow), int(self._kpow.numel()),
                                     int(fill_all), N.ptr(self.z), N.ptr(self.counts), N.ptr(self.kstatus),
@@ -204,7 +276,16 @@ class PoolBatch:
 
     # -- host views ---------------------------------------------------------
     def fetch(self) -> "PoolResults":
-        return PoolResults(self)
+        res = PoolResults(self)
+        while self.exact.size:
+            st = res.status[self.exact]
+            if not (st == SS_WORKSPACE).any():
+                break
+            self._grow(int(res.aux[self.exact].max()))
+            for op in self._ops:                           # validate resets status / aux / stages
+                op()
+            res = PoolResults(self)
+        return res
 
 
 class PoolResults:
@@ -212,9 +293,12 @@ class PoolResults:
 
     def __init__(self, b: PoolBatch):
         self.b = b
-        ib = b._iblock.cpu().numpy()
-        fb = b._fblock.cpu().numpy()
-        view = lambda t: ib[t.storage_offset(): t.storage_offset() + t.numel()]
+        ob = b._oblock.cpu().numpy()                       # the one D2H of the call
+        nf = b._fblock.numel()
+        fb = ob[:nf * 8].view(np.float64)
+        ib = ob[nf * 8:].view(np.int32)
+        ibase = b._iblock.storage_offset()             # in int32 elements
+        view = lambda t: ib[t.storage_offset() - ibase: t.storage_offset() - ibase + t.numel()]
         self.stages = view(b.stages)
         self.members = view(b.members)
         self.gsize = view(b.gsize)
@@ -225,6 +309,7 @@ class PoolResults:
         self.sweep_stats = view(b.sweep_stats).reshape(-1, 4)
         self.z = fb[:b.z.numel()]
         self.total = float(fb[-1])
+        self.feasible = int(view(b.feasible)[0])
 
     def raise_pool(self, p: int) -> None:
         st = int(self.status[p])
@@ -295,14 +380,20 @@ def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int
             lv.append(v)
     st = N.stream_handle(stream)
     I = len(items)
-    ints = torch.from_numpy(np.concatenate([item_ptr, n, layers, li, la, lb]).astype(np.int32)).to(dev)
+    nl = len(li)
+    up = Upload()                                          # one H2D for every input of the call
+    up.add("ints", np.concatenate([item_ptr, n, layers, li, la, lb]).astype(np.int32))
+    up.add("off", mat_off[:-1].astype(np.int64))
+    up.add("lv", np.asarray(lv if nl else [0.0], dtype=np.float64))
+    up.add("flops", flops)
+    dv = up.upload(dev, stream)
+    ints = dv["ints"]
     item_ptr_d, dim_d = ints[:I + 1], ints[I + 1:2 * I + 1]
     layers_d = ints[2 * I + 1:3 * I + 1]
-    nl = len(li)
     li_d, la_d, lb_d = ints[3 * I + 1:3 * I + 1 + nl], ints[3 * I + 1 + nl:3 * I + 1 + 2 * nl], ints[3 * I + 1 + 2 * nl:]
-    off_d = torch.from_numpy(mat_off[:-1].astype(np.int64)).to(dev)
-    lv_d = torch.from_numpy(np.asarray(lv, dtype=np.float64)).to(dev) if nl else None
-    flops_d = torch.from_numpy(flops).to(dev)
+    off_d = dv["off"]
+    lv_d = dv["lv"] if nl else None
+    flops_d = dv["flops"]
     rtt = torch.empty(max(int(mat_off[-1]), 1), dtype=torch.float64, device=dev)
     if I > 65535:
         raise ValueError("at most 65535 objective regions per call")

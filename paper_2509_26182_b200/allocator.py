@@ -166,25 +166,27 @@ def allocate(cluster: ClusterSnapshot, model: ModelSpec, *, alpha: float = 1.0,
     if not packed:
         raise NoFeasiblePipeline(f"no region can host all {L} layers of {model.name!r}")
     pools = [PoolSpec(oc, [g.flops for g in og], L, km) for _, _, og, oc, km in packed]
-    batch = PoolBatch(pools)
+    a = params.alpha if params is not None else alpha
+    # k ** alpha table and the variant pointer ride along in the batch's single H2D copy
+    batch = PoolBatch(pools, extra={"kpow": _kpow_table(max(p.kmax for p in pools), a),
+                                    "var_ptr": np.array([0, len(pools)], dtype=np.int32)},
+                      defer_workspace_check=True)
     batch.stage_counts()
     if params is not None:
-        a = params.alpha
         t = np.full(len(pools), params.t_comp_seconds)
         r = np.full(len(pools), params.rtt_seconds)
     else:
-        a = alpha
         t, r = objective_device(_region_items(cluster, [p[1] for p in packed]), cluster.default_cross_region_rtt_s,
                                 model.flops_per_layer_per_token, [L] * len(pools), mean_tokens_per_request)
-    batch.score_and_best(t, r, _kpow_table(int(batch.km.max()), a))
+    batch.score_and_best(t, r, batch.extra["kpow"])
     # objective_total: the reference's left fold over regions (allocator.py:588), on device
     lib = N.lib()
-    dev = batch.dev
-    var_ptr = torch.tensor([0, len(pools)], dtype=torch.int32, device=dev)
-    feas = torch.empty(1, dtype=torch.int32, device=dev)
-    N.check(lib.ss_variant_reduce(1, N.ptr(var_ptr), N.ptr(batch.koff), N.ptr(batch.best_k), N.ptr(batch.z),
-                                  N.ptr(batch.status), N.ptr(batch.total), N.ptr(feas), None, None,
-                                  N.stream_handle()), "ss_variant_reduce")
+
+    def reduce():
+        N.check(lib.ss_variant_reduce(1, N.ptr(batch.extra["var_ptr"]), N.ptr(batch.koff), N.ptr(batch.best_k),
+                                      N.ptr(batch.z), N.ptr(batch.status), N.ptr(batch.total), N.ptr(batch.feasible),
+                                      None, None, N.stream_handle()), "ss_variant_reduce")
+    batch.log_op(reduce)
     res = batch.fetch()
     pipelines: List[Pipeline] = []
     per_k: List[PerKEntry] = []

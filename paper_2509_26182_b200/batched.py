@@ -296,27 +296,31 @@ class ScenarioReplayer:
                                       ro, N.stream_handle(self.stream)), "ss_replay")
         return out
 
-    def run_from_host(self, leave_h, seeds_h, n_req: int, cost_h, hash_h) -> ReplayResult:
+    def run_from_host(self, leave_h, seeds_h, n_req: int, cost_h, hash_h, gpus_h=None) -> ReplayResult:
         """End-to-end call: host scenario descriptors in, host per-request results out.
 
         leave_h [S, N] uint8 (None when the scenario events are generated on
         the device) and seeds_h [S] int64 (pinned) are copied to the device,
-        the scenario DAGs are rebuilt (membership events, columns, edge blocks
-        or slot program), replay state is reset, n_req requests are routed per
-        scenario and the costs / chain hashes come back into pinned cost_h /
-        hash_h.  Stream-ordered; the caller synchronises.
+        the replay state is reset inside the C ABI (ss_replay_reset:
+        cudaMemsetAsync, no kernel), the scenario DAGs are rebuilt (membership
+        events, columns, edge blocks or slot program), n_req requests are
+        routed per scenario and the costs / chain hashes -- and with gpus_h
+        [S, n_req, L] int16 the chains themselves -- come back into pinned
+        host buffers.  Stream-ordered; the caller synchronises.
         """
         if leave_h is not None:
             self.leave.copy_(leave_h, non_blocking=True)
         self.seeds.copy_(seeds_h, non_blocking=True)
-        self.occ.zero_()
-        self.ring.zero_()
-        self.next_req.zero_()
-        self.status.zero_()
+        st = N.ReplayState(N.ptr(self.gpu_ptr), N.ptr(self.base_tau), N.ptr(self.occ), N.ptr(self.ring),
+                           N.ptr(self.next_req), N.ptr(self.status), N.ptr(self.aux))
+        N.check(N.lib().ss_replay_reset(st, self.S, self.occ.numel(), self.ring.numel(), N.stream_handle(self.stream)),
+                "ss_replay_reset")
         self.build()
-        out = self.run(n_req)
+        out = self.run(n_req, gpus=gpus_h is not None)
         cost_h.copy_(out.cost, non_blocking=True)
         hash_h.copy_(out.chain_hash, non_blocking=True)
+        if gpus_h is not None:
+            gpus_h.copy_(out.gpus, non_blocking=True)
         return out
 
     def triggers(self, *, cov_threshold: float = 0.5, mix_alpha: float = 0.5, kv_reserved=None):

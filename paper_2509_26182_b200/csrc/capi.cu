@@ -27,3 +27,16 @@ extern "C" int ss_limits(int32_t* max_hosts_h, int32_t* max_layers_h, int32_t* m
     if (max_gpus_h) *max_gpus_h = SS_MAX_GPUS;
     return SS_OK;
 }
+
+extern "C" int ss_replay_reset(const ss_replay_state* st, int32_t n_dags, int64_t n_gpus_total, int64_t ring_ints,
+                               void* stream_h) {
+    if (!st || n_dags < 0 || n_gpus_total < 0 || ring_ints < 0) return SS_BAD_INPUT;
+    cudaStream_t s = ss_stream(stream_h);
+    if ((n_gpus_total && cudaMemsetAsync(st->occ, 0, sizeof(int32_t) * (size_t)n_gpus_total, s) != cudaSuccess) ||
+        (ring_ints && cudaMemsetAsync(st->ring, 0, sizeof(int32_t) * (size_t)ring_ints, s) != cudaSuccess) ||
+        (n_dags && (cudaMemsetAsync(st->next_req, 0, sizeof(int64_t) * (size_t)n_dags, s) != cudaSuccess ||
+                    cudaMemsetAsync(st->status, 0, sizeof(int32_t) * (size_t)n_dags, s) != cudaSuccess ||
+                    (st->aux && cudaMemsetAsync(st->aux, 0, sizeof(int32_t) * (size_t)n_dags, s) != cudaSuccess))))
+        return SS_CUDA_ERROR;
+    return SS_OK;
+}
