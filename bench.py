@@ -421,6 +421,8 @@ def chain_gather_check(ex, cl, model, plan, rank, world, stream, R, W, mode, per
         out = rp.run(R, gpus=True)
         rp.raise_first_failure()
         torch.cuda.synchronize()
+        ex.gather_chains(out.gpus, out.cost, dst=0)          # warm-up: NCCL sets up the p2p channels lazily
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         g, c = ex.gather_chains(out.gpus, out.cost, dst=0)

@@ -384,6 +384,17 @@ int ss_replay_slots(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_st
                     const ss_replay_out* out, void* stream_h);
 int ss_set_slot_staging(int32_t stage_bytes, int32_t n_buffers);
 
+/* Cluster slot replay: the same program (ss_slot_program), state, outputs and op script as ss_replay_slots,
+ * for frontiers too wide for two single-CTA tiles per SM.  A thread-block cluster of
+ * ceil(s_rows / (32 * dplc)) <= 8 CTAs shares each scenario: CTA q keeps every source row of the tile but only
+ * its own 32 * dplc destination slots, so it owns complete destination minima; each boundary's costs are
+ * broadcast to the cluster through distributed shared memory (one barrier.cluster per boundary) and CTA 0
+ * holds the backpointers and runs the request epilogue.  dplc = 1 or 2 (0: default 1, env SS_CLUSTER_DPL). */
+int ss_replay_slots_cluster(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_stride, const double* stream,
+                            int64_t stream_stride, int32_t s_cap, int32_t s_rows, const ss_replay_state* st,
+                            const double* occpow, int32_t occpow_len, int32_t window, int32_t n_req,
+                            const ss_replay_out* out, int32_t dplc, void* stream_h);
+
 /* Kernel tuning knobs (0 = default); returns previous values via *_h. */
 int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
 /* Constructive stage counts: batches of at most max_candidates (pool, k) candidates try every group count in

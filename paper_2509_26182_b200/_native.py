@@ -69,6 +69,9 @@ _SIGS = {
     "ss_replay_slots": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_int32, C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(ReplayOut), C.c_void_p]),
+    "ss_replay_slots_cluster": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+                                          C.c_int32, C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
+                                          C.c_int32, C.POINTER(ReplayOut), C.c_int32, C.c_void_p]),
     "ss_set_slot_staging": (C.c_int, [C.c_int32, C.c_int32]),
     "ss_set_cover_parallel_limit": (C.c_int32, [C.c_int32]),
     "ss_replay_warp_smem": (C.c_int64, [C.POINTER(DagSet), C.c_int32, C.c_int32, C.c_int32]),

@@ -69,7 +69,7 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
         mode = "warp" if warp_ok else ("slots" if s_cap <= 96 else "blocks")
     if mode == "warp" and not warp_ok:
         raise ValueError("warp mode needs <= 32 hosts per layer and edges + ring within 227 KB of shared memory")
-    if L < 2 and mode == "slots":
+    if L < 2 and mode in ("slots", "cluster"):
         mode = "blocks"                      # no boundaries: nothing to tile
     return mode, cap, s_cap, occ_len
 
@@ -103,13 +103,14 @@ class ScenarioReplayer:
     def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
                  max_requests: Optional[int] = None, stream=None, mode: str = "auto"):
         """mode "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
-        bytes); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "warp": one warp per scenario
+        bytes); "cluster": the same tile split by destination slots over a thread-block cluster of CTAs
+        (ss_replay_slots_cluster; wide frontiers); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "warp": one warp per scenario
         with its edge blocks resident in shared memory (ss_replay_warp; columns <= 32 hosts); "auto":
         warp when it qualifies, else slots while the tile leaves room for two CTAs per SM (<= 96 slots),
         else blocks.  All modes give bit-identical results."""
         import torch
-        if mode not in ("slots", "blocks", "warp", "auto"):
-            raise ValueError(f"mode must be 'slots', 'blocks', 'warp' or 'auto', got {mode!r}")
+        if mode not in ("slots", "cluster", "blocks", "warp", "auto"):
+            raise ValueError(f"mode must be 'slots', 'cluster', 'blocks', 'warp' or 'auto', got {mode!r}")
         self.torch = torch
         self.scen = scen
         self.window = int(window)
@@ -218,7 +219,7 @@ class ScenarioReplayer:
                                         N.ptr(self.leave), N.ptr(self.col_off), N.ptr(self.col_len),
                                         N.ptr(self.node_gpu), N.ptr(self.status), N.ptr(self.aux), st),
                 "ss_scenario_columns")
-        if self.mode == "slots":
+        if self.mode in ("slots", "cluster"):
             N.check(lib.ss_slot_program(self.S, self.L, self.G, N.ptr(lo_p), N.ptr(hi_p), stride,
                                         N.ptr(self.leave), N.ptr(self.base_rtt),
                                         N.ptr(self.seeds) if self.scen.jitter else None, self.s_cap, self.meta_stride,
@@ -286,6 +287,12 @@ class ScenarioReplayer:
                                             self.stream_stride, self.s_cap, self.s_rows, st, N.ptr(self.occpow),
                                             self.occpow_len, self.window, n_req, ro, N.stream_handle(self.stream)),
                     "ss_replay_slots")
+        elif self.mode == "cluster":
+            N.check(N.lib().ss_replay_slots_cluster(self.dag_set(), N.ptr(self.meta), self.meta_stride,
+                                                    N.ptr(self.stream_buf), self.stream_stride, self.s_cap,
+                                                    self.s_rows, st, N.ptr(self.occpow), self.occpow_len, self.window,
+                                                    n_req, ro, 0, N.stream_handle(self.stream)),
+                    "ss_replay_slots_cluster")
         elif self.mode == "warp":
             mat = self._warp_mats()
             N.check(N.lib().ss_replay_warp(self.dag_set(), st, N.ptr(self.occpow), self.occpow_len, self.window,
@@ -673,8 +680,8 @@ class ScenarioReplayer:
 
     def stream_bytes_per_selection(self) -> float:
         """Slot mode: bytes read from L2/HBM per selection (row/column units of every boundary)."""
-        if self.mode != "slots":
-            raise ValueError("stream bytes are defined for mode='slots'")
+        if self.mode not in ("slots", "cluster"):
+            raise ValueError("stream bytes are defined for the slot modes")
         meta = self.meta.view(self.S, -1)[:, :16].cpu().numpy().view(np.int32)   # hdr: used, Wp, units, inserts
         return float((meta[:, 2].astype(np.int64) * meta[:, 1] * 8).mean())
 

@@ -685,6 +685,480 @@ replay_slots_kernel(ss_dag_set D, SlotArgs A, ReplayArgs R) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster slot replay: the slot tile split by DESTINATION slots over a thread-block cluster
+// ---------------------------------------------------------------------------
+// For frontiers too wide for two single-CTA tiles per SM (C5: 110-150 slots), the CL CTAs of a cluster share
+// one scenario: CTA q keeps Tq[src slot][c] = T[src][q*SCQ + c] -- every source row, its own SCQ destination
+// columns -- so each CTA relaxes every source of a column against its own destinations and owns complete
+// destination minima (no cross-CTA merge of partials).  Per boundary b:
+//   stage(b)  the owner CTA of each position of column b merges its NW range partials (lexicographic
+//             (value, position) == numpy first-index argmin), adds tau, and broadcasts (cost, Tq row offset)
+//             into EVERY CTA's source table through distributed shared memory (st.shared::cluster); the
+//             backpointer goes to CTA 0, which holds the whole table for the backtrack;
+//   barrier.cluster (release / acquire): the source table is complete everywhere;
+//   relax(b)  as the single-CTA kernel, over the CTA's own destination columns;
+//   CTA barrier: partials visible, the producer warp has applied boundary b+1's rows / own columns.
+// The request epilogue (final argmin, backtrack, occupancy update, ring, outputs) runs on CTA 0, which sends
+// the chain's distinct GPUs to the other CTAs (each keeps its own occupancy / tau copy).  The relaxation
+// reads the same fp64 values in the same order as ss_replay / ss_replay_slots: bit-identical results.
+struct ClusterArgs {
+    const uint8_t* meta;
+    int64_t meta_stride;
+    const double* stream;
+    int64_t stream_stride;
+    int s_rows, w, nbuf, stage_bytes, cl, sc, s_cap;
+    int off_T, off_stage, off_full, off_meta, meta_bytes, off_part, off_src, off_bp, off_picks, off_tau, off_occ,
+        off_stamp, off_slotgpu, off_cl, off_coff, off_red, off_cred, off_clist, off_misc, off_base, off_pow, pow_len,
+        off_rel, off_seg, total;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+    return a;
+}
+__device__ __forceinline__ void st_cl_f64(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int DPLC, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
+replay_cluster_kernel(ss_dag_set D, ClusterArgs A, ReplayArgs R) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int SCQ = DPLC * 32;
+    constexpr int NC = NW * 32;
+    constexpr int NT = NC + 32;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const int CL = A.cl;
+    const int q = (int)cluster_rank();
+    const int dag = blockIdx.x / CL;
+    const int qlo = q * SCQ;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int l0 = D.layer_ptr[dag];
+    const int nl = D.layer_ptr[dag + 1] - l0;
+    const int nblk = nl - 1;
+    const int W = A.w;
+    const int SC = A.sc;
+    MetaLayout ml{nblk, A.s_cap, D.max_gpus};
+
+    double* T = reinterpret_cast<double*>(smem + A.off_T);            // [s_rows][W]: own destination columns
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + A.off_full);
+    unsigned char* meta_s = smem + A.off_meta;
+    double* part_v = reinterpret_cast<double*>(smem + A.off_part);     // [2][NW][SCQ]
+    int16_t* part_i = reinterpret_cast<int16_t*>(part_v + 2 * NW * SCQ);
+    double* src_c = reinterpret_cast<double*>(smem + A.off_src);       // [2][SC] source costs by position
+    int* src_r = reinterpret_cast<int*>(src_c + 2 * SC);                // [2][SC] their Tq row byte offsets
+    uint8_t* bp = smem + A.off_bp;                                      // [L][SC] (CTA 0)
+    int* picks = reinterpret_cast<int*>(smem + A.off_picks);
+    double* tau_g = reinterpret_cast<double*>(smem + A.off_tau);
+    int* occ_s = reinterpret_cast<int*>(smem + A.off_occ);
+    int* stamp = reinterpret_cast<int*>(smem + A.off_stamp);
+    int* slot_gpu = reinterpret_cast<int*>(smem + A.off_slotgpu);
+    int* col_len = reinterpret_cast<int*>(smem + A.off_cl);
+    int* coff = reinterpret_cast<int*>(smem + A.off_coff);
+    double* red_v = reinterpret_cast<double*>(smem + A.off_red);       // [NW] CTA-local argmin partials
+    int* red_i = reinterpret_cast<int*>(smem + A.off_red + NW * 8);
+    double* cred_v = reinterpret_cast<double*>(smem + A.off_cred);     // [8] per-CTA argmin partials (CTA 0)
+    int* cred_i = reinterpret_cast<int*>(smem + A.off_cred + 64);
+    int* clist = reinterpret_cast<int*>(smem + A.off_clist);           // [1 + L]: the chain's distinct GPUs
+    volatile int* misc = reinterpret_cast<int*>(smem + A.off_misc);    // [0] status [1] aux [3] chunks/req
+    double* base_s = reinterpret_cast<double*>(smem + A.off_base);
+    double* pow_s = reinterpret_cast<double*>(smem + A.off_pow);
+    int* rel = reinterpret_cast<int*>(smem + A.off_rel);
+    uint8_t* seg_end = smem + A.off_seg;                                // [NW][SC]
+    int* seg_start = reinterpret_cast<int*>(smem + A.off_seg + NW * SC);
+
+    // ---- setup (every CTA of the cluster reaches the same decisions from the same inputs) -------------
+    const uint8_t* meta_g = A.meta + (int64_t)dag * A.meta_stride;
+    if (tid == 0) {
+        misc[0] = SS_OK;
+        misc[1] = 0;
+        if (R.st.status[dag] != SS_OK) misc[0] = -1;
+        for (int b = 0; b < A.nbuf; ++b) mbar_init(&full[b], 1);
+        fence_mbar_init();
+    }
+    {
+        const int4* srcv = reinterpret_cast<const int4*>(meta_g);
+        int4* dstv = reinterpret_cast<int4*>(meta_s);
+        for (int x = tid; x < A.meta_bytes / 16; x += blockDim.x) dstv[x] = srcv[x];
+        for (int l = tid; l < nl; l += blockDim.x) {
+            col_len[l] = D.col_len[l0 + l];
+            coff[l] = D.col_off[l0 + l];
+        }
+        const int gb = R.st.gpu_ptr[dag], gn = R.st.gpu_ptr[dag + 1] - gb;
+        for (int g = tid; g < gn; g += blockDim.x) base_s[g] = R.st.base_tau[gb + g];
+        for (int o = tid; o < A.pow_len; o += blockDim.x) pow_s[o] = R.occpow[o];
+    }
+    __syncthreads();
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(meta_s);
+    const BlkMeta* bm = reinterpret_cast<const BlkMeta*>(meta_s + ml.off_blk());
+    const int16_t* ins = reinterpret_cast<const int16_t*>(meta_s + ml.off_ins());
+    const uint8_t* src_map = meta_s + ml.off_src();
+    const int Wp = hdr[1];
+    const int upc = max(1, A.stage_bytes / (Wp * 8));
+    const int tw = min(Wp, A.s_rows);
+    if (tid == 0 && misc[0] == SS_OK) {
+        if (hdr[0] > A.s_rows || hdr[0] > SC || nl < 2) misc[0] = SS_BAD_INPUT;
+        int chunks = 0;
+        for (int b = 1; b < nblk; ++b) chunks += (2 * bm[b].n_ins + upc - 1) / upc;
+        misc[3] = chunks;
+    }
+    __syncthreads();
+    if (misc[0] != SS_OK) {
+        if (q == 0 && tid == 0 && misc[0] != -1) { R.st.status[dag] = misc[0]; R.st.aux[dag] = misc[1]; }
+        return;                                                  // uniform over the cluster
+    }
+    cluster_sync_all();                                          // every CTA started before any DSMEM write
+    const int n_req = R.n_req;
+    const double* stream_g = A.stream + (int64_t)dag * A.stream_stride;
+
+    // ========================= producer: TMA ring + apply(1..nblk-1) of own columns ==========
+    if (warp == NW) {
+        const int64_t total = (int64_t)n_req * misc[3];
+        int64_t issued = 0;
+        int ib = 1, iu0 = 0;
+        auto issue_next = [&](int buf) {
+            while (ib < nblk && iu0 >= 2 * bm[ib].n_ins) { ++ib; iu0 = 0; }
+            if (ib >= nblk) { ib = 1; iu0 = 0; while (ib < nblk && 2 * bm[ib].n_ins == 0) ++ib; }
+            const BlkMeta m = bm[ib];
+            const int nu = min(upc, 2 * m.n_ins - iu0);
+            const uint32_t bytes = (uint32_t)nu * Wp * 8;
+            fence_proxy_async_smem();
+            mbar_expect_tx(&full[buf], bytes);
+            bulk_g2s(smem + A.off_stage + (size_t)buf * A.stage_bytes, stream_g + (int64_t)(m.unit_start + iu0) * Wp,
+                     bytes, &full[buf]);
+            iu0 += nu;
+            ++issued;
+        };
+        if (lane == 0)
+            for (int b = 0; b < A.nbuf && issued < total; ++b) issue_next(b);
+        int cbuf = 0;
+        uint32_t cphase = 0;
+        int64_t consumed = 0;
+        for (int r = 0; r < n_req; ++r) {
+            cluster_sync_all();                                  // request start
+            if (misc[0] != SS_OK) break;
+            for (int b = 0; b < nblk; ++b) {
+                cluster_sync_all();                              // source table of boundary b complete
+                if (b + 1 < nblk) {
+                    const BlkMeta m = bm[b + 1];
+                    const int units = 2 * m.n_ins;
+                    for (int u0 = 0; u0 < units; u0 += upc) {
+                        const int nu = min(upc, units - u0);
+                        mbar_wait(&full[cbuf], cphase);
+                        const double* stg = reinterpret_cast<const double*>(smem + A.off_stage +
+                                                                            (size_t)cbuf * A.stage_bytes);
+                        for (int ul = 0; ul < nu; ++ul) {
+                            const int u = u0 + ul;
+                            const int slot = ins[2 * (m.ins_start + (u >> 1))];
+                            const double* su = stg + ul * Wp;
+                            if (u & 1) {                         // column of the entering GPU: own slots only
+                                const int c = slot - qlo;
+                                if (c >= 0 && c < SCQ)
+                                    for (int x = lane; x < tw; x += 32) T[x * W + c] = su[x];
+                            } else {                             // row: this CTA's destination range
+#pragma unroll
+                                for (int d = 0; d < DPLC; ++d) {
+                                    const int c = lane + 32 * d;
+                                    if (qlo + c < tw) T[slot * W + c] = su[qlo + c];
+                                }
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0 && issued < total) issue_next(cbuf);
+                        ++consumed;
+                        if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
+                    }
+                    for (int k = lane; k < m.n_ins; k += 32)
+                        slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
+                }
+                all_sync(NT);                                    // boundary b done locally
+            }
+            cluster_sync_all();                                  // epilogue: argmin partials at CTA 0
+            cluster_sync_all();                                  // epilogue: chain broadcast
+        }
+        while (consumed < issued) {
+            mbar_wait(&full[cbuf], cphase);
+            ++consumed;
+            if (++cbuf == A.nbuf) { cbuf = 0; cphase ^= 1u; }
+        }
+        __syncwarp();
+        cluster_sync_all();                                      // matches the consumers' exit barrier
+        return;
+    }
+
+    // ========================= consumers ======================================
+    const int gbase = R.st.gpu_ptr[dag];
+    const int ng = R.st.gpu_ptr[dag + 1] - gbase;
+    const int window = R.window;
+    const int64_t req0 = R.st.next_req[dag];
+    const int ring_stride = D.max_layers + 1;
+    int* ring = R.st.ring + (int64_t)dag * (window > 0 ? window : 1) * ring_stride;
+    for (int g = tid; g < ng; g += NC) {
+        occ_s[g] = R.st.occ[gbase + g];
+        stamp[g] = 0;
+    }
+    auto issue_initial_rows = [&]() {
+        const BlkMeta m = bm[0];
+        const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
+        for (int u = warp; u < m.n_ins; u += NW) {
+            const int slot = ins[2 * (m.ins_start + u)];
+            const double* su = s0 + (int64_t)u * Wp;
+            for (int c = lane; c < SCQ; c += 32)
+                if (qlo + c < tw) cp_async8(T + slot * W + c, su + qlo + c);
+        }
+    };
+    // the release list of the first request comes from the ring in global memory (written by an earlier
+    // launch); later ones are sent by CTA 0 with each chain (the ring is CTA 0's)
+    if (n_req > 0) {
+        if (window > 0 && req0 >= window) {
+            const int* slot = ring + (int64_t)(req0 % window) * ring_stride;
+            for (int k = tid; k < ring_stride; k += NC) rel[k] = slot[k];
+        } else if (tid == 0) {
+            rel[0] = 0;
+        }
+        issue_initial_rows();
+    }
+    const uint32_t bp_0 = peer_addr(bp, 0);
+    int done = 0;
+    consumer_sync(NC);
+
+    // stage(c) for c >= 1: the owner of each position merges its range partials of boundary c-1, adds tau and
+    // broadcasts (cost, row) to every CTA (table c & 1); c == 0: every CTA fills the whole table locally
+    auto stage = [&](int c) {
+        const int rs = col_len[c];
+        const int buf = c & 1;
+        if (c == 0) {
+            for (int p = tid; p < rs; p += NC) {
+                const int sl = src_map[p];
+                src_c[p] = tau_g[slot_gpu[sl]];
+                src_r[p] = sl * W * 8;
+            }
+            return;
+        }
+        const double* pv = part_v + ((c - 1) & 1) * NW * SCQ;
+        const int16_t* pi = part_i + ((c - 1) & 1) * NW * SCQ;
+        for (int p = tid; p < rs; p += NC) {
+            const int sl = src_map[c * A.s_cap + p];
+            const int lc = sl - qlo;
+            if (lc < 0 || lc >= SCQ) continue;                       // another CTA owns this destination
+            double v = pv[lc];
+            int i = pi[lc];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) lex_min(v, i, pv[w * SCQ + lc], (int)pi[w * SCQ + lc]);
+            if (i == PART_NONE) i = 0;
+            const double cst = __dadd_rn(v, tau_g[slot_gpu[sl]]);
+            st_cl_u8(bp_0 + (c - 1) * SC + p, (uint32_t)i);
+            for (int k = 0; k < CL; ++k) {
+                st_cl_f64(peer_addr(src_c + buf * SC + p, k), cst);
+                st_cl_u32(peer_addr(src_r + buf * SC + p, k), (uint32_t)(sl * W * 8));
+            }
+        }
+    };
+
+    for (int r = 0; r < n_req; ++r) {
+        const int64_t req = req0 + r;
+        if (misc[0] == SS_OK) {
+            const BlkMeta m = bm[0];
+            for (int k = tid; k < m.n_ins; k += NC) slot_gpu[ins[2 * (m.ins_start + k)]] = ins[2 * (m.ins_start + k) + 1];
+            cp_async_wait_all();                                     // initial rows
+            consumer_sync(NC);
+            if (window > 0 && req >= window) {
+                const int cnt = rel[0];
+                for (int k = tid; k < cnt; k += NC) occ_s[rel[1 + k]] -= 1;
+            }
+            consumer_sync(NC);
+            for (int g = tid; g < ng; g += NC) {
+                const int o = occ_s[g];
+                if (o < 0 || o >= R.occpow_len) {
+                    atomicExch((int*)&misc[0], o < 0 ? SS_OCC_UNDERFLOW : SS_BAD_INPUT);
+                    misc[1] = g;
+                }
+                const int oc = o < 0 ? 0 : (o >= R.occpow_len ? R.occpow_len - 1 : o);
+                tau_g[g] = base_s[g] * (oc < A.pow_len ? pow_s[oc] : R.occpow[oc]);
+            }
+        }
+        cluster_sync_all();                                          // request start
+        if (misc[0] != SS_OK) break;
+
+        for (int b = 0; b < nblk; ++b) {
+            stage(b);                                                // tau / slot_gpu / partials of b-1: visible
+            cluster_sync_all();                                      // the source table of b is complete
+            const int rs = col_len[b];
+            const int p0 = warp * rs / NW, n = (warp + 1) * rs / NW - p0;
+            const double* cw = src_c + (b & 1) * SC;
+            const int* rw = src_r + (b & 1) * SC;
+            double v[DPLC];
+            int ix[DPLC];
+#pragma unroll
+            for (int d = 0; d < DPLC; ++d) { v[d] = INF; ix[d] = PART_NONE; }
+            const char* Tb = reinterpret_cast<const char*>(T + lane);
+            for (int k = 0; k < n; ++k) {
+                const int p = p0 + k;
+                relax_row<DPLC>(reinterpret_cast<const double*>(Tb + rw[p]), cw[p], p, v, ix);
+            }
+            double* pv = part_v + (b & 1) * NW * SCQ + warp * SCQ;
+            int16_t* pi = part_i + (b & 1) * NW * SCQ + warp * SCQ;
+#pragma unroll
+            for (int d = 0; d < DPLC; ++d) {
+                pv[d * 32 + lane] = v[d];
+                pi[d * 32 + lane] = (int16_t)ix[d];
+            }
+            all_sync(NT);                                            // partials visible; the producer applied b+1
+        }
+        if (r + 1 < n_req) issue_initial_rows();                     // this CTA's tile is no longer read
+
+        // ---- last column: owned costs, CTA argmin partial -> CTA 0 ----------------------------------
+        {
+            const int c = nblk;
+            const int rs = col_len[c];
+            const double* pv = part_v + ((c - 1) & 1) * NW * SCQ;
+            const int16_t* pi = part_i + ((c - 1) & 1) * NW * SCQ;
+            double bv = INF;
+            int bi = IDX_NONE;
+            for (int p = tid; p < rs; p += NC) {
+                const int sl = src_map[c * A.s_cap + p];
+                const int lc = sl - qlo;
+                if (lc < 0 || lc >= SCQ) continue;
+                double v = pv[lc];
+                int i = pi[lc];
+#pragma unroll
+                for (int w = 1; w < NW; ++w) lex_min(v, i, pv[w * SCQ + lc], (int)pi[w * SCQ + lc]);
+                if (i == PART_NONE) i = 0;
+                const double cst = __dadd_rn(v, tau_g[slot_gpu[sl]]);
+                st_cl_u8(bp_0 + (c - 1) * SC + p, (uint32_t)i);
+                lex_min(bv, bi, cst, p);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                lex_min(bv, bi, v2, i2);
+            }
+            if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+            consumer_sync(NC);
+            if (tid == 0) {
+                for (int w = 1; w < NW; ++w) lex_min(bv, bi, red_v[w], red_i[w]);
+                st_cl_f64(peer_addr(cred_v + q, 0), bv);
+                st_cl_u32(peer_addr(cred_i + q, 0), (uint32_t)bi);
+            }
+        }
+        cluster_sync_all();                                          // argmin partials + backpointers at CTA 0
+        if (q == 0) {
+            if (tid == 0) {
+                double v = cred_v[0];
+                int idx = cred_i[0];
+                for (int k = 1; k < CL; ++k) lex_min(v, idx, cred_v[k], cred_i[k]);
+                if (!(v <= DBL_MAX)) {
+                    for (int k = 0; k < CL; ++k) st_cl_u32(peer_addr((const void*)&misc[0], k), (uint32_t)SS_NO_PATH);
+                } else {
+                    picks[nl - 1] = idx;
+                    seg_start[NW] = idx;
+                }
+                if (R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
+            }
+            consumer_sync(NC);
+            if (misc[0] == SS_OK) {
+                {   // segment-parallel backtrack over the consumer warps
+                    const int blo = warp * nblk / NW, bhi = (warp + 1) * nblk / NW;
+                    for (int st = lane; st < SC; st += 32) {
+                        int p = st;
+                        for (int b = bhi - 1; b >= blo; --b) p = min((int)bp[b * SC + p], SC - 1);
+                        seg_end[warp * SC + st] = (uint8_t)p;
+                    }
+                }
+                consumer_sync(NC);
+                if (tid == 0) {
+                    int p = seg_start[NW];
+                    for (int w = NW - 1; w >= 0; --w) {
+                        seg_start[w] = p;
+                        p = seg_end[w * SC + p];
+                    }
+                }
+                consumer_sync(NC);
+                if (lane == 0) {
+                    const int blo = warp * nblk / NW, bhi = (warp + 1) * nblk / NW;
+                    int p = seg_start[warp];
+                    for (int b = bhi - 1; b >= blo; --b) {
+                        p = bp[b * SC + p];
+                        picks[b] = p;
+                    }
+                }
+                consumer_sync(NC);
+                // load update: +1 per distinct GPU (CTA 0's stamps), ring, outputs; the list goes to the peers
+                const int tag = (int)(req & 0x3fffffff) + 1;
+                int* slot = window > 0 ? ring + (int64_t)(req % window) * ring_stride : nullptr;
+                if (tid == 0) clist[0] = 0;
+                consumer_sync(NC);
+                uint64_t h = 0;
+                for (int l = tid; l < nl; l += NC) {
+                    const int g = D.node_gpu[coff[l] + picks[l]];
+                    h += ss_splitmix64(((uint64_t)l << 32) | (uint64_t)g);
+                    if (R.out.gpus) R.out.gpus[((int64_t)dag * n_req + r) * D.max_layers + l] = (int16_t)g;
+                    if (atomicExch(&stamp[g], tag) != tag && window != 0) {
+                        occ_s[g] += 1;
+                        const int at = atomicAdd(&clist[0], 1);
+                        clist[1 + at] = g;
+                        if (slot) slot[1 + at] = g;
+                    }
+                }
+                if (R.out.chain_hash) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+                    if (lane == 0)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&R.out.chain_hash[(int64_t)dag * n_req + r]),
+                                  (unsigned long long)h);
+                }
+                consumer_sync(NC);
+                const int cnt = clist[0];
+                if (tid == 0 && slot) slot[0] = cnt;
+                for (int k = 1; k < CL; ++k)
+                    for (int x = tid; x <= cnt; x += NC) st_cl_u32(peer_addr(clist + x, k), (uint32_t)clist[x]);
+                // the next request's release list (chain req+1-W, already in CTA 0's ring) for every CTA
+                if (r + 1 < n_req && window > 0 && req + 1 >= window) {
+                    consumer_sync(NC);
+                    const int* ns = ring + (int64_t)((req + 1) % window) * ring_stride;
+                    const int ncnt = ns[0];
+                    for (int k = 0; k < CL; ++k)
+                        for (int x = tid; x <= ncnt; x += NC) st_cl_u32(peer_addr(rel + x, k), (uint32_t)ns[x]);
+                }
+            }
+        }
+        cluster_sync_all();                                          // the chain's distinct GPUs everywhere
+        if (misc[0] != SS_OK) continue;                              // the next request-start barrier ends it
+        if (q != 0) {
+            const int cnt = clist[0];
+            for (int k = tid; k < cnt; k += NC) occ_s[clist[1 + k]] += 1;
+        }
+        ++done;
+    }
+    cp_async_wait_all();
+    if (q == 0) {
+        for (int g = tid; g < ng; g += NC) R.st.occ[gbase + g] = occ_s[g];
+        if (tid == 0) {
+            R.st.next_req[dag] = req0 + done;
+            if (misc[0] != SS_OK) { R.st.status[dag] = misc[0]; R.st.aux[dag] = misc[1]; }
+        }
+    }
+    __syncwarp();
+    cluster_sync_all();                                              // no CTA exits while peers may write to it
+}
+
 inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
 constexpr int kSmemPerSM = 228 * 1024;
@@ -842,4 +1316,102 @@ extern "C" int ss_set_slot_staging(int32_t stage_bytes, int32_t n_buffers) {
     if (stage_bytes > 0) g_stage_bytes = (stage_bytes + 127) / 128 * 128;
     if (n_buffers > 0) g_nbuf = n_buffers > 8 ? 8 : n_buffers;
     return SS_OK;
+}
+
+// Cluster slot replay (replay_cluster_kernel): same program, state, outputs and op script as ss_replay_slots;
+// the scenario's slot tile is split by destination slots over a cluster of ceil(s_rows / (32 * dplc)) CTAs
+// (<= 8).  dplc = 1 or 2 destination slots per lane; 0 = default (1; env SS_CLUSTER_DPL overrides).
+extern "C" int ss_replay_slots_cluster(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_stride,
+                                       const double* stream, int64_t stream_stride, int32_t s_cap, int32_t s_rows,
+                                       const ss_replay_state* st, const double* occpow, int32_t occpow_len,
+                                       int32_t window, int32_t n_req, const ss_replay_out* out, int32_t dplc,
+                                       void* stream_h) {
+    if (!dags || !st || !occpow || occpow_len < 1 || n_req < 1 || !meta || !stream) return SS_BAD_INPUT;
+    const ss_dag_set& D = *dags;
+    if (D.n_dags <= 0) return SS_OK;
+    if (s_cap < 32 || s_cap > 256 || (s_cap & 31) || s_rows < 1 || s_rows > s_cap || D.max_layers < 2)
+        return SS_BAD_INPUT;
+    if (dplc <= 0) {
+        const char* e = getenv("SS_CLUSTER_DPL");
+        dplc = e ? atoi(e) : 1;
+    }
+    if (dplc != 1 && dplc != 2) return SS_BAD_INPUT;
+    const int scq = 32 * dplc;
+    const int cl = (s_rows + scq - 1) / scq;
+    if (cl < 1 || cl > 8) return SS_BAD_INPUT;
+    const int nw = 4;
+    ClusterArgs A{};
+    A.meta = meta;
+    A.meta_stride = meta_stride;
+    A.stream = stream;
+    A.stream_stride = stream_stride;
+    A.s_rows = s_rows;
+    A.w = scq + 1;                                       // odd pitch: the producer's column writes are conflict-free
+    A.cl = cl;
+    A.sc = cl * scq;
+    A.s_cap = s_cap;
+    MetaLayout ml{D.max_layers - 1, s_cap, D.max_gpus};
+    A.meta_bytes = ml.bytes();
+    const int SC = A.sc;
+    auto layout = [&](int nbuf, int stage) {
+        A.nbuf = nbuf;
+        A.stage_bytes = stage;
+        int o = 0;
+        A.off_T = o;       o += align_up(s_rows * A.w * 8, 128);
+        A.off_stage = o;   o += A.nbuf * A.stage_bytes;
+        A.off_full = o;    o += 64;
+        A.off_meta = o;    o += align_up(A.meta_bytes, 16);
+        A.off_part = o;    o += align_up(2 * nw * scq * 10, 16);
+        A.off_src = o;     o += align_up(2 * SC * 12, 16);
+        A.off_bp = o;      o += align_up(D.max_layers * SC, 16);
+        A.off_picks = o;   o += align_up(D.max_layers * 4, 16);
+        A.off_tau = o;     o += align_up(D.max_gpus * 8, 16);
+        A.off_occ = o;     o += align_up(D.max_gpus * 4, 16);
+        A.off_stamp = o;   o += align_up(D.max_gpus * 4, 16);
+        A.off_slotgpu = o; o += align_up(SC * 4, 16);
+        A.off_cl = o;      o += align_up(D.max_layers * 4, 16);
+        A.off_coff = o;    o += align_up(D.max_layers * 4, 16);
+        A.off_red = o;     o += align_up(nw * 12, 16);
+        A.off_cred = o;    o += 128;
+        A.off_clist = o;   o += align_up((D.max_layers + 1) * 4, 16);
+        A.off_misc = o;    o += 64;
+        A.off_base = o;    o += align_up(D.max_gpus * 8, 16);
+        A.pow_len = occpow_len < 256 ? occpow_len : 256;
+        A.off_pow = o;     o += align_up(A.pow_len * 8, 16);
+        A.off_rel = o;     o += align_up((D.max_layers + 1) * 4, 16);
+        A.off_seg = o;     o += align_up(nw * SC + (nw + 1) * 4, 16);
+        A.total = o;
+    };
+    const int unit_min = align_up((s_rows + 1) * 8, 128);
+    layout(2, max(g_stage_bytes, unit_min));
+    if (A.total > 227 * 1024) return SS_BAD_INPUT;
+    ReplayArgs R{};
+    R.st = *st;
+    if (out) R.out = *out;
+    R.occpow = occpow;
+    R.occpow_len = occpow_len;
+    R.window = window;
+    R.n_req = n_req;
+    cudaStream_t s = ss_stream(stream_h);
+    if (R.out.chain_hash) cudaMemsetAsync(R.out.chain_hash, 0, sizeof(uint64_t) * (size_t)D.n_dags * n_req, s);
+    auto run = [&](auto kern) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
+            return SS_CUDA_ERROR;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(D.n_dags * cl), 1, 1);
+        cfg.blockDim = dim3((nw + 1) * 32, 1, 1);
+        cfg.dynamicSmemBytes = A.total;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, D, A, R) != cudaSuccess) return SS_CUDA_ERROR;
+        SS_CHECK_LAUNCH();
+        return SS_OK;
+    };
+    return dplc == 1 ? run(replay_cluster_kernel<1, 4>) : run(replay_cluster_kernel<2, 4>);
 }

@@ -55,9 +55,11 @@ def main():
         return best_t, best_v
 
     bt, bv = sweep_best(packs, mine)
-    t_dev, v_dev = ex.argmax(torch.tensor([bt], device="cuda"), torch.tensor([bv], device="cuda"))
+    t_dev, v_dev = ex.argmax(torch.tensor([bt], dtype=torch.float64, device="cuda"),
+                             torch.tensor([bv], dtype=torch.int64, device="cuda"))
     got_abi = (float(t_dev.cpu()[0]), int(v_dev.cpu()[0]))
-    got_torch = global_argmax(torch.tensor(bt, device="cuda"), torch.tensor(float(bv), device="cuda"))
+    got_torch = global_argmax(torch.tensor(bt, dtype=torch.float64, device="cuda"),
+                              torch.tensor(float(bv), dtype=torch.float64, device="cuda"))
     if rank == 0:
         all_ids = np.arange(V)
         want = sweep_best([scen.bench_variants(1, 256, 80, seed0=int(v))[0] for v in all_ids], all_ids)

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--stage", type=int, default=0)
     ap.add_argument("--sbuf", type=int, default=0)
     ap.add_argument("--lib", default="", help="alternative libswarmsched_b200.so (A/B builds)")
+    ap.add_argument("--c5", default="", help="C5 sub-pool (8b / 32b / 70b) instead of synthetic_cluster(--n)")
     args = ap.parse_args()
     import torch
     from paper_2509_26182_b200 import _native as N, scenarios as scen
@@ -40,12 +41,17 @@ def main():
     from helpers_golden import plan_from_golden
     from oracle import alloc_ref
     t0 = time.time()
-    cl, model = scen.synthetic_cluster(args.n, seed=0, model=scen.bench_model(args.L))
+    if args.c5:
+        cl, model = {n: (c, m) for n, c, m in scen.c5_pools(0)}[args.c5]
+        args.L, args.n = model.layer_count, len(cl.gpus)
+    else:
+        cl, model = scen.synthetic_cluster(args.n, seed=0, model=scen.bench_model(args.L))
     d = alloc_ref.allocate(cl, model)
     d["objective"] = d["objective"].hex()
     d["per_k"] = [dict(r, z=r["z"].hex()) for r in d["per_k"]]
     plan = plan_from_golden(d)
-    ss = scen.build_scenarios(cl, model, plan, args.scen, seed0=1, churn=0.05, jitter=not args.nojitter)
+    ss = scen.build_scenarios(cl, model, plan, args.scen, seed0=1, churn=0.05, jitter=not args.nojitter,
+                              host_events=False)
     print(f"prep {time.time()-t0:.1f}s k={plan.replication_count}", flush=True)
     lib = N.lib()
     if args.nbuf or args.budget:
@@ -73,7 +79,7 @@ def main():
     t = float(np.median(times))
     sel = args.scen * args.req
     gbs = float(b2.mean()) * sel / t / 1e9
-    print(json.dumps({"mode": args.mode, "scen": args.scen, "req": args.req, "L": args.L, "n": args.n, "k": plan.replication_count,
+    print(json.dumps({"mode": rp.mode, "s_rows": getattr(rp, "s_rows", None), "scen": args.scen, "req": args.req, "L": args.L, "n": args.n, "k": plan.replication_count,
                       "time_ms": t * 1e3, "sel_per_s": sel / t, "B2_mean": float(b2.mean()),
                       "algo_GBps": gbs, "frac_hbm": gbs / 6538.9, "times": times}))
 

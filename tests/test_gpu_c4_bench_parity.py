@@ -28,13 +28,14 @@ def test_c4_bench_size_sampled_scenarios_vs_oracle(cuda_ready):
     seeds = shard(S, 0, 1)
     dev = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=seeds, host_events=False)
     outs = {}
-    for mode in ("slots", "blocks"):
+    for mode in ("slots", "blocks", "cluster"):
         rp = ScenarioReplayer(dev, window=W, mode=mode, max_requests=R)
         out = rp.run(R, gpus=True)
         rp.raise_first_failure()
         outs[mode] = (out.gpus.cpu().numpy(), out.cost.cpu().numpy(), rp.occ.view(S, -1).cpu().numpy())
-    for a, b in zip(outs["slots"], outs["blocks"]):
-        assert np.array_equal(a, b)
+    for m in ("blocks", "cluster"):
+        for a, b in zip(outs["slots"], outs[m]):
+            assert np.array_equal(a, b), m
     rng = np.random.default_rng(97)
     sample = sorted(set(range(0, S, 97)) | set(rng.choice(S, size=S // 100, replace=False).tolist()))
     host = scen.build_scenarios(cl, model, plan, len(sample), churn=0.05, jitter=True, seeds=seeds[sample])

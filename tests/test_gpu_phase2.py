@@ -107,7 +107,7 @@ def _replayer_for_golden(rep, plan_dict, n_scen=1, seed0=None, mode="slots"):
     return ss, ScenarioReplayer(ss, window=-1 if W is None else W, max_requests=len(rep["routes"]) + 4, mode=mode)
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks", "warp"])
+@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks", "warp"])
 @pytest.mark.parametrize("name", ["c1", "c1_tie", "n32_tie", "rt16", "c2", "c4_s11", "c4_s12"])
 def test_replay_kernel_golden(cuda_ready, router_replays, name, mode):
     """ss_replay / ss_replay_slots (on-device load update) == reference ChainRouter op script, bit-exact."""
@@ -138,7 +138,7 @@ def _hash(gpus_row):
     return sum(splitmix64((l << 32) | int(g)) for l, g in enumerate(gpus_row)) & M
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks"])
+@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks"])
 @pytest.mark.parametrize("window", [64, 0, -1, 1, 7])
 def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
     """C4-shaped batch (L64/N256 pool, churn + jitter) vs the oracle, every scenario."""
@@ -166,7 +166,7 @@ def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
             assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
 
 
-@pytest.mark.parametrize("mode", ["slots", "blocks", "warp"])
+@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks", "warp"])
 def test_replay_tie_pool_vs_oracle(cuda_ready, mode):
     """Homogeneous flops => many exact ties (13-23% of columns): first-index rule must hold."""
     from paper_2509_26182_b200 import scenarios as scen
