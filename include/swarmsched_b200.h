@@ -395,6 +395,31 @@ int ss_replay_slots_cluster(const ss_dag_set* dags, const uint8_t* meta, int64_t
                             const double* occpow, int32_t occpow_len, int32_t window, int32_t n_req,
                             const ss_replay_out* out, int32_t dplc, void* stream_h);
 
+/* Region-tiled replay (replaces router.py:247-260 route/release over router.py:163-185 _relax for pools whose
+ * GPUs fall into regions: the reference bench pool, bench.py:114-138 + topology.py:133-142, and C5).
+ * Same state, outputs and op script as ss_replay; results bit-identical for any input.
+ *   tile_of[g]  region ("tile") of pool GPU g, 0..n_tiles-1 (<= 8 tiles); every tile's frontier must fit 32
+ *               slots (status[s] = SS_BAD_INPUT otherwise);
+ *   bounds      lb[n_tiles][n_tiles] then ub[n_tiles]: lb[S][D] <= every (jittered) S->D entry of the pool
+ *               matrix, ub[D] >= every D->D entry.  A cross-tile block S->D of a boundary is skipped only when
+ *               cmin_S + lb[S][D] > cmin_D + ub[D] (no S candidate can reach, or tie, a D minimum); the
+ *               others are relaxed exactly with entries recomputed from base_rtt (x the jitter of jitter_seed);
+ *   ss_region_program: per-scenario program (meta_stride bytes >= ss_region_meta_bytes, units of stream_stride
+ *               doubles), rt_used[s] = slots needed by the widest tile;
+ *   ss_replay_regions: rt_rows >= max rt_used, pos_cap >= the widest column (<= 256). */
+int64_t ss_region_meta_bytes(int32_t layers, int32_t n_gpus, int32_t n_tiles, int32_t pos_cap);
+int ss_region_program(int32_t n_scen, int32_t layers, int32_t n_gpus, const int32_t* slice_lo,
+                      const int32_t* slice_hi, int64_t slice_stride, const uint8_t* leave, const double* rtt,
+                      const int64_t* jitter_seed, const int32_t* tile_of, int32_t n_tiles, int32_t pos_cap,
+                      int64_t meta_stride, int64_t stream_stride, uint8_t* meta, double* stream, int32_t* rt_used,
+                      int32_t* status, void* stream_h);
+int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, int64_t meta_stride, const double* stream,
+                      int64_t stream_stride, int32_t n_tiles, int32_t pos_cap, int32_t rt_rows,
+                      const double* bounds, const double* base_rtt, const int64_t* jitter_seed,
+                      const ss_replay_state* st, const double* occpow, int32_t occpow_len, int32_t window,
+                      int32_t n_req, const ss_replay_out* out, void* stream_h);
+int ss_set_region_staging(int32_t stage_bytes, int32_t n_buffers);
+
 /* Kernel tuning knobs (0 = default); returns previous values via *_h. */
 int ss_set_tiling(int32_t smem_budget_bytes, int32_t n_buffers, int32_t* old_budget_h, int32_t* old_buffers_h);
 /* Constructive stage counts: batches of at most max_candidates (pool, k) candidates try every group count in

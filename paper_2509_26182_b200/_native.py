@@ -73,6 +73,14 @@ _SIGS = {
                                           C.c_int32, C.POINTER(ReplayState), C.c_void_p, C.c_int32, C.c_int32,
                                           C.c_int32, C.POINTER(ReplayOut), C.c_int32, C.c_void_p]),
     "ss_set_slot_staging": (C.c_int, [C.c_int32, C.c_int32]),
+    "ss_region_meta_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "ss_region_program": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ss_replay_regions": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(ReplayState),
+                                    C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(ReplayOut), C.c_void_p]),
+    "ss_set_region_staging": (C.c_int, [C.c_int32, C.c_int32]),
     "ss_set_cover_parallel_limit": (C.c_int32, [C.c_int32]),
     "ss_replay_warp_smem": (C.c_int64, [C.POINTER(DagSet), C.c_int32, C.c_int32, C.c_int32]),
     "ss_sim_warp": (C.c_int, [C.POINTER(DagSet), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -65,11 +65,19 @@ def _replay_geometry(scen: ScenarioSet, window: int, max_requests: Optional[int]
     probe = N.DagSet(scen.n_scenarios, int(cap.max()), L, scen.n_gpus, None, None, None, None, None, None, None)
     warp_ok = int(cap.max()) <= 32 and int(N.load_library().ss_replay_warp_smem(probe, window, occ_len,
                                                                                 scen.n_gpus)) > 0
+    tiles = region_tiles(scen) if mode in ("auto", "regions") else None
     if mode == "auto":
-        mode = "warp" if warp_ok else ("slots" if s_cap <= 96 else "blocks")
+        if warp_ok:
+            mode = "warp"
+        elif tiles is not None and tiles.fits() and tiles.gap > 0 and int(cap.max()) <= 256:
+            mode = "regions"
+        else:
+            mode = "slots" if s_cap <= 96 else "blocks"
     if mode == "warp" and not warp_ok:
         raise ValueError("warp mode needs <= 32 hosts per layer and edges + ring within 227 KB of shared memory")
-    if L < 2 and mode in ("slots", "cluster"):
+    if mode == "regions" and (tiles is None or not tiles.fits() or int(cap.max()) > 256):
+        raise ValueError("regions mode needs region indices, <= 8 regions and <= 32 frontier slots per region")
+    if L < 2 and mode in ("slots", "cluster", "regions"):
         mode = "blocks"                      # no boundaries: nothing to tile
     return mode, cap, s_cap, occ_len
 
@@ -93,6 +101,67 @@ def _explicit_widths(scen: ScenarioSet):
     return cap, held
 
 
+JITTER_MIN = 768.0 / 1024.0          # ss_jitter / scenarios.jitter_factor: dyadic factors in [768, 1279] / 1024
+JITTER_MAX = 1279.0 / 1024.0
+REGION_MAX_TILES = 8
+
+
+class RegionTiles:
+    """Region tiling of a scenario batch for ss_replay_regions (replay_regions.cu).
+
+    tile_of[g]: the tile (a region of the pool that has GPUs) of pool GPU g; bounds = lb[T][T] ++ ub[T]:
+    lb[S][D] = min over S x D pool pairs of fl(rtt * JITTER_MIN) (<= every jittered entry: fl is monotone),
+    ub[D] = max over D x D pairs of fl(rtt * JITTER_MAX).  held[t] = slots tile t needs (frontier + the zombie
+    boundary + one per join), gap = min_{S != D} lb - max ub (> 0: cross-region blocks are expected to be
+    skipped by the bound test)."""
+
+    def __init__(self, scen: ScenarioSet):
+        reg = np.asarray(scen.region_idx, dtype=np.int64)
+        used = np.unique(reg)
+        remap = np.full(int(reg.max()) + 1, -1, dtype=np.int64)
+        remap[used] = np.arange(used.size)
+        self.tile_of = remap[reg].astype(np.int32)
+        self.n_tiles = int(used.size)
+        T = self.n_tiles
+        rtt = np.asarray(scen.base_rtt, dtype=np.float64)
+        jmin, jmax = (JITTER_MIN, JITTER_MAX) if scen.jitter else (1.0, 1.0)
+        lb = np.full((T, T), np.inf)
+        ub = np.zeros(T)
+        members = [np.nonzero(self.tile_of == t)[0] for t in range(T)]
+        for a in range(T):
+            ub[a] = float((rtt[np.ix_(members[a], members[a])] * jmax).max())
+            for b in range(T):
+                if a != b:
+                    lb[a, b] = float((rtt[np.ix_(members[a], members[b])] * jmin).min())
+        self.bounds = np.concatenate([lb.reshape(-1), ub])
+        off = lb[~np.eye(T, dtype=bool)]
+        self.gap = float(off.min() - ub.max()) if T > 1 else -np.inf
+        # slots per tile: GPUs held at each boundary (interval [max(lo-2,0), hi] incl. the zombie boundary)
+        L = scen.layer_count
+        if scen.slice_lo_s is not None and not scen.device_events and scen.joins == 0:
+            lo, hi = scen.slice_lo_s.astype(np.int64), scen.slice_hi_s.astype(np.int64)
+            ok = ~scen.leave & (lo <= hi) & (hi >= 1)
+        else:
+            lo, hi = scen.slice_lo[None, :].astype(np.int64), scen.slice_hi[None, :].astype(np.int64)
+            ok = (lo <= hi) & (hi >= 1)
+        b = np.arange(max(L - 1, 1))
+        held = np.zeros(T, dtype=np.int64)
+        for t in range(T):
+            m = ok & (self.tile_of[None, :] == t)
+            inb = (np.maximum(lo - 2, 0)[:, :, None] <= b) & (hi[:, :, None] >= b) & m[:, :, None]
+            held[t] = int(inb.sum(axis=1).max()) if inb.size else 0
+        self.held = held + scen.joins
+
+    def fits(self) -> bool:
+        return 1 <= self.n_tiles <= REGION_MAX_TILES and int(self.held.max()) <= 32
+
+
+def region_tiles(scen: ScenarioSet) -> Optional[RegionTiles]:
+    if getattr(scen, "region_idx", None) is None or scen.layer_count < 2:
+        return None
+    return RegionTiles(scen)
+
+
 def replay_mode(scen: ScenarioSet, *, window: int = 64, max_requests: Optional[int] = None,
                 mode: str = "auto") -> str:
     """The replay kernel ScenarioReplayer would use for these scenarios (no GPU needed)."""
@@ -102,15 +171,16 @@ def replay_mode(scen: ScenarioSet, *, window: int = 64, max_requests: Optional[i
 class ScenarioReplayer:
     def __init__(self, scen: ScenarioSet, *, window: int = 64, exponent: float = 1.0,
                  max_requests: Optional[int] = None, stream=None, mode: str = "auto"):
-        """mode "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
+        """mode "regions": one SM-resident slot tile per region of the pool, cross-region blocks relaxed only
+        where an exact bound test cannot exclude them (ss_region_program + ss_replay_regions); "slots": SM-resident slot tile (ss_slot_program + ss_replay_slots, ~10x fewer HBM
         bytes); "cluster": the same tile split by destination slots over a thread-block cluster of CTAs
         (ss_replay_slots_cluster; wide frontiers); "blocks": streamed edge blocks (ss_dag_edges + ss_replay); "warp": one warp per scenario
         with its edge blocks resident in shared memory (ss_replay_warp; columns <= 32 hosts); "auto":
         warp when it qualifies, else slots while the tile leaves room for two CTAs per SM (<= 96 slots),
         else blocks.  All modes give bit-identical results."""
         import torch
-        if mode not in ("slots", "cluster", "blocks", "warp", "auto"):
-            raise ValueError(f"mode must be 'slots', 'cluster', 'blocks', 'warp' or 'auto', got {mode!r}")
+        if mode not in ("slots", "cluster", "blocks", "warp", "regions", "auto"):
+            raise ValueError(f"mode must be 'slots', 'cluster', 'blocks', 'warp', 'regions' or 'auto', got {mode!r}")
         self.torch = torch
         self.scen = scen
         self.window = int(window)
@@ -149,6 +219,22 @@ class ScenarioReplayer:
         self.node_gpu = torch.empty(S * cap_nodes, dtype=t32, device=dev)
         if mode in ("blocks", "warp"):
             self.edge_val = torch.empty(S * edge_stride, dtype=f64, device=dev)
+        elif mode == "regions":
+            self.edge_val = None
+            tiles = region_tiles(scen)
+            self.tiles = tiles
+            self.pos_cap = int(min(256, -(-int(cap.max()) // 4) * 4))
+            n_plan = int(((hi >= lo) & (hi >= 1)).sum()) + scen.joins
+            lib = N.load_library()
+            self.meta_stride = int(lib.ss_region_meta_bytes(L, G, tiles.n_tiles, self.pos_cap))
+            self.stream_stride = 2 * max(n_plan, 1) * 32
+            self.meta = torch.empty(S * self.meta_stride, dtype=torch.uint8, device=dev)
+            self.stream_buf = torch.empty(max(S * self.stream_stride, 2), dtype=f64, device=dev)
+            self.s_used = torch.zeros(S, dtype=t32, device=dev)
+            self.prog_status = torch.zeros(S, dtype=t32, device=dev)
+            self.tile_of = up(tiles.tile_of, t32)
+            self.bounds = up(tiles.bounds, f64)
+            self.s_rows = 32
         else:
             self.edge_val = None
             if s_cap > 256:
@@ -231,6 +317,18 @@ class ScenarioReplayer:
             if bad.size:
                 raise ValueError(f"slot program failed for scenario {int(bad[0])} (slots > {self.s_cap})")
             self.s_rows = int(max(1, used.max()))
+        elif self.mode == "regions":
+            N.check(lib.ss_region_program(self.S, self.L, self.G, N.ptr(lo_p), N.ptr(hi_p), stride,
+                                          N.ptr(self.leave), N.ptr(self.base_rtt),
+                                          N.ptr(self.seeds) if self.scen.jitter else None, N.ptr(self.tile_of),
+                                          self.tiles.n_tiles, self.pos_cap, self.meta_stride, self.stream_stride,
+                                          N.ptr(self.meta), N.ptr(self.stream_buf), N.ptr(self.s_used),
+                                          N.ptr(self.prog_status), st), "ss_region_program")
+            used = self.s_used.cpu().numpy()
+            bad = np.nonzero(self.prog_status.cpu().numpy())[0]
+            if bad.size:
+                raise ValueError(f"region program failed for scenario {int(bad[0])} (a region needs > 32 slots)")
+            self.s_rows = int(max(1, used.max()))
         elif self.scen.jitter:
             N.check(lib.ss_dag_edges(self.dag_set(), None, None, N.ptr(self.base_rtt), N.ptr(self.seeds), self.G,
                                      N.ptr(self.edge_val), st), "ss_dag_edges")
@@ -287,6 +385,13 @@ class ScenarioReplayer:
                                             self.stream_stride, self.s_cap, self.s_rows, st, N.ptr(self.occpow),
                                             self.occpow_len, self.window, n_req, ro, N.stream_handle(self.stream)),
                     "ss_replay_slots")
+        elif self.mode == "regions":
+            N.check(N.lib().ss_replay_regions(self.dag_set(), N.ptr(self.meta), self.meta_stride,
+                                              N.ptr(self.stream_buf), self.stream_stride, self.tiles.n_tiles,
+                                              self.pos_cap, self.s_rows, N.ptr(self.bounds), N.ptr(self.base_rtt),
+                                              N.ptr(self.seeds) if self.scen.jitter else None, st,
+                                              N.ptr(self.occpow), self.occpow_len, self.window, n_req, ro,
+                                              N.stream_handle(self.stream)), "ss_replay_regions")
         elif self.mode == "cluster":
             N.check(N.lib().ss_replay_slots_cluster(self.dag_set(), N.ptr(self.meta), self.meta_stride,
                                                     N.ptr(self.stream_buf), self.stream_stride, self.s_cap,
@@ -680,8 +785,8 @@ class ScenarioReplayer:
 
     def stream_bytes_per_selection(self) -> float:
         """Slot mode: bytes read from L2/HBM per selection (row/column units of every boundary)."""
-        if self.mode not in ("slots", "cluster"):
-            raise ValueError("stream bytes are defined for the slot modes")
+        if self.mode not in ("slots", "cluster", "regions"):
+            raise ValueError("stream bytes are defined for the slot and region modes")
         meta = self.meta.view(self.S, -1)[:, :16].cpu().numpy().view(np.int32)   # hdr: used, Wp, units, inserts
         return float((meta[:, 2].astype(np.int64) * meta[:, 1] * 8).mean())
 

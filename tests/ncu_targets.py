@@ -31,7 +31,7 @@ def main(what):
         else:
             rp = ScenarioReplayer(ss, window=64, mode="warp")
             rp.run(64)
-    elif what in ("slots", "blocks", "cluster"):
+    elif what in ("slots", "blocks", "cluster", "regions"):
         cl, model = scen.synthetic_cluster(256, seed=0, model=scen.bench_model(64))
         plan = allocate(cl, model)
         S = 1184

@@ -96,7 +96,8 @@ def test_replay_mode_selection():
     assert replay_mode(ss, window=64, mode="blocks") == "blocks"
     cl, model, plan = plan_for(256, 64)                 # C4: k = 73
     ss = scen.build_scenarios(cl, model, plan, 2, churn=0.0, jitter=False)
-    assert replay_mode(ss, window=64) == "slots"
+    assert replay_mode(ss, window=64) == "regions"       # 4 regions, <= 25 slots each, bound gap 6.25 ms
+    assert replay_mode(ss, window=64, mode="slots") == "slots"
     with pytest.raises(ValueError):
         replay_mode(ss, window=64, mode="warp")
     cl, model, plan = plan_for(144, 10)                 # k = 129: tile too wide for 2 CTAs/SM

@@ -1,10 +1,10 @@
 """Parity at the bench's own size ("every 97th scenario in full plus 1% random others").
 
 The headline workload exactly as bench.py builds it -- C4 pool (L64/N256, k=73), 1,184 scenarios with
-device-drawn departures + jitter, W=64 -- through both throughput kernels, for 320 requests (5 x W): the timed
+device-drawn departures + jitter, W=64 -- through every throughput kernel (regions, slots, blocks, cluster), for 320 requests (5 x W): the timed
 region's steady state, with a release before every route from request 64 on and up to 64 live chains.  Every 97th scenario
 plus a seeded 1% random sample is replayed by the oracle on the same (host-drawn, identical) scenario states
-and must match chain for chain, cost for cost, occupancy for occupancy.  The two kernels must agree on all
+and must match chain for chain, cost for cost, occupancy for occupancy.  The kernels must agree on all
 1,184 scenarios.
 """
 
@@ -28,12 +28,12 @@ def test_c4_bench_size_sampled_scenarios_vs_oracle(cuda_ready):
     seeds = shard(S, 0, 1)
     dev = scen.build_scenarios(cl, model, plan, S, churn=0.05, jitter=True, seeds=seeds, host_events=False)
     outs = {}
-    for mode in ("slots", "blocks", "cluster"):
+    for mode in ("regions", "slots", "blocks", "cluster"):
         rp = ScenarioReplayer(dev, window=W, mode=mode, max_requests=R)
         out = rp.run(R, gpus=True)
         rp.raise_first_failure()
         outs[mode] = (out.gpus.cpu().numpy(), out.cost.cpu().numpy(), rp.occ.view(S, -1).cpu().numpy())
-    for m in ("blocks", "cluster"):
+    for m in ("blocks", "cluster", "regions"):
         for a, b in zip(outs["slots"], outs[m]):
             assert np.array_equal(a, b), m
     rng = np.random.default_rng(97)

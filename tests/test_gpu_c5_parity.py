@@ -51,7 +51,7 @@ def test_c5_sub_pool(cuda_ready, c5_cases, name):
     ss = scen.build_scenarios(cl, model, plan, len(seeds), seeds=seeds, churn=0.05, jitter=True, host_events=False)
     from paper_2509_26182_b200.errors import DeviceError
     outs = {}
-    for mode in ("blocks", "slots", "cluster"):
+    for mode in ("blocks", "slots", "cluster", "regions"):
         rp = ScenarioReplayer(ss, window=W, mode=mode, max_requests=R)
         try:
             out = rp.run(R, gpus=True)

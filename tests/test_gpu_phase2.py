@@ -138,7 +138,7 @@ def _hash(gpus_row):
     return sum(splitmix64((l << 32) | int(g)) for l, g in enumerate(gpus_row)) & M
 
 
-@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks"])
+@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks", "regions"])
 @pytest.mark.parametrize("window", [64, 0, -1, 1, 7])
 def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
     """C4-shaped batch (L64/N256 pool, churn + jitter) vs the oracle, every scenario."""
@@ -166,7 +166,7 @@ def test_replay_many_scenarios_vs_oracle(cuda_ready, window, mode):
             assert int(hashes[s, r]) & ((1 << 64) - 1) == _hash(want_g[r])
 
 
-@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks", "warp"])
+@pytest.mark.parametrize("mode", ["slots", "cluster", "blocks", "warp", "regions"])
 def test_replay_tie_pool_vs_oracle(cuda_ready, mode):
     """Homogeneous flops => many exact ties (13-23% of columns): first-index rule must hold."""
     from paper_2509_26182_b200 import scenarios as scen
