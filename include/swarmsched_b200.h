@@ -400,10 +400,13 @@ int ss_replay_slots_cluster(const ss_dag_set* dags, const uint8_t* meta, int64_t
  * Same state, outputs and op script as ss_replay; results bit-identical for any input.
  *   tile_of[g]  region ("tile") of pool GPU g, 0..n_tiles-1 (<= 8 tiles); every tile's frontier must fit 32
  *               slots (status[s] = SS_BAD_INPUT otherwise);
- *   bounds      lb[n_tiles][n_tiles] then ub[n_tiles]: lb[S][D] <= every (jittered) S->D entry of the pool
- *               matrix, ub[D] >= every D->D entry.  A cross-tile block S->D of a boundary is skipped only when
- *               cmin_S + lb[S][D] > cmin_D + ub[D] (no S candidate can reach, or tie, a D minimum); the
- *               others are relaxed exactly with entries recomputed from base_rtt (x the jitter of jitter_seed);
+ *   bounds      lb[n_tiles][n_tiles], ub[n_tiles], then uni[n_tiles][n_tiles]: lb[S][D] <= every (jittered)
+ *               S->D entry of the pool matrix, ub[D] >= every D->D entry, uni[S][D] = the value of every S->D
+ *               pool entry when they are all equal (e.g. the default cross-region RTT), else NaN.  A cross-tile
+ *               block S->D of a boundary is skipped only when cmin_S + lb[S][D] > cmin_D + ub[D], or exceeds the
+ *               largest intra-tile destination minimum (no S candidate can reach, or tie, a D minimum); the
+ *               others are relaxed exactly with entries recomputed from uni[S][D] or base_rtt (x the jitter of
+ *               jitter_seed);
  *   ss_region_program: per-scenario program (meta_stride bytes >= ss_region_meta_bytes, units of stream_stride
  *               doubles), rt_used[s] = slots needed by the widest tile;
  *   ss_replay_regions: rt_rows >= max rt_used, pos_cap >= the widest column (<= 256). */

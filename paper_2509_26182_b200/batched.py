@@ -25,6 +25,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
+from . import scenarios as _scen
 from .errors import raise_for_status
 from .scenarios import ScenarioSet
 
@@ -101,15 +102,16 @@ def _explicit_widths(scen: ScenarioSet):
     return cap, held
 
 
-JITTER_MIN = 768.0 / 1024.0          # ss_jitter / scenarios.jitter_factor: dyadic factors in [768, 1279] / 1024
-JITTER_MAX = 1279.0 / 1024.0
+JITTER_MIN = float(_scen.JITTER_Q[0])     # ss_jitter / scenarios.jitter_factor: LogNormal(0, 0.2) quantile grid
+JITTER_MAX = float(_scen.JITTER_Q[-1])
 REGION_MAX_TILES = 8
 
 
 class RegionTiles:
     """Region tiling of a scenario batch for ss_replay_regions (replay_regions.cu).
 
-    tile_of[g]: the tile (a region of the pool that has GPUs) of pool GPU g; bounds = lb[T][T] ++ ub[T]:
+    tile_of[g]: the tile (a region of the pool that has GPUs) of pool GPU g; bounds = lb[T][T] ++ ub[T] ++ uni[T][T]
+    (uni[S][D]: the common value of every S x D pool entry, NaN when they differ):
     lb[S][D] = min over S x D pool pairs of fl(rtt * JITTER_MIN) (<= every jittered entry: fl is monotone),
     ub[D] = max over D x D pairs of fl(rtt * JITTER_MAX).  held[t] = slots tile t needs (frontier + the zombie
     boundary + one per join), gap = min_{S != D} lb - max ub (> 0: cross-region blocks are expected to be
@@ -127,13 +129,17 @@ class RegionTiles:
         jmin, jmax = (JITTER_MIN, JITTER_MAX) if scen.jitter else (1.0, 1.0)
         lb = np.full((T, T), np.inf)
         ub = np.zeros(T)
+        uni = np.full((T, T), np.nan)
         members = [np.nonzero(self.tile_of == t)[0] for t in range(T)]
         for a in range(T):
             ub[a] = float((rtt[np.ix_(members[a], members[a])] * jmax).max())
             for b in range(T):
                 if a != b:
-                    lb[a, b] = float((rtt[np.ix_(members[a], members[b])] * jmin).min())
-        self.bounds = np.concatenate([lb.reshape(-1), ub])
+                    blk = rtt[np.ix_(members[a], members[b])]
+                    lb[a, b] = float((blk * jmin).min())
+                    if blk.size and np.isfinite(blk.flat[0]) and (blk == blk.flat[0]).all():
+                        uni[a, b] = float(blk.flat[0])      # e.g. every pair at the default cross-region RTT
+        self.bounds = np.concatenate([lb.reshape(-1), ub, uni.reshape(-1)])
         off = lb[~np.eye(T, dtype=bool)]
         self.gap = float(off.min() - ub.max()) if T > 1 else -np.inf
         # slots per tile: GPUs held at each boundary (interval [max(lo-2,0), hi] incl. the zombie boundary)

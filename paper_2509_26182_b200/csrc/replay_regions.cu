@@ -225,13 +225,13 @@ struct RgArgs {
     int64_t meta_stride;
     const double* stream;
     int64_t stream_stride;
-    const double* bounds;        // lb[n_tiles][n_tiles], ub[n_tiles]
+    const double* bounds;        // lb[n_tiles][n_tiles], ub[n_tiles], uni[n_tiles][n_tiles]
     const double* base_rtt;      // [n_gpus][n_gpus] pool matrix (cross-tile blocks that survive the bound test)
     const int64_t* jitter_seed;  // [n_dags] or NULL
     int pos_cap, rt, nbuf, stage_bytes;
     int off_T, off_stage, off_bar, off_meta, meta_smem, off_cw, off_rw, off_cmin, off_bp, off_picks, off_tau,
         off_occ, off_stamp, off_slotgpu, off_cl, off_coff, off_red, off_misc, off_pow, pow_len, off_rel, off_seg,
-        off_bnd, total;
+        off_bnd, off_jq, off_pg, total;
     unsigned long long* cross;   // diagnostics (env SS_REGION_STATS=1): [0] blocks tested [1] blocks relaxed
 };
 
@@ -270,7 +270,7 @@ __device__ __forceinline__ int rg_ld_pair(const uint16_t* p) {
 //              reused one boundary late, so nothing relaxed at b-1 is overwritten);
 //   consumers, after it : relax boundary b inside the tile, then the cross-tile blocks the bound test keeps.
 template <int NTL>
-__global__ void __launch_bounds__((NTL + 1) * 32)
+__global__ void __launch_bounds__((NTL + 1) * 32, NTL <= 4 ? 4 : 2)
 replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     extern __shared__ __align__(128) unsigned char smem[];
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -308,6 +308,9 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     int* seg_start = reinterpret_cast<int*>(smem + A.off_seg + ((NTL * PC + 15) & ~15));
     double* lb_s = reinterpret_cast<double*>(smem + A.off_bnd);              // [NTL][NTL]
     double* ub_s = lb_s + NTL * NTL;                                          // [NTL]
+    const double* uni_s = ub_s + NTL;                                         // [NTL][NTL] uniform S->D entry or NaN
+    float* jq_s = reinterpret_cast<float*>(smem + A.off_jq);                  // [1024] jitter quantiles
+    int* pg_all = reinterpret_cast<int*>(smem + A.off_pg);                    // [2][NTL][32] source gpu | pos << 16
 
     // ---- setup ---------------------------------------------------------------
     const uint8_t* meta_g = A.meta + (int64_t)dag * A.meta_stride;
@@ -327,8 +330,10 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
         for (int q = tid; q < A.meta_smem / 16; q += NT) dstv[q] = srcv[q];
         for (int l = tid; l < nl; l += NT) coff[l] = D.col_off[l0 + l];
         for (int o = tid; o < A.pow_len; o += NT) pow_s[o] = R.occpow[o];
-        for (int q = tid; q < NTL * NTL + NTL; q += NT) lb_s[q] = A.bounds[q];
+        for (int q = tid; q < 2 * NTL * NTL + NTL; q += NT) lb_s[q] = A.bounds[q];
         for (int q = tid; q < NTL * 32; q += NT) slot_gpu[q] = 0;
+        if (A.jitter_seed)
+            for (int q = tid; q < 1024; q += NT) jq_s[q] = ss_jitter_q[q];
     }
     __syncthreads();
     const int32_t* hdr = reinterpret_cast<const int32_t*>(meta_s);
@@ -465,7 +470,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     const uint16_t* pw_g = pairs_g + (int64_t)w * (nblk + 1) * 32 + lane;   // column c: pw_g[c * 32]
     double* const cw0 = cw_all + w * 32;
     int* const rw0 = rw_all + w * 32;
-    unsigned n_test = 0, n_cross = 0;
+    unsigned n_test = 0, n_cross = 0, n_src = 0;
     int done = 0;
     rg_bar_cons(NC);
 
@@ -523,6 +528,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             int* rw = rw0 + boff * 32;
             cw[lane] = c;                                        // lanes >= n: +inf, row 0 (pairs of sources)
             rw[lane] = sl * (RG_P * 8);
+            pg_all[boff * 32 + w * 32 + lane] = sg_w[sl] | (pos << 16);   // source lane's GPU and position
             // bounds on this column's minimum cost from the high words (costs are >= 0, so their bit patterns
             // order like the values): [hi:0] <= min <= [hi+1:0] -- one REDUX instead of a 5-step shuffle tree
             const unsigned hmin = __reduce_min_sync(0xffffffffu, (unsigned)__double2hiint(c));
@@ -534,6 +540,8 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             const double ubd = __dadd_rn(cmin_hi, ub_w);                                // >= every v_j here
             const bool keep_S = cross_lane && !(__dadd_rn(cmin_all[boff + (lane < NTL ? lane : 0)], lb_lane) > ubd);
             unsigned tiles = __ballot_sync(0xffffffffu, keep_S);
+            // destination slots of boundary b (the sources of column b + 1): only their minima bound the test below
+            const unsigned dmask = __reduce_or_sync(0xffffffffu, pr_n1 != RG_PAIR_NONE ? 1u << (pr_n1 & 31) : 0u);
 
             // ---- relax boundary b inside the tile: sources in position order, strict <, two chains (even / odd
             //      sources) merged lexicographically == numpy's first-index argmin ---------------------------------
@@ -555,38 +563,59 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             // ---- cross-tile blocks the bound test keeps (rare): only their sources whose candidates can still
             //      reach ubd, entries recomputed from the pool matrix eight at a time (one L2 round trip per batch)
             if (A.cross) n_test += NTL - 1;
+            double vmax = ubd;
+            if (tiles) {
+                // the intra-region minima are known now: a source can only matter where fl(c + lb) <= some v_j,
+                // so bound by the largest destination minimum ([hi+1:0] >= v for v >= 0) instead of ubd
+                const unsigned hv = __reduce_max_sync(0xffffffffu, ((dmask >> lane) & 1u) ? (unsigned)__double2hiint(v) : 0u);
+                const double vb = hv >= 0x7ff00000u ? INF : __hiloint2double((int)(hv + 1u), 0);
+                vmax = vb < ubd ? vb : ubd;
+                unsigned t2 = 0;
+                for (unsigned tt = tiles; tt; tt &= tt - 1) {
+                    const int S = __ffs(tt) - 1;
+                    if (!(__dadd_rn(cmin_all[boff + S], lb_s[S * NTL + w]) > vmax)) t2 |= 1u << S;
+                }
+                tiles = t2;
+            }
             while (tiles) {
                 const int S = __ffs(tiles) - 1;
                 tiles &= tiles - 1;
                 const double lbS = lb_s[S * NTL + w];
+                const double uS = uni_s[S * NTL + w];                     // every S->D pool entry, or NaN
+                const bool uniform = uS == uS;
                 const double* cwS = cw_all + (boff + S) * 32;
-                const int prS = rg_ld_pair(pairs_g + ((int64_t)S * (nblk + 1) + b) * 32 + lane);
-                const bool srcS = prS != RG_PAIR_NONE;
-                unsigned keep = __ballot_sync(0xffffffffu, srcS && !(__dadd_rn(cwS[lane], lbS) > ubd));
-                if (keep) ++n_cross;
-                const int gsl = slot_gpu[S * 32 + (prS & 31)];           // lane k: source k's GPU and position
-                const int psl = (prS >> 8) & 0xff;
+                // sources of S: lanes whose cost is finite (lanes >= the column length publish +inf)
+                unsigned keep = __ballot_sync(0xffffffffu, cwS[lane] < INF && !(__dadd_rn(cwS[lane], lbS) > vmax));
+                if (A.cross) { n_cross += keep != 0; n_src += __popc(keep); }
+                const int pgl = pg_all[(boff + S) * 32 + lane];          // lane k: source k's GPU and position
+                const int gsl = pgl & 0xffff;
+                const int psl = pgl >> 16;
                 const int gd = sg_w[lane];
+                // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
+                // from the shared-memory table, four sources per round
                 while (keep) {
-                    int kk[8];
-                    double e[8];
+                    constexpr int KB = 4;
+                    int kk[KB], gs[KB];
+                    double e[KB];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < KB; ++q) {
                         kk[q] = keep ? __ffs(keep) - 1 : -1;
                         keep &= keep - 1;
                     }
-                    int gs[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) gs[q] = __shfl_sync(0xffffffffu, gsl, kk[q] & 31);
+                    for (int q = 0; q < KB; ++q) gs[q] = __shfl_sync(0xffffffffu, gsl, kk[q] & 31);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) e[q] = kk[q] >= 0 ? A.base_rtt[(int64_t)gs[q] * G + gd] : INF;
+                    for (int q = 0; q < KB; ++q) {
+                        double x = kk[q] < 0 ? INF : (uniform ? uS : A.base_rtt[(int64_t)gs[q] * G + gd]);
+                        if (A.jitter_seed && kk[q] >= 0)
+                            x = __dmul_rn(x, (double)jq_s[ss_jitter_index(mix, (uint32_t)gs[q], (uint32_t)gd)]);
+                        e[q] = x;
+                    }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < KB; ++q) {
                         const int p = __shfl_sync(0xffffffffu, psl, kk[q] & 31);
                         if (kk[q] < 0) continue;
-                        double x = e[q];
-                        if (A.jitter_seed) x = x * ss_jitter(mix, (uint32_t)gs[q], (uint32_t)gd);
-                        const double a = __dadd_rn(cwS[kk[q]], x);
+                        const double a = __dadd_rn(cwS[kk[q]], e[q]);
                         if (a < v || (a == v && p < pv)) { v = a; pv = p; }
                     }
                 }
@@ -681,6 +710,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     if (A.cross && lane == 0) {
         atomicAdd(&A.cross[0], (unsigned long long)n_test);
         atomicAdd(&A.cross[1], (unsigned long long)n_cross);
+        atomicAdd(&A.cross[2], (unsigned long long)n_src);
     }
     for (int g = tid; g < ng; g += NC) R.st.occ[gbase + g] = occ_s[g];
     if (tid == 0) {
@@ -760,7 +790,7 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     A.off_cw = o;      o += 2 * n_tiles * 32 * 8;
     A.off_rw = o;      o += 2 * n_tiles * 32 * 4;
     A.off_cmin = o;    o += rg_align(2 * n_tiles * 8, 16);
-    A.off_bnd = o;     o += rg_align((n_tiles * n_tiles + n_tiles) * 8, 16);
+    A.off_bnd = o;     o += rg_align((2 * n_tiles * n_tiles + n_tiles) * 8, 16);
     A.off_bp = o;      o += rg_align((L - 1) * pos_cap, 16);
     A.off_picks = o;   o += rg_align(L * 4, 16);
     A.off_tau = o;     o += rg_align(D.max_gpus * 8, 16);
@@ -774,6 +804,8 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     A.off_pow = o;     o += rg_align(A.pow_len * 8, 16);
     A.off_rel = o;     o += rg_align((L + 1) * 4, 16);
     A.off_seg = o;     o += rg_align(n_tiles * pos_cap, 16) + rg_align(n_tiles * 4, 16);
+    A.off_pg = o;      o += 2 * n_tiles * 32 * 4;
+    A.off_jq = o;      o += jitter_seed ? 1024 * 4 : 0;
     A.total = o;
     if (A.total > 227 * 1024) return SS_BAD_INPUT;
     RgReplayArgs R{};
@@ -786,8 +818,8 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     cudaStream_t s = ss_stream(stream_h);
     if (R.out.chain_hash) cudaMemsetAsync(R.out.chain_hash, 0, sizeof(uint64_t) * (size_t)D.n_dags * n_req, s);
     const bool stats = getenv("SS_REGION_STATS") != nullptr;
-    if (stats && cudaMalloc(&A.cross, 2 * sizeof(unsigned long long)) == cudaSuccess)
-        cudaMemsetAsync(A.cross, 0, 2 * sizeof(unsigned long long), s);
+    if (stats && cudaMalloc(&A.cross, 3 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(A.cross, 0, 3 * sizeof(unsigned long long), s);
     auto run = [&](auto kern) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
             return SS_CUDA_ERROR;
@@ -808,11 +840,12 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     }
     if (rc != SS_OK) return rc;
     if (A.cross) {
-        unsigned long long h[2];
+        unsigned long long h[3];
         cudaMemcpyAsync(h, A.cross, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        fprintf(stderr, "region stats: smem=%d rt=%d tiles=%d | cross blocks tested %llu relaxed %llu (%.4f%%)\n",
-                A.total, rt_rows, n_tiles, h[0], h[1], h[0] ? 100.0 * (double)h[1] / (double)h[0] : 0.0);
+        fprintf(stderr, "region stats: smem=%d rt=%d tiles=%d | cross blocks tested %llu relaxed %llu (%.4f%%), "
+                "%.2f sources per relaxed block\n", A.total, rt_rows, n_tiles, h[0], h[1],
+                h[0] ? 100.0 * (double)h[1] / (double)h[0] : 0.0, h[1] ? (double)h[2] / (double)h[1] : 0.0);
         cudaFree(A.cross);
     }
     return SS_OK;

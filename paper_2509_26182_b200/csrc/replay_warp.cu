@@ -36,7 +36,8 @@ struct WarpReplay {
 
 // NWD = 1: one warp owns the scenario (<= 8 hosts per column, warp_route).  NWD = 2..4: the destinations of
 // every boundary are spread over NWD warps (mw_route); the rest of the request stays on warp 0.
-template <int NWD, int SPL, bool MAT = false>
+// LPD > 0: pad_route over padded edge blocks (LPD lanes per destination, SPL sources per lane, NWD warps).
+template <int NWD, int SPL, bool MAT = false, int LPD = 0>
 __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, WarpLayout A, WarpReplay R) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NT = NWD * 32;
@@ -63,11 +64,17 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
     double* costs = reinterpret_cast<double*>(smem + A.off_cost);   // [2][40] column costs (32 hosts + 8 pad)
     __shared__ double vshare;
     __shared__ int flag[3];
+    __shared__ int ishare[16];
+    int* pdst = reinterpret_cast<int*>(smem + A.off_dst);
+    uint8_t* path = smem + A.off_path;
 
     // ---- one-time staging: columns, edges, per-GPU state, ring --------------
-    if (warp == 0)
+    if (warp == 0) {
         flag[0] = stage_dag(D, A, l0, nl, E, node, cl, noff, eoff, lane,
                             A.mat_dim ? R.mat + (int64_t)dag * A.mat_dim * A.mat_dim : nullptr) ? 0 : 1;
+        if (LPD > 0 && !flag[0]) stage_pad_dst(node, cl, noff, nblk, A.pad, D.max_gpus, pdst, lane);
+        if (lane == 0) tau[D.max_gpus] = INF;                       // pad_route's sentinel slot
+    }
     __syncthreads();
     if (flag[0]) {
         if (tid == 0) R.st.status[dag] = SS_BAD_INPUT;
@@ -129,7 +136,10 @@ __global__ void __launch_bounds__(NWD * 32) replay_warp_kernel(ss_dag_set D, War
         mark(0);
         // ---- DP over the layer columns + final argmin / backtrack ------------------
         double v;
-        if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_pitch);
+        if constexpr (LPD > 0)
+            v = pad_route<LPD, SPL, NWD>(E, pdst, node, cl, nblk, tau, costs, bp, picks, path, D.max_layers, &vshare,
+                                         ishare, tid);
+        else if constexpr (NWD == 1) v = warp_route<MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, lane, A.mat_pitch);
         else v = mw_route<NWD, SPL, MAT>(E, node, cl, noff, eoff, nblk, tau, costs, bp, picks, &vshare, tid, A.mat_pitch);
         mark(1);
         if (tid == 0 && R.out.cost) R.out.cost[(int64_t)dag * n_req + r] = v;
@@ -355,6 +365,27 @@ __global__ void __launch_bounds__(NWD * 32) admission_warp_kernel(ss_dag_set D, 
 
 }  // namespace
 
+// Latency path (a batch that fits on the SMs, 9..32 hosts, edge-block mode): pad_route with LPD lanes per
+// destination over padded edge blocks.  Returns LPD (1, 2, 4) or 0 for mw_route.  Env SS_WARP_ROUTE=mw|pad1|pad2|pad4.
+static int warp_pad_lpd(const ss_dag_set& D, bool mat) {
+    if (D.max_hosts <= 8 || D.max_hosts > 32 || mat) return 0;
+    int lpd = D.n_dags <= sm_count() ? 2 : 0;
+    if (const char* e = getenv("SS_WARP_ROUTE")) {
+        if (e[0] == 'm') lpd = 0;
+        else if (e[0] == 'p') lpd = atoi(e + 3);
+    }
+    return (lpd == 1 || lpd == 2 || lpd == 4) ? lpd : 0;
+}
+
+// padded width P = LPD * HS for the instantiated shapes (HS rounded up), 0 if none fits
+static int warp_pad_width(int lpd, int hosts) {
+    static const int hs1[] = {12, 18, 24, 32}, hs2[] = {6, 9, 12, 16}, hs4[] = {3, 5, 6, 8};
+    const int* hs = lpd == 1 ? hs1 : (lpd == 2 ? hs2 : hs4);
+    for (int k = 0; k < 4; ++k)
+        if (lpd * hs[k] >= hosts) return lpd * hs[k];
+    return 0;
+}
+
 extern "C" int64_t ss_replay_warp_smem(const ss_dag_set* dags, int32_t window, int32_t occpow_len, int32_t mat_dim) {
     if (!dags) return -1;
     WarpLayout A{};
@@ -370,6 +401,12 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
     if (!D.edge_val || !D.edge_off) return SS_BAD_INPUT;
     WarpLayout A{};
     if (!warp_layout(D, window, occpow_len, A, mat ? mat_dim : 0)) return SS_BAD_INPUT;
+    int lpd = warp_pad_lpd(D, A.mat_dim > 0);
+    if (lpd > 0) {
+        WarpLayout Ap{};
+        if (warp_layout(D, window, occpow_len, Ap, 0, warp_pad_width(lpd, D.max_hosts))) A = Ap;
+        else lpd = 0;                                            // padded blocks do not fit: mw_route
+    }
     WarpReplay R{};
     R.mat = mat;
     R.st = *st;
@@ -390,9 +427,28 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
         kern<<<D.n_dags, threads, A.total, s>>>(D, A, R);
         return SS_OK;
     };
-    // destinations per boundary over ceil(hosts / 8) warps (latency: C2's 17 hosts -> 3 warps)
     int rc;
     const bool mm = A.mat_dim > 0;                               // matrix mode: separate instantiations
+    if (lpd > 0) {
+        const int P = A.pad;
+        if (lpd == 1) {
+            if (P == 12) rc = run(replay_warp_kernel<1, 12, false, 1>, 32);
+            else if (P == 18) rc = run(replay_warp_kernel<1, 18, false, 1>, 32);
+            else if (P == 24) rc = run(replay_warp_kernel<1, 24, false, 1>, 32);
+            else rc = run(replay_warp_kernel<1, 32, false, 1>, 32);
+        } else if (lpd == 2) {
+            if (P == 12) rc = run(replay_warp_kernel<1, 6, false, 2>, 32);
+            else if (P == 18) rc = run(replay_warp_kernel<2, 9, false, 2>, 64);
+            else if (P == 24) rc = run(replay_warp_kernel<2, 12, false, 2>, 64);
+            else rc = run(replay_warp_kernel<2, 16, false, 2>, 64);
+        } else {
+            if (P == 12) rc = run(replay_warp_kernel<2, 3, false, 4>, 64);
+            else if (P == 20) rc = run(replay_warp_kernel<3, 5, false, 4>, 96);
+            else if (P == 24) rc = run(replay_warp_kernel<3, 6, false, 4>, 96);
+            else rc = run(replay_warp_kernel<4, 8, false, 4>, 128);
+        }
+    } else {
+    // destinations per boundary over ceil(hosts / 8) warps (C2's 17 hosts -> 3 warps)
     switch ((D.max_hosts + 3) / 4) {                             // source slots per lane
         case 0: case 1: case 2: rc = mm ? run(replay_warp_kernel<1, 8, true>, 32) : run(replay_warp_kernel<1, 8>, 32); break;
         case 3: rc = mm ? run(replay_warp_kernel<2, 3, true>, 64) : run(replay_warp_kernel<2, 3>, 64); break;
@@ -401,6 +457,7 @@ extern "C" int ss_replay_warp(const ss_dag_set* dags, const ss_replay_state* st,
         case 6: rc = mm ? run(replay_warp_kernel<3, 6, true>, 96) : run(replay_warp_kernel<3, 6>, 96); break;
         case 7: rc = mm ? run(replay_warp_kernel<4, 7, true>, 128) : run(replay_warp_kernel<4, 7>, 128); break;
         default: rc = mm ? run(replay_warp_kernel<4, 8, true>, 128) : run(replay_warp_kernel<4, 8>, 128); break;
+    }
     }
     if (rc != SS_OK) return rc;
     SS_CHECK_LAUNCH();

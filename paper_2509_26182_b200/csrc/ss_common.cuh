@@ -25,11 +25,21 @@ __host__ __device__ __forceinline__ uint64_t ss_splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-// Pair jitter of scenarios.py:jitter_factor -- exact dyadic factor in [0.75, 1.25).
-__device__ __forceinline__ double ss_jitter(uint64_t seed_mix, uint32_t i, uint32_t j) {
+// Pair jitter of scenarios.py:jitter_factor -- one LogNormal(0, 0.2) factor per unordered GPU pair (SURVEY.md
+// 8(d) C4), drawn by inverse-CDF sampling on the 1024 float32 quantiles of jitter_lognormal.inc (the file
+// scenarios.py parses too, so host and device scenario matrices are the same IEEE products rtt * (double)Q[i]).
+// Global memory, not __constant__: the lanes of a warp index different entries.
+static __device__ const float ss_jitter_q[1024] = {
+#include "jitter_lognormal.inc"
+};
+
+__device__ __forceinline__ uint32_t ss_jitter_index(uint64_t seed_mix, uint32_t i, uint32_t j) {
     if (i > j) { uint32_t t = i; i = j; j = t; }
-    uint64_t h = ss_splitmix64(seed_mix ^ ((uint64_t(i) << 32) | uint64_t(j)));
-    return double(768u + uint32_t(h % 512u)) / 1024.0;
+    return (uint32_t)(ss_splitmix64(seed_mix ^ ((uint64_t(i) << 32) | uint64_t(j))) & 1023u);
+}
+
+__device__ __forceinline__ double ss_jitter(uint64_t seed_mix, uint32_t i, uint32_t j) {
+    return (double)__ldg(&ss_jitter_q[ss_jitter_index(seed_mix, i, j)]);
 }
 
 // ---------------------------------------------------------------------------

@@ -19,8 +19,9 @@ struct WarpLayout {
     int mat_dim;       // > 0: the scenario's whole RTT matrix (mat_dim^2 fp64) replaces the edge blocks in E
     int mat_pitch;     // its row pitch in E: odd (mat_dim | 1), so lanes gathering one column from different
                        // source rows (mw_route: 4 source lanes per destination) hit different banks
+    int pad;           // > 0: padded edge blocks (pad_route): block b = E + b * pad^2, E_b[i * pad + j], +inf padded
     int off_E, off_node, off_cl, off_noff, off_eoff, off_bp, off_picks, off_tau, off_base, off_occ, off_stamp,
-        off_ring, off_pow, off_cost, off_kv, off_tcap, total;
+        off_ring, off_pow, off_cost, off_kv, off_tcap, off_dst, off_path, total;
 };
 
 __device__ __forceinline__ void lexmin(double& v, int& i, double v2, int i2) {
@@ -48,7 +49,12 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
                 e += cl[l] * cl[l + 1];
             }
         }
-        if (A.mat_dim == 0 && e > A.e_cap) bad = 1;
+        if (A.pad > 0) {
+            if ((int64_t)nblk * A.pad * A.pad > A.e_cap) bad = 1;
+            for (int l = 0; l < nl; ++l) if (cl[l] > A.pad) bad = 1;
+        } else if (A.mat_dim == 0 && e > A.e_cap) {
+            bad = 1;
+        }
         cl[nl] = bad;                                            // scratch flag (cl has max_layers + 1 slots)
     }
     __syncwarp();
@@ -56,7 +62,16 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
     for (int l = 0; l < nl; ++l) {
         const int len = cl[l];
         if (lane < len) node[noff[l] + lane] = D.node_gpu[D.col_off[l0 + l] + lane];
-        if (l < nblk && A.mat_dim == 0) {
+        if (l < nblk && A.pad > 0) {
+            const double INF = __longlong_as_double(0x7ff0000000000000ll);
+            const double* src = D.edge_val + D.edge_off[l0 + l];
+            const int P = A.pad, rd = cl[l + 1];
+            double* dst = E + (int64_t)l * P * P;
+            for (int q = lane; q < P * P; q += 32) {
+                const int i = q / P, j = q - i * P;
+                dst[q] = (i < len && j < rd) ? src[i * rd + j] : INF;
+            }
+        } else if (l < nblk && A.mat_dim == 0) {
             const double* src = D.edge_val + D.edge_off[l0 + l];
             const int cnt = len * cl[l + 1];
             for (int q = lane; q < cnt; q += 32) E[eoff[l] + q] = src[q];
@@ -71,6 +86,18 @@ __device__ inline bool stage_dag(const ss_dag_set& D, const WarpLayout& A, int l
     }
     __syncwarp();
     return true;
+}
+
+// pad_route's destination table: dst[b * P + j] = the GPU of position j in column b + 1 (its tau index), or
+// `sentinel` (a tau slot holding +inf) past the column and for the two spare rows b = nblk, nblk + 1 that the
+// two-boundary-ahead prefetch reads.  Called by one warp after stage_dag.
+__device__ inline void stage_pad_dst(const int* node, const int* cl, const int* noff, int nblk, int P, int sentinel,
+                                     int* dst, int lane) {
+    for (int q = lane; q < (nblk + 2) * P; q += 32) {
+        const int b = q / P, j = q - b * P;
+        dst[q] = (b < nblk && j < cl[b + 1]) ? node[noff[b + 1] + j] : sentinel;
+    }
+    __syncwarp();
 }
 
 // Chain DP of one request on a warp-resident DAG (router.py:163-197): lane j owns host j of the next column;
@@ -146,6 +173,150 @@ __device__ inline double warp_route(const double* E, const int* node, const int*
     return v;
 }
 
+// Chain DP of one request over padded edge blocks (A.pad = P = LPD * HS >= every column length): lane group j
+// (LPD adjacent lanes, NWD = ceil(P * LPD / 32) warps) owns destination j; lane h of the group scans the HS
+// sources [h * HS, (h + 1) * HS).  Block b is E + b * P^2 with E_b[i][j] at i * P + j and +inf past the column
+// lengths, so every edge load has a compile-time offset from one per-boundary base and needs no predicate; the
+// destination's tau comes from dst[] (stage_pad_dst; +inf sentinel past the column, so c = v + tau is +inf there
+// without a branch), loaded two boundaries ahead.  Per lane: HS independent DADDs and a first-index tournament
+// (left operands hold lower source indices, the right one wins only on a strict `<`); then log2(LPD) shuffle
+// rounds in which the lane holding the lower index range takes its partner only on `<`, the other on `<=`, so
+// every lane of the group ends with the same lexicographic (value, index) minimum == numpy's first-index argmin
+// (all-+inf resolves to 0) and all of them store it (same value, same address: no predicate).  The costs of a
+// column sit in shared memory with every lane group's segment 16-B aligned (slot(i) = (i / HS) * CS + i % HS,
+// CS = HS rounded up to even) and are read as double2 broadcasts.  One warp: __syncwarp per boundary; more:
+// one named barrier.  The backtrack is segment-parallel: every thread but the last chases one start position of
+// a lower segment (recording its path), the last thread chases the chosen end through the top segment, and the
+// segment ends are chained by one thread.  Same contract as warp_route.
+template <int LPD, int HS, int NWD>
+__device__ double pad_route(const double* E, const int* dst, const int* node, const int* cl, int nblk,
+                            const double* tau, double* costs, uint8_t* bp, int* picks, uint8_t* path, int L,
+                            double* vshare, int* ishare, int tid) {
+    constexpr int P = LPD * HS;
+    constexpr int CS = (HS + 1) & ~1;
+    constexpr int NT = NWD * 32;
+    static_assert(LPD == 1 || LPD == 2 || LPD == 4, "pad_route: 1, 2 or 4 lanes per destination");
+    static_assert(LPD * CS <= 39 && P <= 32 && P * LPD <= NT, "pad_route: shape");
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const int j0 = tid / LPD, h = tid % LPD;
+    const bool own = j0 < P;                                   // idle lanes store into spare slots
+    const int j = own ? j0 : 0;
+    const int js = own ? (j / HS) * CS + j % HS : 39;          // cost slot written (39: spare)
+    const int jb = own ? j : 31;                               // backpointer column written (31: spare when P < 32)
+    auto sync = [] { if (NWD == 1) __syncwarp(); else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
+    for (int i = tid; i < P; i += NT) costs[(i / HS) * CS + i % HS] = i < cl[0] ? tau[node[i]] : INF;
+    const double* ep = E + (h * HS) * P + j;
+    double e[HS];
+#pragma unroll
+    for (int k = 0; k < HS; ++k) e[k] = nblk > 0 ? ep[k * P] : INF;
+    double td = tau[dst[j]];                                   // boundary 0's destination tau
+    int dn1 = dst[P + j];                                      // boundary 1's destination GPU
+    sync();
+    for (int b = 0; b < nblk; ++b) {
+        const double* cs = costs + (b & 1) * 40 + h * CS;
+        double* nx = costs + ((b & 1) ^ 1) * 40;
+        // every cost load issued before the first add (one shared-memory round trip per boundary)
+        double c[HS];
+#pragma unroll
+        for (int k = 0; k + 1 < HS; k += 2) {
+            const double2 c2 = *reinterpret_cast<const double2*>(cs + k);
+            c[k] = c2.x;
+            c[k + 1] = c2.y;
+        }
+        if (HS & 1) c[HS - 1] = cs[HS - 1];
+        double a[HS];
+        int ix[HS];
+#pragma unroll
+        for (int k = 0; k < HS; ++k) {
+            a[k] = __dadd_rn(c[k], e[k]);
+            ix[k] = k;
+        }
+#pragma unroll
+        for (int w = 1; w < HS; w <<= 1)
+#pragma unroll
+            for (int k = 0; k + w < HS; k += 2 * w)
+                if (a[k + w] < a[k]) { a[k] = a[k + w]; ix[k] = ix[k + w]; }
+        double best = a[0];
+        int bi = h * HS + ix[0];
+#pragma unroll
+        for (int o = 1; o < LPD; o <<= 1) {
+            const double v2 = __shfl_xor_sync(FULL, best, o);
+            const int i2 = __shfl_xor_sync(FULL, bi, o);
+            const bool take = (h & o) ? !(best < v2) : (v2 < best);   // partner holds lower indices iff h & o
+            best = take ? v2 : best;
+            bi = take ? i2 : bi;
+        }
+        nx[js] = __dadd_rn(best, td);
+        bp[b * 32 + jb] = (uint8_t)bi;
+        // next boundary's operands (independent of the costs): edges, tau of its destinations, GPUs of b + 2's
+        ep += P * P;
+        if (b + 1 < nblk) {
+#pragma unroll
+            for (int k = 0; k < HS; ++k) e[k] = ep[k * P];
+        }
+        td = tau[dn1];
+        dn1 = dst[(b + 2) * P + j];
+        sync();
+    }
+    const double* cl_last = costs + (nblk & 1) * 40;
+    if (tid < 32) {
+        const int ln = tid;
+        double v = ln < cl[nblk] ? cl_last[(ln / HS) * CS + ln % HS] : INF;
+        int idx = ln < cl[nblk] ? ln : NONE;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(FULL, v, o);
+            const int i2 = __shfl_xor_sync(FULL, idx, o);
+            lexmin(v, idx, v2, i2);
+        }
+        if (ln == 0) {
+            *vshare = v;
+            ishare[0] = idx;
+        }
+    }
+    if (NWD == 1) __syncwarp(); else __syncthreads();
+    const double v = *vshare;
+    if (!(v <= DBL_MAX)) return v;
+    // segment-parallel backtrack: nlow lower segments x P start positions + one thread for the top segment
+    constexpr int NLOW = (NT - 1) / P;
+    constexpr int NSEG = NLOW + 1;
+    const int top_lo = NLOW * nblk / NSEG;
+    if (tid == NT - 1) {
+        int p = ishare[0];
+        picks[nblk] = p;
+        for (int b = nblk - 1; b >= top_lo; --b) {
+            p = bp[b * 32 + p];
+            picks[b] = p;
+        }
+    } else if (tid < NLOW * P) {
+        const int sg = tid / P;
+        const int lo = sg * nblk / NSEG, hi = (sg + 1) * nblk / NSEG;
+        int p = tid % P;
+        uint8_t* pt = path + tid * L;
+        for (int b = hi - 1; b >= lo; --b) {
+            p = bp[b * 32 + min(p, 31)];
+            pt[b - lo] = (uint8_t)p;
+        }
+    }
+    if (NWD == 1) __syncwarp(); else __syncthreads();
+    if (tid == 0) {
+        int cur = picks[top_lo];                                 // position at the top segment's low column
+        for (int sg = NLOW - 1; sg >= 0; --sg) {
+            ishare[1 + sg] = cur;
+            cur = path[(sg * P + cur) * L];                       // position at the segment's low column
+        }
+    }
+    if (NWD == 1) __syncwarp(); else __syncthreads();
+    for (int b = tid; b < top_lo; b += NT) {
+        int sg = 0;
+        while (sg + 1 < NLOW && b >= (sg + 1) * nblk / NSEG) ++sg;
+        const int lo = sg * nblk / NSEG;
+        picks[b] = path[(sg * P + ishare[1 + sg]) * L + (b - lo)];
+    }
+    if (NWD == 1) __syncwarp(); else __syncthreads();
+    return v;
+}
+
 inline int align16(int x) { return (x + 15) / 16 * 16; }
 
 // mat_dim > 0 offers matrix mode (the caller has per-scenario RTT matrices of that dimension).  It is taken
@@ -164,10 +335,14 @@ inline int sm_count() {
     return n;
 }
 
-inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A, int mat_dim = 0) {
-    if (D.max_hosts > 32 || D.max_layers < 1) return false;
-    const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * D.max_hosts * D.max_hosts;
-    A.mat_dim = (mat_dim > 0 && (int64_t)mat_dim * (mat_dim | 1) < e_cap && D.n_dags > sm_count()) ? mat_dim : 0;
+inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len, WarpLayout& A, int mat_dim = 0,
+                        int pad = 0) {
+    if (D.max_hosts > 32 || D.max_layers < 1 || pad < 0 || pad > 32 || (pad > 0 && pad < D.max_hosts)) return false;
+    const int hw = pad > 0 ? pad : D.max_hosts;
+    const int64_t e_cap = (int64_t)(D.max_layers > 1 ? D.max_layers - 1 : 0) * hw * hw;
+    A.pad = pad;
+    A.mat_dim = (pad == 0 && mat_dim > 0 && (int64_t)mat_dim * (mat_dim | 1) < e_cap && D.n_dags > sm_count())
+                    ? mat_dim : 0;
     A.mat_pitch = A.mat_dim | 1;
     const int64_t ring_len = window > 0 ? (int64_t)window * (D.max_layers + 1) : 0;
     if (e_cap > (1 << 20) || ring_len > (1 << 20)) return false;
@@ -182,7 +357,7 @@ inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len,
     A.off_eoff = o;   o += align16(D.max_layers * 4);
     A.off_bp = o;     o += align16(D.max_layers * 32);
     A.off_picks = o;  o += align16(D.max_layers * 4);
-    A.off_tau = o;    o += align16(D.max_gpus * 8);
+    A.off_tau = o;    o += align16((D.max_gpus + 1) * 8);          // + the +inf sentinel slot (pad_route)
     A.off_base = o;   o += align16(D.max_gpus * 8);
     A.off_occ = o;    o += align16(D.max_gpus * 4);
     A.off_stamp = o;  o += align16(D.max_gpus * 4);
@@ -191,6 +366,8 @@ inline bool warp_layout(const ss_dag_set& D, int32_t window, int32_t occpow_len,
     A.off_cost = o;   o += 2 * 40 * 8;
     A.off_kv = o;     o += align16(D.max_gpus * 8);
     A.off_tcap = o;   o += align16(D.max_gpus * 8);
+    A.off_dst = o;    o += pad > 0 ? align16((D.max_layers + 1) * pad * 4) : 0;
+    A.off_path = o;   o += pad > 0 ? align16(128 * D.max_layers) : 0;
     A.total = o;
     return A.total <= 227 * 1024;
 }

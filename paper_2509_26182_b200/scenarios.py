@@ -6,14 +6,17 @@
   10 ms default across), so a pool built here is the reference's pool.
 * Scenario states (C4/C5) are the base pool after churn (a seeded set of plan
   GPUs leaves, as ``MembershipManager.on_leave`` would, no rebalance) and with
-  a seeded per-pair RTT jitter.  The jitter factor is an exactly representable
-  dyadic rational derived from a splitmix64 hash, so the device generator
-  (``ss_scenario_rtt``) and the host/oracle produce bit-identical RTTs:
-  ``rtt_ab * ((768 + h % 512) / 1024)``, i.e. a uniform factor in [0.75, 1.25).
+  a seeded per-pair RTT jitter: one LogNormal(0, 0.2) factor per unordered GPU
+  pair, quantile ``h & 1023`` of the 1024-point float32 grid
+  in ``csrc/jitter_lognormal.inc`` with h the pair's splitmix64 hash.  Kernels and
+  host read the same committed table, so the device generators
+  (``ss_scenario_rtt``, the edge / unit writers) and the host/oracle produce
+  bit-identical RTTs: ``rtt_ab * Q[h & 1023]``.
 """
 
 from __future__ import annotations
 
+import os
 import random
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -122,10 +125,25 @@ def pair_hash(seed: int, i: int, j: int) -> int:
     return splitmix64((splitmix64(seed & MASK64) ^ ((i << 32) | j)) & MASK64)
 
 
+def _jitter_table() -> np.ndarray:
+    """The 1024 LogNormal(0, 0.2) float32 quantiles of csrc/jitter_lognormal.inc (the kernels include the same file)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "jitter_lognormal.inc")
+    with open(path) as fh:
+        vals = [float.fromhex(t) for line in fh if not line.startswith("//")
+                for t in line.replace(",", " ").split()]
+    if len(vals) != 1024:
+        raise RuntimeError(f"{path}: expected 1024 quantiles, found {len(vals)}")
+    return np.array(vals, dtype=np.float64)
+
+
+JITTER_Q = _jitter_table()
+
+
 def jitter_factor(seed: int, i: int, j: int) -> float:
+    """One LogNormal(0, 0.2) factor per unordered GPU pair: quantile h & 1023 of JITTER_Q."""
     if i > j:
         i, j = j, i
-    return (768 + pair_hash(seed, i, j) % 512) / 1024.0
+    return float(JITTER_Q[pair_hash(seed, i, j) & 1023])
 
 
 def jitter_factor_matrix(seed: int, n: int) -> np.ndarray:
@@ -138,7 +156,7 @@ def jitter_factor_matrix(seed: int, n: int) -> np.ndarray:
         x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         x = x ^ (x >> np.uint64(31))
-    f = (768.0 + (x % np.uint64(512)).astype(np.float64)) / 1024.0
+    f = JITTER_Q[(x & np.uint64(1023)).astype(np.int64)]
     out = np.ones((n, n))
     out[i, j] = f
     out[j, i] = f

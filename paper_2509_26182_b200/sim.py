@@ -5,7 +5,8 @@ Same names, fields and semantics as the reference for the pieces the hot path fe
 * ``Request`` (sim.py:62-76), the trace wire format ``request_from_dict`` / ``request_to_dict`` /
   ``load_trace`` / ``save_trace`` (79-115, JSON lines ``{"id", "t", "prompt_tokens", "output_tokens"}``);
 * ``generate_trace`` (118-148): Poisson arrivals from ``random.Random(seed)``, ids ``r00000``...;
-* ``percentile`` (151-159, nearest rank) and ``MetricsReport`` (190-217);
+* ``percentile`` (151-159, nearest rank), ``LatencyModel`` (161-186, the tau law of the device replays) and
+  ``MetricsReport`` (190-217);
 * ``baseline_plan`` (513-553): the naive placement the simulator is compared against (capacity-sorted first fit,
   equal-speed water-fill through the device ``solve_lambda`` / ``hamilton_round``);
 * ``run_simulation`` (478-510): the discrete-event serving simulation of one cluster / plan / trace.  The event
@@ -100,6 +101,31 @@ def percentile(values: Sequence[float], p: float) -> float:
         raise ValueError(f"p must be in (0, 100], got {p}")
     ordered = sorted(values)
     return ordered[max(1, math.ceil(p * len(ordered) / 100.0)) - 1]
+
+
+class LatencyModel:
+    """Per-layer step time from GPU speed plus a contention multiplier (sim.py:161-186): the tau law every device
+    replay applies, tau(g) = base(g) * occpow[occ(g)] with base(g) = flops_per_layer_per_token / flops(g) and
+    occpow[o] = (1 + o) ** e (``batched.occ_power_table``).
+
+    ``manager`` is anything with ``gpu(gpu_id) -> GpuNode`` -- the reference passes its MembershipManager; a
+    ``ClusterSnapshot`` works the same way here.
+    """
+
+    def __init__(self, model: ModelSpec, manager, contention_exponent: float = 1.0):
+        self.model = model
+        self.manager = manager
+        self.contention_exponent = contention_exponent
+
+    def base_s(self, gpu_id: str) -> float:
+        return self.model.flops_per_layer_per_token / self.manager.gpu(gpu_id).flops
+
+    def published(self, gpu_id: str, layer: int, occupancy: int) -> float:
+        """What the GPU advertises: the step time a new chain would see (occupancy + itself)."""
+        return self.base_s(gpu_id) * (1 + occupancy) ** self.contention_exponent
+
+    def executing(self, gpu_id: str, live_chains: int) -> float:
+        return self.base_s(gpu_id) * max(1, live_chains) ** self.contention_exponent
 
 
 @dataclass(frozen=True)

@@ -100,3 +100,27 @@ def test_regions_matches_slots_on_c4_batch(cuda_ready):
     for m in ("slots", "blocks"):
         for a, b in zip(res["regions"], res[m]):
             assert np.array_equal(a, b), m
+
+
+def test_regions_nonuniform_cross_links_vs_oracle(cuda_ready):
+    """Explicit cross-region links of different RTTs (uni[S][D] = NaN): kept blocks read the pool matrix entry by
+    entry instead of the per-tile-pair constant; many are kept (cross links 0.9-1.6 ms vs 1 ms inside)."""
+    import random
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import region_tiles
+    from paper_2509_26182_b200.topology import ClusterSnapshot
+    cl, model, plan = _pool(96, 40, seed=7)
+    rng = random.Random(7)
+    ids = sorted(g.id for g in cl.gpus)
+    links = dict(cl.links)
+    for i in range(len(ids)):
+        for j in range(i + 1, len(ids)):
+            a, b = cl.gpu(ids[i]), cl.gpu(ids[j])
+            if a.region != b.region and rng.random() < 0.5:
+                links[(ids[i], ids[j])] = rng.uniform(0.0009, 0.0016)
+    cl2 = ClusterSnapshot(gpus=cl.gpus, links=links, default_cross_region_rtt_s=0.0012)
+    ss = scen.build_scenarios(cl2, model, plan, 10, seed0=300, churn=0.05, jitter=True)
+    t = region_tiles(ss)
+    T = t.n_tiles
+    assert np.isnan(t.bounds[T * T + T:]).reshape(T, T)[~np.eye(T, dtype=bool)].all()
+    _check(ss, 70, 16)

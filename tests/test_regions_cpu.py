@@ -22,8 +22,14 @@ def _check_bounds(ss, n_scen):
     t = region_tiles(ss)
     T = t.n_tiles
     lb = t.bounds[:T * T].reshape(T, T)
-    ub = t.bounds[T * T:]
+    ub = t.bounds[T * T:T * T + T]
+    uni = t.bounds[T * T + T:].reshape(T, T)
     mem = [np.nonzero(t.tile_of == k)[0] for k in range(T)]
+    base = np.asarray(ss.base_rtt)
+    for a in range(T):                     # uni[S][D]: the common pool value the kernel multiplies by the jitter
+        for b in range(T):
+            if a != b and np.isfinite(uni[a, b]):
+                assert np.all(base[np.ix_(mem[a], mem[b])] == uni[a, b])
     for s in range(n_scen):
         m = ss.scenario_rtt(s)
         for a in range(T):
@@ -40,6 +46,8 @@ def test_region_bounds_hold_on_c4_scenarios():
     ss = scen.build_scenarios(cl, model, _plan(cl, model), 24, seed0=3, churn=0.05, jitter=True)
     t = _check_bounds(ss, 24)
     assert t.n_tiles == 4 and t.fits() and t.gap > 0
+    uni = t.bounds[20:].reshape(4, 4)
+    assert np.all(uni[~np.eye(4, dtype=bool)] == 0.010)      # every cross pair at the default cross-region RTT
 
 
 def test_region_bounds_hold_on_c5_scenarios():
@@ -48,6 +56,8 @@ def test_region_bounds_hold_on_c5_scenarios():
     ss = scen.build_scenarios(cl, model, _plan(cl, model), 6, seed0=11, churn=0.05, jitter=True)
     t = _check_bounds(ss, 6)
     assert t.n_tiles == 8 and t.fits() and t.gap > 0
+    uni = t.bounds[72:].reshape(8, 8)
+    assert np.isfinite(uni[~np.eye(8, dtype=bool)]).all()   # the explicit table is uniform per region pair
 
 
 def test_region_tiles_without_jitter_are_the_pool_extremes():
@@ -58,4 +68,4 @@ def test_region_tiles_without_jitter_are_the_pool_extremes():
     t = region_tiles(ss)
     T = t.n_tiles
     assert np.all(t.bounds[:T * T].reshape(T, T)[~np.eye(T, dtype=bool)] == 0.010)   # default cross-region RTT
-    assert np.all(t.bounds[T * T:] == 0.001)                                          # intra-region links
+    assert np.all(t.bounds[T * T:T * T + T] == 0.001)                                 # intra-region links

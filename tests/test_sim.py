@@ -227,3 +227,19 @@ def test_baseline_plan_matches_reference(cuda_ready):
         d = plan_to_dict(baseline_plan(cl, model))
         d["objective"] = float(d["objective"]).hex()
         assert d == c["plan"], name
+
+
+def test_latency_model_is_the_device_tau_law():
+    """LatencyModel (sim.py:161-186) == the tau every device replay applies: base_tau[g] * occpow[occ]."""
+    from paper_2509_26182_b200 import LatencyModel, scenarios as scen
+    from paper_2509_26182_b200.batched import occ_power_table
+    ss = pool({"n": 16, "L": 32})
+    cl, model = scen.synthetic_cluster(16, seed=0, model=scen.bench_model(32))
+    for e in (1.0, 0.5, 2.0):
+        lm = LatencyModel(model, cl, contention_exponent=e)
+        pw = occ_power_table(8, e)
+        for g, gid in enumerate(ss.ids):
+            assert lm.base_s(gid) == ss.base_tau[g]
+            for o in range(8):
+                assert lm.published(gid, 1, o) == ss.base_tau[g] * pw[o]
+            assert lm.executing(gid, 0) == lm.executing(gid, 1) == ss.base_tau[g] * 1.0 ** e
