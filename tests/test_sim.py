@@ -103,12 +103,16 @@ def test_dropin_trace_api_matches_reference_draws(sim_cases, tmp_path):
         Request("x", 0.0, 0, 1)
 
 
-def test_run_simulation_rejects_what_the_device_path_does_not_run():
-    from paper_2509_26182_b200 import run_simulation
-    with pytest.raises(NotImplementedError):
-        run_simulation(None, None, None, [], membership_events=[object()])
-    with pytest.raises(NotImplementedError):
-        run_simulation(None, None, None, [], ttl_multiplier=0.5)
+def test_membership_event_validation():
+    """MembershipEvent (membership.py:55-70): joins carry a GPU record (their id becomes gpu_id), leaves an id."""
+    from paper_2509_26182_b200 import MembershipEvent
+    from paper_2509_26182_b200.topology import GpuNode
+    g = GpuNode(id="x", region="r", vram_bytes=1e10, flops=1e14)
+    assert MembershipEvent(at_s=1.0, kind="join", gpu=g).gpu_id == "x"
+    assert MembershipEvent(at_s=1.0, kind="leave", gpu_id="y").gpu is None
+    for bad in (dict(kind="join"), dict(kind="leave"), dict(kind="move", gpu_id="y")):
+        with pytest.raises(ValueError):
+            MembershipEvent(at_s=0.0, **bad)
 
 
 @pytest.mark.gpu
