@@ -357,16 +357,9 @@ class PoolResults:
         return [int(x) for x in self.counts[base: base + total]]
 
 
-def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int], tokens: float, stream=None):
-    """estimate_objective_params for many regions on device.
-
-    items: list of (flops_in_cluster_order, links) where links is a list of
-    (a_idx, b_idx, rtt) with region-local cluster-order indices.  Returns
-    device tensors (t_comp, rtt).
-    """
-    torch = _torch()
-    lib = N.lib()
-    dev = torch.device("cuda")
+def objective_pack(items, layers: Sequence[int]):
+    """Host arrays of estimate_objective_params for many regions (see objective_device): name -> ndarray for one
+    Upload, plus (regions, link count, total matrix entries)."""
     n = np.array([len(f) for f, _ in items], dtype=np.int64)
     item_ptr = np.concatenate([[0], np.cumsum(n)])
     mat_off = np.concatenate([[0], np.cumsum(n * n)])
@@ -378,33 +371,53 @@ def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int
             la.append(a)
             lb.append(b)
             lv.append(v)
-    st = N.stream_handle(stream)
-    I = len(items)
-    nl = len(li)
-    up = Upload()                                          # one H2D for every input of the call
-    up.add("ints", np.concatenate([item_ptr, n, layers, li, la, lb]).astype(np.int32))
-    up.add("off", mat_off[:-1].astype(np.int64))
-    up.add("lv", np.asarray(lv if nl else [0.0], dtype=np.float64))
-    up.add("flops", flops)
-    dv = up.upload(dev, stream)
-    ints = dv["ints"]
+    I, nl = len(items), len(li)
+    if I > 65535:
+        raise ValueError("at most 65535 objective regions per call")
+    arrays = {"obj_ints": np.concatenate([item_ptr, n, layers, li, la, lb]).astype(np.int32),
+              "obj_off": mat_off[:-1].astype(np.int64),
+              "obj_lv": np.asarray(lv if nl else [0.0], dtype=np.float64),
+              "obj_flops": flops}
+    return arrays, (I, nl, int(mat_off[-1]))
+
+
+def objective_launch(dv, meta, default_rtt: float, fpl: float, tokens: float, stream=None):
+    """Launch ss_rtt_fill + ss_objective on uploaded objective_pack arrays; returns device (t_comp, rtt)."""
+    torch = _torch()
+    lib = N.lib()
+    dev = dv["obj_flops"].device
+    I, nl, mat_total = meta
+    ints = dv["obj_ints"]
     item_ptr_d, dim_d = ints[:I + 1], ints[I + 1:2 * I + 1]
     layers_d = ints[2 * I + 1:3 * I + 1]
     li_d, la_d, lb_d = ints[3 * I + 1:3 * I + 1 + nl], ints[3 * I + 1 + nl:3 * I + 1 + 2 * nl], ints[3 * I + 1 + 2 * nl:]
-    off_d = dv["off"]
-    lv_d = dv["lv"] if nl else None
-    flops_d = dv["flops"]
-    rtt = torch.empty(max(int(mat_off[-1]), 1), dtype=torch.float64, device=dev)
-    if I > 65535:
-        raise ValueError("at most 65535 objective regions per call")
+    off_d, flops_d = dv["obj_off"], dv["obj_flops"]
+    lv_d = dv["obj_lv"] if nl else None
+    st = N.stream_handle(stream)
+    rtt = torch.empty(max(mat_total, 1), dtype=torch.float64, device=dev)
     N.check(lib.ss_rtt_fill(I, N.ptr(off_d), N.ptr(dim_d), N.ptr(rtt), float(default_rtt), nl,
                             N.ptr(li_d) if nl else None, N.ptr(la_d) if nl else None, N.ptr(lb_d) if nl else None,
                             N.ptr(lv_d), st), "ss_rtt_fill")
-    t = torch.empty(I, dtype=torch.float64, device=dev)
-    r = torch.empty(I, dtype=torch.float64, device=dev)
+    tr = torch.empty(2 * I, dtype=torch.float64, device=dev)
+    t, r = tr[:I], tr[I:]
     N.check(lib.ss_objective(I, N.ptr(item_ptr_d), N.ptr(flops_d), N.ptr(off_d), N.ptr(rtt), float(fpl),
                              N.ptr(layers_d), float(tokens), N.ptr(t), N.ptr(r), st), "ss_objective")
     return t, r
+
+
+def objective_device(items, default_rtt: float, fpl: float, layers: Sequence[int], tokens: float, stream=None):
+    """estimate_objective_params for many regions on device.
+
+    items: list of (flops_in_cluster_order, links) where links is a list of
+    (a_idx, b_idx, rtt) with region-local cluster-order indices.  Returns
+    device tensors (t_comp, rtt).
+    """
+    torch = _torch()
+    arrays, meta = objective_pack(items, layers)
+    up = Upload()                                          # one H2D for every input of the call
+    for name, arr in arrays.items():
+        up.add(name, arr)
+    return objective_launch(up.upload(torch.device("cuda"), stream), meta, default_rtt, fpl, tokens, stream)
 
 
 def objective_dense(flops_cluster_order, rtt_mats, fpl: float, layers: int, tokens: float, stream=None):

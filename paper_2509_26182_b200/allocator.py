@@ -25,7 +25,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native as N
-from ._phase1 import PoolBatch, PoolSpec, objective_device
+from ._phase1 import PoolBatch, PoolSpec, objective_device, objective_launch, objective_pack
 from .errors import DegenerateObjective, NoFeasiblePipeline, SS_OK, raise_for_status
 from .plan import AllocationPlan, PerKEntry, Pipeline
 from .topology import ClusterSnapshot, GpuNode, LayerSlice, ModelSpec, layer_capacity
@@ -167,17 +167,21 @@ def allocate(cluster: ClusterSnapshot, model: ModelSpec, *, alpha: float = 1.0,
         raise NoFeasiblePipeline(f"no region can host all {L} layers of {model.name!r}")
     pools = [PoolSpec(oc, [g.flops for g in og], L, km) for _, _, og, oc, km in packed]
     a = params.alpha if params is not None else alpha
-    # k ** alpha table and the variant pointer ride along in the batch's single H2D copy
-    batch = PoolBatch(pools, extra={"kpow": _kpow_table(max(p.kmax for p in pools), a),
-                                    "var_ptr": np.array([0, len(pools)], dtype=np.int32)},
-                      defer_workspace_check=True)
+    # k ** alpha table, the variant pointer and the objective inputs ride along in the batch's single H2D copy
+    extra = {"kpow": _kpow_table(max(p.kmax for p in pools), a), "var_ptr": np.array([0, len(pools)], dtype=np.int32)}
+    if params is not None:
+        extra["tr"] = np.concatenate([np.full(len(pools), params.t_comp_seconds),
+                                      np.full(len(pools), params.rtt_seconds)])
+    else:
+        obj_arrays, obj_meta = objective_pack(_region_items(cluster, [p[1] for p in packed]), [L] * len(pools))
+        extra.update(obj_arrays)
+    batch = PoolBatch(pools, extra=extra, defer_workspace_check=True)
     batch.stage_counts()
     if params is not None:
-        t = np.full(len(pools), params.t_comp_seconds)
-        r = np.full(len(pools), params.rtt_seconds)
+        t, r = batch.extra["tr"][:len(pools)], batch.extra["tr"][len(pools):]
     else:
-        t, r = objective_device(_region_items(cluster, [p[1] for p in packed]), cluster.default_cross_region_rtt_s,
-                                model.flops_per_layer_per_token, [L] * len(pools), mean_tokens_per_request)
+        t, r = objective_launch(batch.extra, obj_meta, cluster.default_cross_region_rtt_s,
+                                model.flops_per_layer_per_token, mean_tokens_per_request)
     batch.score_and_best(t, r, batch.extra["kpow"])
     # objective_total: the reference's left fold over regions (allocator.py:588), on device
     lib = N.lib()

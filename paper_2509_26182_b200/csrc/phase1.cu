@@ -1065,47 +1065,62 @@ __global__ void score_fill_kernel(ss_pool_set P, const int64_t* koff, const int3
 }
 
 // per pool: best k by (z, k); water-fill the best k's groups unless already filled
+// One CTA per pool: thread 0 picks the best k (ascending k, ties -> the larger k, the first failing score raises);
+// without fill_all the chosen k's groups are water-filled in parallel, one thread per group, and the pool takes
+// the status of the lowest failing group -- the group the reference's sequential loop raises on.
 __global__ void best_k_kernel(ss_pool_set P, const int64_t* koff, const int32_t* stages, const int32_t* members,
                               const int32_t* gsize, const double* z, const int32_t* kstatus,
                               const int32_t* fstatus, int fill_all, int32_t* best_k, int32_t* counts,
                               int32_t* pool_status) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P.n_pools) return;
-    best_k[p] = 0;
-    if (pool_status[p] != SS_OK) return;
-    int bk = 0;
-    double bz = 0.0;
-    for (int k = 1; k <= P.kmax[p]; ++k) {
-        const int64_t ko = koff[p] + k - 1;
-        if (stages[ko] == 0) continue;
-        if (kstatus[ko] != SS_OK) { pool_status[p] = kstatus[ko]; return; }   // score raises for any k
-        if (bk == 0 || z[ko] >= bz) { bk = k; bz = z[ko]; }                 // ascending k: ties -> larger k
+    const int p = blockIdx.x;
+    __shared__ int s_bk;
+    __shared__ unsigned long long s_err;                     // (group << 32) | status of the lowest failing group
+    if (threadIdx.x == 0) {
+        s_bk = 0;
+        s_err = ~0ull;
+        best_k[p] = 0;
+        if (pool_status[p] == SS_OK) {
+            int bk = 0;
+            double bz = 0.0;
+            bool bad = false;
+            for (int k = 1; k <= P.kmax[p] && !bad; ++k) {
+                const int64_t ko = koff[p] + k - 1;
+                if (stages[ko] == 0) continue;
+                if (kstatus[ko] != SS_OK) { pool_status[p] = kstatus[ko]; bad = true; break; }
+                if (bk == 0 || z[ko] >= bz) { bk = k; bz = z[ko]; }
+            }
+            if (!bad) {
+                best_k[p] = bk;
+                if (bk > 0 && fill_all && fstatus && fstatus[koff[p] + bk - 1] != SS_OK)
+                    pool_status[p] = fstatus[koff[p] + bk - 1];
+                if (!fill_all) s_bk = bk;
+            }
+        }
     }
-    best_k[p] = bk;
+    __syncthreads();
+    const int bk = s_bk;
     if (bk == 0) return;
-    if (fill_all) {
-        if (fstatus && fstatus[koff[p] + bk - 1] != SS_OK) pool_status[p] = fstatus[koff[p] + bk - 1];
-        return;
-    }
     const int off = P.pool_ptr[p], n_all = P.pool_ptr[p + 1] - off;
     const int kmax = P.kmax[p];
     const int* mem = members + P.memb_off[p] + (int64_t)(bk - 1) * n_all;
     const int* gs = gsize + P.gsz_off[p] + (int64_t)(bk - 1) * kmax;
     int* cnt = counts + P.memb_off[p] + (int64_t)(bk - 1) * n_all;
-    int pos = 0;
-    int capv[NMAX];
-    double flv[NMAX];
-    for (int g = 0; g < bk; ++g) {
+    for (int g = threadIdx.x; g < bk; g += blockDim.x) {
+        int pos = 0;
+        for (int q = 0; q < g; ++q) pos += gs[q];
         const int sz = gs[g];
+        int capv[NMAX];
+        double flv[NMAX];
         for (int q = 0; q < sz; ++q) {
             capv[q] = P.caps[off + mem[pos + q]];
             flv[q] = P.flops[off + mem[pos + q]];
         }
         int aux = 0;
         const int wst = stage_lengths(flv, capv, sz, P.layers[p], cnt + pos, &aux);
-        if (wst != SS_OK) { pool_status[p] = wst; return; }
-        pos += sz;
+        if (wst != SS_OK) atomicMin(&s_err, ((unsigned long long)g << 32) | (unsigned)wst);
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_err != ~0ull) pool_status[p] = (int32_t)(unsigned)(s_err & 0xffffffffull);
 }
 
 __global__ void variant_reduce_kernel(int32_t n_var, const int32_t* var_ptr, const int64_t* koff, const int32_t* best_k,
@@ -1307,9 +1322,9 @@ extern "C" int ss_phase1_best(const ss_pool_set* pools, const int64_t* koff, con
                               const int32_t* fstatus, int32_t fill_all, int32_t* best_k, int32_t* counts,
                               int32_t* pool_status, void* stream) {
     if (!pools || pools->n_pools <= 0) return SS_OK;
-    best_k_kernel<<<grid_for(pools->n_pools, 64), 64, 0, ss_stream(stream)>>>(*pools, koff, stages, members, gsize, z,
-                                                                             kstatus, fstatus, fill_all, best_k,
-                                                                             counts, pool_status);
+    best_k_kernel<<<pools->n_pools, fill_all ? 32 : 128, 0, ss_stream(stream)>>>(*pools, koff, stages, members, gsize,
+                                                                                z, kstatus, fstatus, fill_all, best_k,
+                                                                                counts, pool_status);
     SS_CHECK_LAUNCH();
     return SS_OK;
 }
