@@ -33,7 +33,6 @@ namespace {
 
 constexpr int RG_HDR = 16;
 constexpr int RG_MAX_TILES = 8;
-constexpr int RG_P = 34;               // tile row pitch (doubles): 16-B aligned rows, 2-way conflicts on column writes
 constexpr int RG_BAR_ALL = 3;          // consumers + producer
 constexpr int RG_BAR_CONS = 4;         // consumers only
 constexpr int RG_POS_NONE = 0xffff;
@@ -228,7 +227,7 @@ struct RgArgs {
     const double* bounds;        // lb[n_tiles][n_tiles], ub[n_tiles], uni[n_tiles][n_tiles]
     const double* base_rtt;      // [n_gpus][n_gpus] pool matrix (cross-tile blocks that survive the bound test)
     const int64_t* jitter_seed;  // [n_dags] or NULL
-    int pos_cap, rt, nbuf, stage_bytes;
+    int pos_cap, rt, tp, nbuf, stage_bytes;
     int off_T, off_stage, off_bar, off_meta, meta_smem, off_cw, off_rw, off_cmin, off_bp, off_picks, off_tau,
         off_occ, off_stamp, off_slotgpu, off_cl, off_coff, off_red, off_misc, off_pow, pow_len, off_rel, off_seg,
         off_bnd, off_jq, off_pg, total;
@@ -280,6 +279,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int PC = A.pos_cap;
     const int RT = A.rt;
+    const int TP = A.tp;                                      // tile row pitch (doubles, even)
     const int l0 = D.layer_ptr[dag];
     const int nl = D.layer_ptr[dag + 1] - l0;
     const int nblk = nl - 1;
@@ -385,7 +385,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             const double* s0 = stream_g + (int64_t)m.unit_start * Wp;
             for (int u = lane; u < m.n_ins; u += 32) {
                 const int code = ins[2 * (m.ins_start + u)];
-                bulk_g2s(T + ((code >> 5) * RT + (code & 31)) * RG_P, s0 + (int64_t)u * Wp, ub, rows_bar);
+                bulk_g2s(T + ((code >> 5) * RT + (code & 31)) * TP, s0 + (int64_t)u * Wp, ub, rows_bar);
             }
             ++rows_issued;
         };
@@ -411,13 +411,13 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                         // unit pairs (row, column) of one entering GPU: T_t[q][lane] and T_t[lane][q]
                         for (int ul = 0; ul < nu; ul += 2) {
                             const int code = ins[2 * (m.ins_start + ((u0 + ul) >> 1))];
-                            double* Tt = T + (code >> 5) * RT * RG_P;
+                            double* Tt = T + (code >> 5) * RT * TP;
                             const int q = code & 31;
                             const double xr = stg[ul * Wp];
                             const double xc = stg[(ul + 1) * Wp];
                             if (live) {
-                                Tt[q * RG_P + lane] = xr;
-                                Tt[lane * RG_P + q] = xc;
+                                Tt[q * TP + lane] = xr;
+                                Tt[lane * TP + q] = xc;
                             }
                         }
                         __syncwarp();
@@ -461,7 +461,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
         }
     };
     if (n_req > 0) prefetch_release(req0);
-    const double* Tw = T + w * RT * RG_P;
+    const double* Tw = T + w * RT * TP;
     int* sg_w = slot_gpu + w * 32;
     const double ub_w = ub_s[w];
     // lane S < NTL, S != w: the bound of source tile S against this tile (lane-parallel block test)
@@ -527,7 +527,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             double* cw = cw0 + boff * 32;
             int* rw = rw0 + boff * 32;
             cw[lane] = c;                                        // lanes >= n: +inf, row 0 (pairs of sources)
-            rw[lane] = sl * (RG_P * 8);
+            rw[lane] = sl * (TP * 8);
             pg_all[boff * 32 + w * 32 + lane] = sg_w[sl] | (pos << 16);   // source lane's GPU and position
             // bounds on this column's minimum cost from the high words (costs are >= 0, so their bit patterns
             // order like the values): [hi:0] <= min <= [hi+1:0] -- one REDUX instead of a 5-step shuffle tree
@@ -783,7 +783,12 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     A.nbuf = g_rg_nbuf;
     const int L = D.max_layers;
     int o = 0;
-    A.off_T = o;       o += rg_align(n_tiles * rt_rows * RG_P * 8, 128);
+    // tile row pitch: >= the unit length (rt_rows + 1, even), even so bulk-copied rows stay 16-B aligned; lanes past
+    // the pitch read the next row (their slots are not destinations), the last row's by the 32-double pad
+    A.tp = (rt_rows + 2) & ~1;
+    if (const char* e = getenv("SS_REGION_TP")) { const int tp = atoi(e); if (tp >= A.tp && tp % 2 == 0) A.tp = tp; }
+    if (const char* e = getenv("SS_REGION_NBUF")) { const int nb = atoi(e); if (nb >= 1 && nb <= 8) A.nbuf = nb; }
+    A.off_T = o;       o += rg_align((n_tiles * rt_rows * A.tp + 32) * 8, 128);
     A.off_stage = o;   o += A.nbuf * A.stage_bytes;
     A.off_bar = o;     o += 128;
     A.off_meta = o;    o += rg_align(A.meta_smem, 16);
