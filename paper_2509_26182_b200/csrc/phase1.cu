@@ -291,22 +291,20 @@ struct Bits {
 
 __device__ __forceinline__ bool bits_test(const Bits& b, int i) { return (b.w[i >> 6] >> (i & 63)) & 1ull; }
 
-struct Frame {          // one peel() activation; its pool = range(m) minus the picks of frames above it
+struct Frame {          // one peel() activation
     Mask picked;
+    Mask avail;         // its pool: range(m) minus the picks of the frames above it (set when the frame is entered)
     int total, need;
     short targets[4];
     signed char nt, ti;
 };
 
-__device__ void frame_pool(const Frame* fr, int d, int m, Mask& pool) {
+__device__ void range_mask(int m, Mask& pool) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {                            // range(m) word by word
         const int lo = w * 64;
         pool.w[w] = m >= lo + 64 ? ~0ull : (m > lo ? (1ull << (m - lo)) - 1ull : 0ull);
     }
-    for (int q = 0; q < d; ++q)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) pool.w[w] &= ~fr[q].picked.w[w];
 }
 
 __device__ int pool_items(const Mask& pool, int m, uint16_t* items) {
@@ -318,37 +316,84 @@ __device__ int pool_items(const Mask& pool, int m, uint16_t* items) {
     return n;
 }
 
-// reach[p + 1] = reach[p] | ((reach[p] << v_p) & (2^(2L) - 1)) with the running set kept in registers
-__device__ void compute_reach(const int* caps, int L, const uint16_t* items, int n, Bits* reach) {
-    static_assert(BWORDS == 4, "compute_reach is written for 4 words");
+// Subset-sum reach rows reach[p + 1] = reach[p] | ((reach[p] << v_p) & (2^(2L) - 1)), up to 256 bits.  The rows
+// live in the thread's local memory and only their ceil(2L / 64) live words are stored and read back (2 of 4 at
+// L = 64), which halves the peel's local-memory traffic there.  Checkpointing every 2nd-8th row and rebuilding the
+// rest in registers during the walk cut DRAM traffic 5x but measured 5-9% slower at C3 (L = 80), so every row is
+// kept.
+struct Reach4 { uint64_t r0, r1, r2, r3; };
+
+__device__ __forceinline__ void reach_step(Reach4& r, int s, const uint64_t* lim) {
+    const int ws = s >> 6, bs = s & 63;
+    const uint64_t w0 = ws == 0 ? r.r0 : 0ull;
+    const uint64_t w1 = ws == 0 ? r.r1 : (ws == 1 ? r.r0 : 0ull);
+    const uint64_t w2 = ws == 0 ? r.r2 : (ws == 1 ? r.r1 : (ws == 2 ? r.r0 : 0ull));
+    const uint64_t w3 = ws == 0 ? r.r3 : (ws == 1 ? r.r2 : (ws == 2 ? r.r1 : (ws == 3 ? r.r0 : 0ull)));
+    // (lo >> 1) >> (63 - bs) == lo >> (64 - bs) for bs >= 1 and 0 for bs == 0 (no 64-bit shift by 64)
+    r.r0 |= (w0 << bs) & lim[0];
+    r.r1 |= ((w1 << bs) | ((w0 >> 1) >> (63 - bs))) & lim[1];
+    r.r2 |= ((w2 << bs) | ((w1 >> 1) >> (63 - bs))) & lim[2];
+    r.r3 |= ((w3 << bs) | ((w2 >> 1) >> (63 - bs))) & lim[3];
+}
+
+__device__ __forceinline__ void reach_limits(int L, uint64_t* lim) {
     const int nbits = 2 * L;
-    uint64_t lim[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int lo = q * 64;
         lim[q] = lo >= nbits ? 0ull : (nbits - lo >= 64 ? ~0ull : (1ull << (nbits - lo)) - 1ull);
     }
-    uint64_t r0 = 1, r1 = 0, r2 = 0, r3 = 0;
-    reach[0].w[0] = r0; reach[0].w[1] = 0; reach[0].w[2] = 0; reach[0].w[3] = 0;
+}
+
+__device__ __forceinline__ bool reach_test(const Reach4& r, int i) {
+    const int w = i >> 6;
+    const uint64_t x = w == 0 ? r.r0 : (w == 1 ? r.r1 : (w == 2 ? r.r2 : r.r3));
+    return (x >> (i & 63)) & 1ull;
+}
+
+__device__ __forceinline__ void reach_store(Reach4& dst, const Reach4& r, int nw) {
+    dst.r0 = r.r0;
+    dst.r1 = r.r1;
+    if (nw > 2) dst.r2 = r.r2;
+    if (nw > 3) dst.r3 = r.r3;
+}
+
+__device__ __forceinline__ bool reach_load_test(const Reach4& src, int i) {
+    const int w = i >> 6;                                    // i < 2L: only live words are read
+    const uint64_t x = w == 0 ? src.r0 : (w == 1 ? src.r1 : (w == 2 ? src.r2 : src.r3));
+    return (x >> (i & 63)) & 1ull;
+}
+
+// forward pass: rows[p] = reach[p] for p <= n (live words only), returns reach[n]
+__device__ Reach4 compute_reach(const int* caps, int L, const uint16_t* items, int n, Reach4* rows) {
+    static_assert(BWORDS == 4, "reach rows are 4 words");
+    uint64_t lim[4];
+    reach_limits(L, lim);
+    const int nw = (2 * L + 63) >> 6;
+    Reach4 r{1ull, 0ull, 0ull, 0ull};
+    reach_store(rows[0], r, nw);
     for (int p = 0; p < n; ++p) {
-        const int s = cval(caps, items[p], L);
-        const int ws = s >> 6, bs = s & 63;
-        const uint64_t w0 = ws == 0 ? r0 : 0ull;
-        const uint64_t w1 = ws == 0 ? r1 : (ws == 1 ? r0 : 0ull);
-        const uint64_t w2 = ws == 0 ? r2 : (ws == 1 ? r1 : (ws == 2 ? r0 : 0ull));
-        const uint64_t w3 = ws == 0 ? r3 : (ws == 1 ? r2 : (ws == 2 ? r1 : (ws == 3 ? r0 : 0ull)));
-        // (lo >> 1) >> (63 - bs) == lo >> (64 - bs) for bs >= 1 and 0 for bs == 0 (no 64-bit shift by 64)
-        r0 |= (w0 << bs) & lim[0];
-        r1 |= ((w1 << bs) | ((w0 >> 1) >> (63 - bs))) & lim[1];
-        r2 |= ((w2 << bs) | ((w1 >> 1) >> (63 - bs))) & lim[2];
-        r3 |= ((w3 << bs) | ((w2 >> 1) >> (63 - bs))) & lim[3];
-        reach[p + 1].w[0] = r0; reach[p + 1].w[1] = r1; reach[p + 1].w[2] = r2; reach[p + 1].w[3] = r3;
+        reach_step(r, cval(caps, items[p], L), lim);
+        reach_store(rows[p + 1], r, nw);
+    }
+    return r;
+}
+
+// the try's backward walk (allocator.py:401-409): from the last item down, an item is picked unless the reach row
+// before it already holds the remaining target
+__device__ void reach_walk(const int* caps, int L, const uint16_t* items, int n, const Reach4* rows, int tgt,
+                           Mask& picked) {
+    int rem = tgt;
+    for (int pos = n - 1; pos >= 0; --pos) {
+        if (reach_load_test(rows[pos], rem)) continue;
+        picked.set(items[pos]);
+        rem -= cval(caps, items[pos], L);
     }
 }
 
 // returns true on success; the k groups are then fr[0..k-1].picked, in peel order
 // cancel (optional): the parallel-m search's best success so far; an attempt at a larger m gives up
-__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reach, uint16_t* items,
+__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck, uint16_t* items,
                      const volatile int32_t* cancel = nullptr) {
     int budget = m <= 24 ? 300 : 80;
     int d = 0;
@@ -356,6 +401,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
     for (int i = 0; i < m; ++i) total += cval(caps, i, L);
     fr[0].total = total;
     fr[0].need = k;
+    range_mask(m, fr[0].avail);
     enum { ENTER, TRY, RET } state = ENTER;
     bool ok = false;
     int reach_owner = -1;
@@ -366,8 +412,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
             if (budget <= 0) { ok = false; state = RET; continue; }
             --budget;
             if (cancel && *cancel < m) return false;        // a smaller m already succeeded
-            Mask pool;
-            frame_pool(fr, d, m, pool);
+            const Mask pool = f.avail;
             if (f.total < f.need * L || pool.count() < f.need) { ok = false; state = RET; continue; }
             if (f.need == 1) {
                 int short_ = L;
@@ -383,11 +428,11 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
                 continue;
             }
             const int n = pool_items(pool, m, items);
-            compute_reach(caps, L, items, n, reach);
+            const Reach4 last = compute_reach(caps, L, items, n, ck);
             reach_owner = d;
             f.nt = 0;
             for (int t = L; t < 2 * L && f.nt < 4; ++t)
-                if (bits_test(reach[n], t)) f.targets[f.nt++] = (short)t;
+                if (reach_test(last, t)) f.targets[f.nt++] = (short)t;
             f.ti = 0;
             state = TRY;
             continue;
@@ -395,21 +440,16 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Bits* reac
         if (state == TRY) {
             Frame& f = fr[d];
             if (f.ti >= f.nt) { ok = false; state = RET; continue; }
-            Mask pool;
-            frame_pool(fr, d, m, pool);
-            const int n = pool_items(pool, m, items);
-            if (reach_owner != d) { compute_reach(caps, L, items, n, reach); reach_owner = d; }
+            const int n = pool_items(f.avail, m, items);
+            if (reach_owner != d) { compute_reach(caps, L, items, n, ck); reach_owner = d; }
             const int tgt = f.targets[f.ti];
-            int rem = tgt;
             f.picked.clear();
-            for (int pos = n - 1; pos >= 0; --pos) {
-                if (bits_test(reach[pos], rem)) continue;
-                f.picked.set(items[pos]);
-                rem -= cval(caps, items[pos], L);
-            }
+            reach_walk(caps, L, items, n, ck, tgt, f.picked);
             Frame& c = fr[d + 1];
             c.total = f.total - tgt;
             c.need = f.need - 1;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) c.avail.w[w] = f.avail.w[w] & ~f.picked.w[w];
             ++d;
             state = ENTER;
             continue;
@@ -829,7 +869,7 @@ __device__ bool cover_setup(const ss_pool_set& P, const int64_t* koff, int p, in
 }
 
 // One attempt at group count m: best-fit, then peel.  On success writes the groups when mout != nullptr.
-__device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr, Bits* reach, uint16_t* items,
+__device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr, Reach4* reach, uint16_t* items,
                           int* mout, int* gout, int32_t* stage_out, const volatile int32_t* cancel = nullptr) {
     if (best_fit(cc.caps, m, k, cc.L, G, cancel)) {
         if (mout) {
@@ -874,7 +914,7 @@ __global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages
     if (!feasible) { stall[cc.ko] = 2; return; }                // reference `break` (infeasible k)
     Lists G;
     Frame fr[KMAX + 2];
-    Bits reach[NMAX + 1];
+    Reach4 reach[NMAX + 1];
     uint16_t items[NMAX];
     int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
     int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
@@ -900,7 +940,7 @@ __global__ void cover_try_kernel(ss_pool_set P, const int64_t* koff, const int32
     if (m > cc.n) return;
     Lists G;
     Frame fr[KMAX + 2];
-    Bits reach[NMAX + 1];
+    Reach4 reach[NMAX + 1];
     uint16_t items[NMAX];
     if (cover_try(cc, k, m, G, fr, reach, items, nullptr, nullptr, nullptr, best_m + c)) atomicMin(&best_m[c], m);
 }
@@ -922,7 +962,7 @@ __global__ void cover_finish_kernel(ss_pool_set P, const int64_t* koff, int32_t*
     if (m < cc.m0 || m > cc.n) { stall[cc.ko] = 1; return; }
     Lists G;
     Frame fr[KMAX + 2];
-    Bits reach[NMAX + 1];
+    Reach4 reach[NMAX + 1];
     uint16_t items[NMAX];
     int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
     int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
