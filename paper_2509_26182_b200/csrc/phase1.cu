@@ -359,8 +359,7 @@ __device__ __forceinline__ void reach_store(Reach4& dst, const Reach4& r, int nw
 }
 
 __device__ __forceinline__ bool reach_load_test(const Reach4& src, int i) {
-    const int w = i >> 6;                                    // i < 2L: only live words are read
-    const uint64_t x = w == 0 ? src.r0 : (w == 1 ? src.r1 : (w == 2 ? src.r2 : src.r3));
+    const uint64_t x = (&src.r0)[i >> 6];                    // one load: the word holding bit i (< 2L, live)
     return (x >> (i & 63)) & 1ull;
 }
 
@@ -404,7 +403,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
     range_mask(m, fr[0].avail);
     enum { ENTER, TRY, RET } state = ENTER;
     bool ok = false;
-    int reach_owner = -1;
+    int reach_owner = -1, owner_n = 0;
     for (;;) {
         if (state == ENTER) {
             Frame& f = fr[d];
@@ -430,6 +429,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
             const int n = pool_items(pool, m, items);
             const Reach4 last = compute_reach(caps, L, items, n, ck);
             reach_owner = d;
+            owner_n = n;
             f.nt = 0;
             for (int t = L; t < 2 * L && f.nt < 4; ++t)
                 if (reach_test(last, t)) f.targets[f.nt++] = (short)t;
@@ -440,8 +440,14 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
         if (state == TRY) {
             Frame& f = fr[d];
             if (f.ti >= f.nt) { ok = false; state = RET; continue; }
-            const int n = pool_items(f.avail, m, items);
-            if (reach_owner != d) { compute_reach(caps, L, items, n, ck); reach_owner = d; }
+            // items[] and the reach rows still hold this frame's unless a deeper frame overwrote them
+            int n = owner_n;
+            if (reach_owner != d) {
+                n = pool_items(f.avail, m, items);
+                compute_reach(caps, L, items, n, ck);
+                reach_owner = d;
+                owner_n = n;
+            }
             const int tgt = f.targets[f.ti];
             f.picked.clear();
             reach_walk(caps, L, items, n, ck, tgt, f.picked);
