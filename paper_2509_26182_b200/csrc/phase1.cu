@@ -285,11 +285,6 @@ struct Mask {   // subset of range(m), m <= 256
     __device__ int count() const { return __popcll(w[0]) + __popcll(w[1]) + __popcll(w[2]) + __popcll(w[3]); }
 };
 
-struct Bits {
-    uint64_t w[BWORDS];
-};
-
-__device__ __forceinline__ bool bits_test(const Bits& b, int i) { return (b.w[i >> 6] >> (i & 63)) & 1ull; }
 
 struct Frame {          // one peel() activation
     Mask picked;
@@ -307,14 +302,6 @@ __device__ void range_mask(int m, Mask& pool) {
     }
 }
 
-__device__ int pool_items(const Mask& pool, int m, uint16_t* items) {
-    int n = 0;                                               // set bits in ascending order
-#pragma unroll
-    for (int w = 0; w < 4; ++w)
-        for (uint64_t x = pool.w[w]; x; x &= x - 1) items[n++] = (uint16_t)(w * 64 + __ffsll((long long)x) - 1);
-    (void)m;
-    return n;
-}
 
 // Subset-sum reach rows reach[p + 1] = reach[p] | ((reach[p] << v_p) & (2^(2L) - 1)), up to 256 bits.  The rows
 // live in the thread's local memory and only their ceil(2L / 64) live words are stored and read back (2 of 4 at
@@ -363,36 +350,46 @@ __device__ __forceinline__ bool reach_load_test(const Reach4& src, int i) {
     return (x >> (i & 63)) & 1ull;
 }
 
-// forward pass: rows[p] = reach[p] for p <= n (live words only), returns reach[n]
-__device__ Reach4 compute_reach(const int* caps, int L, const uint16_t* items, int n, Reach4* rows) {
+// forward pass over the pool's items in ascending order (set bits of the mask): rows[p] = reach[p] for p <= n
+// (live words only); returns reach[n] and the item count
+__device__ Reach4 compute_reach(const int* caps, int L, const Mask& pool, Reach4* rows, int& n_out) {
     static_assert(BWORDS == 4, "reach rows are 4 words");
     uint64_t lim[4];
     reach_limits(L, lim);
     const int nw = (2 * L + 63) >> 6;
     Reach4 r{1ull, 0ull, 0ull, 0ull};
     reach_store(rows[0], r, nw);
-    for (int p = 0; p < n; ++p) {
-        reach_step(r, cval(caps, items[p], L), lim);
-        reach_store(rows[p + 1], r, nw);
-    }
+    int p = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+        for (uint64_t x = pool.w[w]; x; x &= x - 1) {
+            reach_step(r, cval(caps, w * 64 + __ffsll((long long)x) - 1, L), lim);
+            reach_store(rows[++p], r, nw);
+        }
+    n_out = p;
     return r;
 }
 
-// the try's backward walk (allocator.py:401-409): from the last item down, an item is picked unless the reach row
-// before it already holds the remaining target
-__device__ void reach_walk(const int* caps, int L, const uint16_t* items, int n, const Reach4* rows, int tgt,
+// the try's backward walk (allocator.py:401-409): from the last item down (set bits in descending order), an item
+// is picked unless the reach row before it already holds the remaining target
+__device__ void reach_walk(const int* caps, int L, const Mask& pool, int n, const Reach4* rows, int tgt,
                            Mask& picked) {
-    int rem = tgt;
-    for (int pos = n - 1; pos >= 0; --pos) {
-        if (reach_load_test(rows[pos], rem)) continue;
-        picked.set(items[pos]);
-        rem -= cval(caps, items[pos], L);
-    }
+    int rem = tgt, pos = n - 1;
+#pragma unroll
+    for (int w = 3; w >= 0; --w)
+        for (uint64_t x = pool.w[w]; x; --pos) {
+            const int b = 63 - __clzll((long long)x);
+            x &= ~(1ull << b);
+            if (reach_load_test(rows[pos], rem)) continue;
+            const int i = w * 64 + b;
+            picked.set(i);
+            rem -= cval(caps, i, L);
+        }
 }
 
 // returns true on success; the k groups are then fr[0..k-1].picked, in peel order
 // cancel (optional): the parallel-m search's best success so far; an attempt at a larger m gives up
-__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck, uint16_t* items,
+__device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck,
                      const volatile int32_t* cancel = nullptr) {
     int budget = m <= 24 ? 300 : 80;
     int d = 0;
@@ -426,8 +423,8 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
                 state = RET;
                 continue;
             }
-            const int n = pool_items(pool, m, items);
-            const Reach4 last = compute_reach(caps, L, items, n, ck);
+            int n = 0;
+            const Reach4 last = compute_reach(caps, L, pool, ck, n);
             reach_owner = d;
             owner_n = n;
             f.nt = 0;
@@ -440,17 +437,16 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
         if (state == TRY) {
             Frame& f = fr[d];
             if (f.ti >= f.nt) { ok = false; state = RET; continue; }
-            // items[] and the reach rows still hold this frame's unless a deeper frame overwrote them
+            // the reach rows (and item count) still hold this frame's unless a deeper frame overwrote them
             int n = owner_n;
             if (reach_owner != d) {
-                n = pool_items(f.avail, m, items);
-                compute_reach(caps, L, items, n, ck);
+                compute_reach(caps, L, f.avail, ck, n);
                 reach_owner = d;
                 owner_n = n;
             }
             const int tgt = f.targets[f.ti];
             f.picked.clear();
-            reach_walk(caps, L, items, n, ck, tgt, f.picked);
+            reach_walk(caps, L, f.avail, n, ck, tgt, f.picked);
             Frame& c = fr[d + 1];
             c.total = f.total - tgt;
             c.need = f.need - 1;
@@ -875,7 +871,7 @@ __device__ bool cover_setup(const ss_pool_set& P, const int64_t* koff, int p, in
 }
 
 // One attempt at group count m: best-fit, then peel.  On success writes the groups when mout != nullptr.
-__device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr, Reach4* reach, uint16_t* items,
+__device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr, Reach4* reach,
                           int* mout, int* gout, int32_t* stage_out, const volatile int32_t* cancel = nullptr) {
     if (best_fit(cc.caps, m, k, cc.L, G, cancel)) {
         if (mout) {
@@ -889,7 +885,7 @@ __device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr
         }
         return true;
     }
-    if (peel(cc.caps, m, k, cc.L, fr, reach, items, cancel)) {
+    if (peel(cc.caps, m, k, cc.L, fr, reach, cancel)) {
         if (mout) {
             int pos = 0, stg = 0;
             for (int g = 0; g < k; ++g) {
@@ -921,11 +917,10 @@ __global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages
     Lists G;
     Frame fr[KMAX + 2];
     Reach4 reach[NMAX + 1];
-    uint16_t items[NMAX];
     int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
     int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
     for (int m = cc.m0; m <= cc.n; ++m)
-        if (cover_try(cc, k, m, G, fr, reach, items, mout, gout, stages + cc.ko)) return;
+        if (cover_try(cc, k, m, G, fr, reach, mout, gout, stages + cc.ko)) return;
     stall[cc.ko] = 1;                                            // constructive grouping stalled
 }
 
@@ -947,8 +942,7 @@ __global__ void cover_try_kernel(ss_pool_set P, const int64_t* koff, const int32
     Lists G;
     Frame fr[KMAX + 2];
     Reach4 reach[NMAX + 1];
-    uint16_t items[NMAX];
-    if (cover_try(cc, k, m, G, fr, reach, items, nullptr, nullptr, nullptr, best_m + c)) atomicMin(&best_m[c], m);
+    if (cover_try(cc, k, m, G, fr, reach, nullptr, nullptr, nullptr, best_m + c)) atomicMin(&best_m[c], m);
 }
 
 // small batches: rebuild the groups at the smallest successful m (or record the stall)
@@ -969,10 +963,9 @@ __global__ void cover_finish_kernel(ss_pool_set P, const int64_t* koff, int32_t*
     Lists G;
     Frame fr[KMAX + 2];
     Reach4 reach[NMAX + 1];
-    uint16_t items[NMAX];
     int* mout = members + P.memb_off[p] + (int64_t)(k - 1) * cc.n_all;
     int* gout = gsize + P.gsz_off[p] + (int64_t)(k - 1) * cc.kmax;
-    if (!cover_try(cc, k, m, G, fr, reach, items, mout, gout, stages + cc.ko)) stall[cc.ko] = 1;
+    if (!cover_try(cc, k, m, G, fr, reach, mout, gout, stages + cc.ko)) stall[cc.ko] = 1;
 }
 
 // per pool: apply "first stalled / infeasible k drops every larger k"; validate order
