@@ -31,6 +31,15 @@
 
 namespace {
 
+#ifndef RG_UNROLL
+#define RG_UNROLL 8                      // source pairs per unrolled step of the intra-tile relaxation
+#endif
+#ifndef RG_KB
+#define RG_KB 4                          // kept cross-tile sources per round
+#endif
+
+constexpr int RG_UNROLL_N = RG_UNROLL;
+
 constexpr int RG_HDR = 16;
 constexpr int RG_MAX_TILES = 8;
 constexpr int RG_BAR_ALL = 3;          // consumers + producer
@@ -548,7 +557,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             double v = INF, v1 = INF;
             int ix = 0x7fff, ix1 = 0x7fff;
             const char* Tb = reinterpret_cast<const char*>(Tw + lane);
-#pragma unroll 4
+#pragma unroll RG_UNROLL_N
             for (int k = 0; k < n; k += 2) {
                 const double2 c01 = *reinterpret_cast<const double2*>(cw + k);
                 const int2 r2 = *reinterpret_cast<const int2*>(rw + k);
@@ -594,7 +603,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                 // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
                 // from the shared-memory table, four sources per round
                 while (keep) {
-                    constexpr int KB = 4;
+                    constexpr int KB = RG_KB;
                     int kk[KB], gs[KB];
                     double e[KB];
 #pragma unroll
