@@ -34,6 +34,9 @@ namespace {
 #ifndef RG_UNROLL
 #define RG_UNROLL 8                      // source pairs per unrolled step of the intra-tile relaxation
 #endif
+#ifndef RG_MINB_WIDE
+#define RG_MINB_WIDE 3                   // CTAs per SM the register budget is sized for (5..8 tiles)
+#endif
 #ifndef RG_KB
 #define RG_KB 4                          // kept cross-tile sources per round
 #endif
@@ -278,7 +281,7 @@ __device__ __forceinline__ int rg_ld_pair(const uint16_t* p) {
 //              reused one boundary late, so nothing relaxed at b-1 is overwritten);
 //   consumers, after it : relax boundary b inside the tile, then the cross-tile blocks the bound test keeps.
 template <int NTL>
-__global__ void __launch_bounds__((NTL + 1) * 32, NTL <= 4 ? 4 : 2)
+__global__ void __launch_bounds__((NTL + 1) * 32, NTL <= 4 ? 4 : RG_MINB_WIDE)
 replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     extern __shared__ __align__(128) unsigned char smem[];
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
