@@ -310,17 +310,23 @@ __device__ void range_mask(int m, Mask& pool) {
 // kept.
 struct Reach4 { uint64_t r0, r1, r2, r3; };
 
+// NW = ceil(2L / 64) live words (templated: the dead words' shifts drop out)
+template <int NW>
 __device__ __forceinline__ void reach_step(Reach4& r, int s, const uint64_t* lim) {
     const int ws = s >> 6, bs = s & 63;
     const uint64_t w0 = ws == 0 ? r.r0 : 0ull;
     const uint64_t w1 = ws == 0 ? r.r1 : (ws == 1 ? r.r0 : 0ull);
-    const uint64_t w2 = ws == 0 ? r.r2 : (ws == 1 ? r.r1 : (ws == 2 ? r.r0 : 0ull));
-    const uint64_t w3 = ws == 0 ? r.r3 : (ws == 1 ? r.r2 : (ws == 2 ? r.r1 : (ws == 3 ? r.r0 : 0ull)));
     // (lo >> 1) >> (63 - bs) == lo >> (64 - bs) for bs >= 1 and 0 for bs == 0 (no 64-bit shift by 64)
+    if constexpr (NW > 2) {
+        const uint64_t w2 = ws == 0 ? r.r2 : (ws == 1 ? r.r1 : (ws == 2 ? r.r0 : 0ull));
+        if constexpr (NW > 3) {
+            const uint64_t w3 = ws == 0 ? r.r3 : (ws == 1 ? r.r2 : (ws == 2 ? r.r1 : (ws == 3 ? r.r0 : 0ull)));
+            r.r3 |= ((w3 << bs) | ((w2 >> 1) >> (63 - bs))) & lim[3];
+        }
+        r.r2 |= ((w2 << bs) | ((w1 >> 1) >> (63 - bs))) & lim[2];
+    }
+    if constexpr (NW > 1) r.r1 |= ((w1 << bs) | ((w0 >> 1) >> (63 - bs))) & lim[1];
     r.r0 |= (w0 << bs) & lim[0];
-    r.r1 |= ((w1 << bs) | ((w0 >> 1) >> (63 - bs))) & lim[1];
-    r.r2 |= ((w2 << bs) | ((w1 >> 1) >> (63 - bs))) & lim[2];
-    r.r3 |= ((w3 << bs) | ((w2 >> 1) >> (63 - bs))) & lim[3];
 }
 
 __device__ __forceinline__ void reach_limits(int L, uint64_t* lim) {
@@ -338,11 +344,12 @@ __device__ __forceinline__ bool reach_test(const Reach4& r, int i) {
     return (x >> (i & 63)) & 1ull;
 }
 
-__device__ __forceinline__ void reach_store(Reach4& dst, const Reach4& r, int nw) {
+template <int NW>
+__device__ __forceinline__ void reach_store(Reach4& dst, const Reach4& r) {
     dst.r0 = r.r0;
-    dst.r1 = r.r1;
-    if (nw > 2) dst.r2 = r.r2;
-    if (nw > 3) dst.r3 = r.r3;
+    if constexpr (NW > 1) dst.r1 = r.r1;
+    if constexpr (NW > 2) dst.r2 = r.r2;
+    if constexpr (NW > 3) dst.r3 = r.r3;
 }
 
 __device__ __forceinline__ bool reach_load_test(const Reach4& src, int i) {
@@ -352,19 +359,19 @@ __device__ __forceinline__ bool reach_load_test(const Reach4& src, int i) {
 
 // forward pass over the pool's items in ascending order (set bits of the mask): rows[p] = reach[p] for p <= n
 // (live words only); returns reach[n] and the item count
+template <int NW>
 __device__ Reach4 compute_reach(const int* caps, int L, const Mask& pool, Reach4* rows, int& n_out) {
     static_assert(BWORDS == 4, "reach rows are 4 words");
     uint64_t lim[4];
     reach_limits(L, lim);
-    const int nw = (2 * L + 63) >> 6;
     Reach4 r{1ull, 0ull, 0ull, 0ull};
-    reach_store(rows[0], r, nw);
+    reach_store<NW>(rows[0], r);
     int p = 0;
 #pragma unroll
     for (int w = 0; w < 4; ++w)
         for (uint64_t x = pool.w[w]; x; x &= x - 1) {
-            reach_step(r, cval(caps, w * 64 + __ffsll((long long)x) - 1, L), lim);
-            reach_store(rows[++p], r, nw);
+            reach_step<NW>(r, cval(caps, w * 64 + __ffsll((long long)x) - 1, L), lim);
+            reach_store<NW>(rows[++p], r);
         }
     n_out = p;
     return r;
@@ -389,6 +396,7 @@ __device__ void reach_walk(const int* caps, int L, const Mask& pool, int n, cons
 
 // returns true on success; the k groups are then fr[0..k-1].picked, in peel order
 // cancel (optional): the parallel-m search's best success so far; an attempt at a larger m gives up
+template <int NW>
 __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck,
                      const volatile int32_t* cancel = nullptr) {
     int budget = m <= 24 ? 300 : 80;
@@ -424,7 +432,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
                 continue;
             }
             int n = 0;
-            const Reach4 last = compute_reach(caps, L, pool, ck, n);
+            const Reach4 last = compute_reach<NW>(caps, L, pool, ck, n);
             reach_owner = d;
             owner_n = n;
             f.nt = 0;
@@ -440,7 +448,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
             // the reach rows (and item count) still hold this frame's unless a deeper frame overwrote them
             int n = owner_n;
             if (reach_owner != d) {
-                compute_reach(caps, L, f.avail, ck, n);
+                compute_reach<NW>(caps, L, f.avail, ck, n);
                 reach_owner = d;
                 owner_n = n;
             }
@@ -885,7 +893,12 @@ __device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr
         }
         return true;
     }
-    if (peel(cc.caps, m, k, cc.L, fr, reach, cancel)) {
+    const int nw = (2 * cc.L + 63) >> 6;                     // live reach words (L <= 128)
+    const bool peeled = nw <= 1 ? peel<1>(cc.caps, m, k, cc.L, fr, reach, cancel)
+                      : nw == 2 ? peel<2>(cc.caps, m, k, cc.L, fr, reach, cancel)
+                      : nw == 3 ? peel<3>(cc.caps, m, k, cc.L, fr, reach, cancel)
+                                : peel<4>(cc.caps, m, k, cc.L, fr, reach, cancel);
+    if (peeled) {
         if (mout) {
             int pos = 0, stg = 0;
             for (int g = 0; g < k; ++g) {
