@@ -378,7 +378,9 @@ __device__ Reach4 compute_reach(const int* caps, int L, const Mask& pool, Reach4
 }
 
 // the try's backward walk (allocator.py:401-409): from the last item down (set bits in descending order), an item
-// is picked unless the reach row before it already holds the remaining target
+// is picked unless the reach row before it already holds the remaining target.  (Loading four positions' rows
+// ahead of their tests measured slower: 143 registers per thread.)
+template <int NW>
 __device__ void reach_walk(const int* caps, int L, const Mask& pool, int n, const Reach4* rows, int tgt,
                            Mask& picked) {
     int rem = tgt, pos = n - 1;
@@ -436,8 +438,18 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
             reach_owner = d;
             owner_n = n;
             f.nt = 0;
-            for (int t = L; t < 2 * L && f.nt < 4; ++t)
-                if (reach_test(last, t)) f.targets[f.nt++] = (short)t;
+            // the first (up to) four reachable totals in [L, 2L): set bits of reach[n] from bit L up
+            {
+                const uint64_t words[4] = {last.r0, last.r1, last.r2, last.r3};
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    const int lo = w * 64;
+                    if (lo + 64 <= L || f.nt >= 4) continue;
+                    uint64_t x = words[w];
+                    if (L > lo) x &= ~0ull << (L - lo);          // bits >= L (the reach limits clear >= 2L)
+                    for (; x && f.nt < 4; x &= x - 1) f.targets[f.nt++] = (short)(lo + __ffsll((long long)x) - 1);
+                }
+            }
             f.ti = 0;
             state = TRY;
             continue;
@@ -454,7 +466,7 @@ __device__ bool peel(const int* caps, int m, int k, int L, Frame* fr, Reach4* ck
             }
             const int tgt = f.targets[f.ti];
             f.picked.clear();
-            reach_walk(caps, L, f.avail, n, ck, tgt, f.picked);
+            reach_walk<NW>(caps, L, f.avail, n, ck, tgt, f.picked);
             Frame& c = fr[d + 1];
             c.total = f.total - tgt;
             c.need = f.need - 1;

@@ -1,6 +1,6 @@
 """Ad-hoc ncu targets (not a test): one launch of a chosen kernel family at its bench shape.
 
-    ncu --set full -k regex:<kernel> -c 1 python tests/ncu_targets.py <admission|sim|exact|cover|warp|slots|blocks|c5>
+    ncu --set full -k regex:<kernel> -c 1 python tests/ncu_targets.py <admission|sim|exact|cover|cover64|warp|slots|blocks|c5>
 
 ``slots`` / ``blocks``: bench.py's own headline launch (C4 pool, 1,184 device-churned scenarios, 64 requests, W=64),
 launched twice -- profile the second (``-s 1 -c 1``), whose requests 64..127 run the steady state.
@@ -51,8 +51,8 @@ def main(what):
     elif what == "exact":
         packed, _ = scen.bench_variants(256, 64, 64, seed0=0)      # C2-shaped pools: 16 GPUs per region
         VariantSweep(packed, fill_all=True).run()
-    elif what == "cover":
-        packed, _ = scen.bench_variants(1812, 256, 80, seed0=0)
+    elif what in ("cover", "cover64"):
+        packed, _ = scen.bench_variants(1812, 256, 80 if what == "cover" else 64, seed0=0)
         VariantSweep(packed, fill_all=True).run()
     torch.cuda.synchronize()
 
