@@ -33,9 +33,18 @@ static __device__ const float ss_jitter_q[1024] = {
 #include "jitter_lognormal.inc"
 };
 
+// quantile index of the unordered pair (i, j) under seed_mix = splitmix64(scenario seed): the pair folded into 32 bits
+// with two odd multipliers and the seed, then the lowbias32 finaliser (xorshift-multiply); top 10 bits.  Cheap
+// enough to run per entry in the region replay's kept cross-region blocks.
 __device__ __forceinline__ uint32_t ss_jitter_index(uint64_t seed_mix, uint32_t i, uint32_t j) {
     if (i > j) { uint32_t t = i; i = j; j = t; }
-    return (uint32_t)(ss_splitmix64(seed_mix ^ ((uint64_t(i) << 32) | uint64_t(j))) & 1023u);
+    uint32_t x = i * 0x9E3779B1u + j * 0x85EBCA77u + ((uint32_t)seed_mix ^ (uint32_t)(seed_mix >> 32));
+    x ^= x >> 16;
+    x *= 0x7FEB352Du;
+    x ^= x >> 15;
+    x *= 0x846CA68Bu;
+    x ^= x >> 16;
+    return x >> 22;
 }
 
 __device__ __forceinline__ double ss_jitter(uint64_t seed_mix, uint32_t i, uint32_t j) {

@@ -7,11 +7,11 @@
 * Scenario states (C4/C5) are the base pool after churn (a seeded set of plan
   GPUs leaves, as ``MembershipManager.on_leave`` would, no rebalance) and with
   a seeded per-pair RTT jitter: one LogNormal(0, 0.2) factor per unordered GPU
-  pair, quantile ``h & 1023`` of the 1024-point float32 grid
-  in ``csrc/jitter_lognormal.inc`` with h the pair's splitmix64 hash.  Kernels and
+  pair, quantile ``jitter_index(seed, i, j)`` (a 32-bit pair
+  hash, top 10 bits) of the 1024-point float32 grid in ``csrc/jitter_lognormal.inc``.  Kernels and
   host read the same committed table, so the device generators
   (``ss_scenario_rtt``, the edge / unit writers) and the host/oracle produce
-  bit-identical RTTs: ``rtt_ab * Q[h & 1023]``.
+  bit-identical RTTs: ``rtt_ab * Q[jitter_index(seed, a, b)]``.
 """
 
 from __future__ import annotations
@@ -120,11 +120,6 @@ def splitmix64(x: int) -> int:
     return x ^ (x >> 31)
 
 
-def pair_hash(seed: int, i: int, j: int) -> int:
-    """Hash of an unordered GPU pair (i < j) under a scenario seed."""
-    return splitmix64((splitmix64(seed & MASK64) ^ ((i << 32) | j)) & MASK64)
-
-
 def _jitter_table() -> np.ndarray:
     """The 1024 LogNormal(0, 0.2) float32 quantiles of csrc/jitter_lognormal.inc (the kernels include the same file)."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "jitter_lognormal.inc")
@@ -139,24 +134,38 @@ def _jitter_table() -> np.ndarray:
 JITTER_Q = _jitter_table()
 
 
-def jitter_factor(seed: int, i: int, j: int) -> float:
-    """One LogNormal(0, 0.2) factor per unordered GPU pair: quantile h & 1023 of JITTER_Q."""
+def jitter_index(seed: int, i: int, j: int) -> int:
+    """Quantile index of the unordered pair (i, j): ss_jitter_index (ss_common.cuh) in Python integers."""
     if i > j:
         i, j = j, i
-    return float(JITTER_Q[pair_hash(seed, i, j) & 1023])
+    mix = splitmix64(seed & MASK64)
+    x = (i * 0x9E3779B1 + j * 0x85EBCA77 + ((mix ^ (mix >> 32)) & 0xFFFFFFFF)) & 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x7FEB352D) & 0xFFFFFFFF
+    x ^= x >> 15
+    x = (x * 0x846CA68B) & 0xFFFFFFFF
+    x ^= x >> 16
+    return x >> 22
+
+
+def jitter_factor(seed: int, i: int, j: int) -> float:
+    """One LogNormal(0, 0.2) factor per unordered GPU pair: quantile jitter_index of JITTER_Q."""
+    return float(JITTER_Q[jitter_index(seed, i, j)])
 
 
 def jitter_factor_matrix(seed: int, n: int) -> np.ndarray:
-    """Vectorised jitter_factor over all pairs (diagonal 1.0) -- numpy uint64 arithmetic."""
+    """Vectorised jitter_factor over all pairs (diagonal 1.0) -- numpy uint32 arithmetic."""
     i, j = np.triu_indices(n, 1)
-    s = np.uint64(splitmix64(seed & MASK64))
+    mix = splitmix64(seed & MASK64)
+    h0 = np.uint32((mix ^ (mix >> 32)) & 0xFFFFFFFF)
     with np.errstate(over="ignore"):
-        x = s ^ ((i.astype(np.uint64) << np.uint64(32)) | j.astype(np.uint64))
-        x = x + np.uint64(0x9E3779B97F4A7C15)
-        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        x = x ^ (x >> np.uint64(31))
-    f = JITTER_Q[(x & np.uint64(1023)).astype(np.int64)]
+        x = i.astype(np.uint32) * np.uint32(0x9E3779B1) + j.astype(np.uint32) * np.uint32(0x85EBCA77) + h0
+        x ^= x >> np.uint32(16)
+        x *= np.uint32(0x7FEB352D)
+        x ^= x >> np.uint32(15)
+        x *= np.uint32(0x846CA68B)
+        x ^= x >> np.uint32(16)
+    f = JITTER_Q[(x >> np.uint32(22)).astype(np.int64)]
     out = np.ones((n, n))
     out[i, j] = f
     out[j, i] = f
