@@ -270,7 +270,8 @@ def run_ours(args):
                       "launch time, so frac is NOT a DRAM fraction: the kernel keeps one RTT tile per region in shared "
                       "memory (%.0f KB per selection of entering GPUs' rows / columns cross L2/HBM) and relaxes only "
                       "the intra-region pairs (%.0f of the %.0f dense pairs per selection) plus the cross-region "
-                      "blocks an exact bound test cannot exclude (~1%% at C4); results are bit-identical to the dense "
+                      "blocks an exact bound test cannot exclude (~5%% of them in the C4 steady state with the LogNormal "
+                      "jitter); results are bit-identical to the dense "
                       "DP. It is bound by instruction issue and boundary-barrier latency (ncu block below; DESIGN.md)"
                       % (stream_b / 1e3, relaxed["intra_region_pairs"], relaxed["dense_pairs"]))
     elif args.mode == "slots":
@@ -379,7 +380,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C4: L=64 model over a 256-GPU heterogeneous pool (k=%d replicas), %d "
-                                   "churn+jitter scenario states per GPU x %d requests per step, W=%d "
+                                   "churn + LogNormal(0, 0.2) pair-jitter scenario states per GPU x %d requests per step, W=%d "
                                    "route/release window, on-device load update" % (plan.replication_count, S, R, W),
                        "scenarios_per_gpu": S, "requests_per_step": R, "window": W, "layers": 64, "pool_gpus": 256,
                        "replicas": plan.replication_count, "parallelism": f"scenario-sharded x{world}",
