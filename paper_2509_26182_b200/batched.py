@@ -150,12 +150,21 @@ class RegionTiles:
         else:
             lo, hi = scen.slice_lo[None, :].astype(np.int64), scen.slice_hi[None, :].astype(np.int64)
             ok = (lo <= hi) & (hi >= 1)
-        b = np.arange(max(L - 1, 1))
+        # per (scenario, tile) a difference array over the boundaries -> running counts -> the peak per tile
+        nb = max(L - 1, 1)
+        start = np.maximum(lo - 2, 0)
+        end = np.minimum(hi, nb - 1)
+        valid = ok & (start <= end)
+        si, gi = np.nonzero(valid)
         held = np.zeros(T, dtype=np.int64)
-        for t in range(T):
-            m = ok & (self.tile_of[None, :] == t)
-            inb = (np.maximum(lo - 2, 0)[:, :, None] <= b) & (hi[:, :, None] >= b) & m[:, :, None]
-            held[t] = int(inb.sum(axis=1).max()) if inb.size else 0
+        if si.size:
+            n_rows = valid.shape[0]
+            row = si * T + self.tile_of[gi]
+            width = nb + 1
+            delta = (np.bincount(row * width + start[si, gi], minlength=n_rows * T * width)
+                     - np.bincount(row * width + end[si, gi] + 1, minlength=n_rows * T * width))
+            counts = np.cumsum(delta.reshape(n_rows, T, width), axis=2)[:, :, :nb]
+            held = counts.max(axis=(0, 2)).astype(np.int64)
         self.held = held + scen.joins
 
     def fits(self) -> bool:
@@ -165,7 +174,14 @@ class RegionTiles:
 def region_tiles(scen: ScenarioSet) -> Optional[RegionTiles]:
     if getattr(scen, "region_idx", None) is None or scen.layer_count < 2:
         return None
-    return RegionTiles(scen)
+    cached = getattr(scen, "_region_tiles", None)             # a ScenarioSet is not mutated after it is built
+    if cached is None:
+        cached = RegionTiles(scen)
+        try:
+            scen._region_tiles = cached
+        except AttributeError:
+            pass
+    return cached
 
 
 def replay_mode(scen: ScenarioSet, *, window: int = 64, max_requests: Optional[int] = None,
