@@ -58,13 +58,16 @@ int g_rg_nbuf = 3;
 //   ins   : per entering GPU {tile * 32 + local slot, gpu}
 //   pairs : per tile, per column, 32 entries {local slot | position << 8} of the tile's hosts in position
 //           (sorted-id) order, 0xffff past the last -- read by the consumers straight from L1/L2
+//   lbg   : per pool GPU g and tile t, a float rounded down <= every jittered g -> h entry with h in tile t, h != g
+//           (the per-source bound of the cross-tile filter; staged in shared memory)
 // The first three parts (up to off_pairs) are staged in shared memory by the replay kernel.
 struct RgLayout {
     int n_blk, n_tiles, pos_cap, n_cap;
     __host__ __device__ int off_blk() const { return RG_HDR; }
     __host__ __device__ int off_ins() const { return RG_HDR + n_blk * 8; }
     __host__ __device__ int off_pairs() const { return (off_ins() + n_cap * 4 + 127) / 128 * 128; }
-    __host__ __device__ int bytes() const { return off_pairs() + n_tiles * (n_blk + 1) * 64; }
+    __host__ __device__ int off_lbg() const { return (off_pairs() + n_tiles * (n_blk + 1) * 64 + 15) / 16 * 16; }
+    __host__ __device__ int bytes() const { return (off_lbg() + n_cap * n_tiles * 4 + 127) / 128 * 128; }
 };
 
 constexpr uint16_t RG_PAIR_NONE = 0xffff;
@@ -226,6 +229,19 @@ __global__ void region_program_kernel(int32_t layers, int32_t n_gpus, const int3
             st[(int64_t)(m.unit_start + u) * wp + t] = v;
         }
     }
+    // per-source cross-tile bounds: min over the pool GPUs h of tile t of the jittered g -> h entry, rounded down
+    float* lbg = reinterpret_cast<float*>(mt + ml.off_lbg());
+    for (int e = tid; e < n_gpus * n_tiles; e += blockDim.x) {
+        const int g = e / n_tiles, t = e - g * n_tiles;
+        double lo_v = __longlong_as_double(0x7ff0000000000000ll);
+        for (int h = 0; h < n_gpus; ++h) {
+            if (h == g || tile_of[h] != t) continue;
+            double v = rtt[(int64_t)g * dim + h];
+            if (jit) v = v * ss_jitter(mix, (uint32_t)g, (uint32_t)h);
+            lo_v = v < lo_v ? v : lo_v;
+        }
+        lbg[e] = __double2float_rd(lo_v);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -242,7 +258,8 @@ struct RgArgs {
     int pos_cap, rt, tp, nbuf, stage_bytes;
     int off_T, off_stage, off_bar, off_meta, meta_smem, off_cw, off_rw, off_cmin, off_bp, off_picks, off_tau,
         off_occ, off_stamp, off_slotgpu, off_cl, off_coff, off_red, off_misc, off_pow, pow_len, off_rel, off_seg,
-        off_bnd, off_jq, off_pg, total;
+        off_bnd, off_jq, off_pg, off_lbg, total;
+    int use_lbg;                 // 1: per-source cross-tile bounds staged in shared memory (off_lbg)
     unsigned long long* cross;   // diagnostics (env SS_REGION_STATS=1): [0] blocks tested [1] blocks relaxed
 };
 
@@ -323,6 +340,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     const double* uni_s = ub_s + NTL;                                         // [NTL][NTL] uniform S->D entry or NaN
     float* jq_s = reinterpret_cast<float*>(smem + A.off_jq);                  // [1024] jitter quantiles
     int* pg_all = reinterpret_cast<int*>(smem + A.off_pg);                    // [2][NTL][32] source gpu | pos << 16
+    float* lbg_s = reinterpret_cast<float*>(smem + A.off_lbg);                // [n_gpus][NTL] per-source bounds
 
     // ---- setup ---------------------------------------------------------------
     const uint8_t* meta_g = A.meta + (int64_t)dag * A.meta_stride;
@@ -344,6 +362,9 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
         for (int o = tid; o < A.pow_len; o += NT) pow_s[o] = R.occpow[o];
         for (int q = tid; q < 2 * NTL * NTL + NTL; q += NT) lb_s[q] = A.bounds[q];
         for (int q = tid; q < NTL * 32; q += NT) slot_gpu[q] = 0;
+        const float* lbg_g = reinterpret_cast<const float*>(meta_g + ml.off_lbg());
+        if (A.use_lbg)
+            for (int q = tid; q < D.max_gpus * NTL; q += NT) lbg_s[q] = lbg_g[q];
         if (A.jitter_seed)
             for (int q = tid; q < 1024; q += NT) jq_s[q] = ss_jitter_q[q];
     }
@@ -597,10 +618,12 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                 const bool uniform = uS == uS;
                 const double* cwS = cw_all + (boff + S) * 32;
                 // sources of S: lanes whose cost is finite (lanes >= the column length publish +inf)
-                unsigned keep = __ballot_sync(0xffffffffu, cwS[lane] < INF && !(__dadd_rn(cwS[lane], lbS) > vmax));
-                if (A.cross) { n_cross += keep != 0; n_src += __popc(keep); }
                 const int pgl = pg_all[(boff + S) * 32 + lane];          // lane k: source k's GPU and position
                 const int gsl = pgl & 0xffff;
+                // source k can only reach a destination of this tile if c_k + (its own bound to the tile) <= vmax
+                const double lbk = (A.use_lbg && cwS[lane] < INF) ? (double)lbg_s[gsl * NTL + w] : lbS;
+                unsigned keep = __ballot_sync(0xffffffffu, cwS[lane] < INF && !(__dadd_rn(cwS[lane], lbk) > vmax));
+                if (A.cross) { n_cross += keep != 0; n_src += __popc(keep); }
                 const int psl = pgl >> 16;
                 const int gd = sg_w[lane];
                 // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
@@ -823,6 +846,8 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     A.off_seg = o;     o += rg_align(n_tiles * pos_cap, 16) + rg_align(n_tiles * 4, 16);
     A.off_pg = o;      o += 2 * n_tiles * 32 * 4;
     A.off_jq = o;      o += jitter_seed ? 1024 * 4 : 0;
+    A.off_lbg = o;     o += rg_align(D.max_gpus * n_tiles * 4, 16);   // last: dropped when it costs occupancy
+    A.use_lbg = 1;
     A.total = o;
     if (A.total > 227 * 1024) return SS_BAD_INPUT;
     RgReplayArgs R{};
@@ -838,9 +863,19 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     if (stats && cudaMalloc(&A.cross, 3 * sizeof(unsigned long long)) == cudaSuccess)
         cudaMemsetAsync(A.cross, 0, 3 * sizeof(unsigned long long), s);
     auto run = [&](auto kern) -> int {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, A.total) != cudaSuccess)
+        const int threads = (n_tiles + 1) * 32;
+        // the per-source bound table rides in shared memory only when it costs no CTA per SM
+        const int with_lbg = A.total, without_lbg = A.off_lbg;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, with_lbg) != cudaSuccess)
             return SS_CUDA_ERROR;
-        kern<<<D.n_dags, (n_tiles + 1) * 32, A.total, s>>>(D, A, R);
+        int b_with = 0, b_without = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_with, kern, threads, with_lbg) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_without, kern, threads, without_lbg) == cudaSuccess &&
+            b_with < b_without) {
+            A.use_lbg = 0;
+            A.total = without_lbg;
+        }
+        kern<<<D.n_dags, threads, A.total, s>>>(D, A, R);
         SS_CHECK_LAUNCH();
         return SS_OK;
     };
