@@ -16,6 +16,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import os
+
 import numpy as np
 
 from . import _native as N
@@ -132,7 +134,22 @@ class PoolBatch:
         all_k = _ramp(km)
         # one thread per candidate: order by (k, pool) so a warp's 32 candidates share k (and hence loop
         # trip counts) -- outputs are addressed by (pool, k), so the order is free
-        o = np.lexsort((cand_pool, cand_k))
+        order_mode = os.environ.get("SS_COVER_ORDER", "k")
+        if order_mode in ("m0", "km0") and cand_pool.size:
+            # group candidates by their first group count m0 = max(k * ceil(L / cap0), bisect(prefix, k * L))
+            # (cover_setup), then k: a warp's candidates start their m loops together
+            Lp = A.layers.astype(np.int64)[cand_pool]
+            cl = np.minimum(caps, np.repeat(A.layers.astype(np.int64), n))       # clamped caps, pool-major
+            pref = np.cumsum(cl)
+            base = np.concatenate([[0], pref])[pool_ptr[:-1]]
+            target = cand_k * Lp
+            m_cap = np.searchsorted(pref, base[cand_pool] + target, side="left") - pool_ptr[:-1][cand_pool] + 1
+            m_cap = np.minimum(m_cap, usable[cand_pool])
+            c0 = np.maximum(cl[pool_ptr[:-1][cand_pool]], 1)
+            m0 = np.maximum(cand_k * ((Lp + c0 - 1) // c0), m_cap)
+            o = np.lexsort((cand_pool, cand_k, m0)) if order_mode == "m0" else np.lexsort((cand_pool, m0, cand_k))
+        else:
+            o = np.lexsort((cand_pool, cand_k))
         cand_pool, cand_k = cand_pool[o], cand_k[o]
         o = np.lexsort((all_pool, all_k))
         all_pool, all_k = all_pool[o], all_k[o]
