@@ -876,6 +876,21 @@ def _roofline(mode, S, R, achieved, hbm, peak_src, kernel_name, note, stream_b, 
                       "dram_bytes_per_selection": nc["per_selection"]["dram_bytes"],
                       "l2_hit_pct": nc["l2_hit_pct"], "fp64_pipe_pct": nc["fp64_pipe_pct"],
                       "duration_ms_under_ncu": nc["duration_ms"]}
+        if out["bound"] == "issue":
+            # the bound that binds: one warp instruction per SM sub-partition per cycle.  Selections/s if every
+            # issue slot of the GPU issued this kernel's instruction mix, against the measured launch
+            import torch
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            clock = nc["sm_cycles"] / (nc["duration_ms"] * 1e-3)          # SM cycles per second under ncu
+            slots = sms * 4 * clock
+            at_full = slots / nc["per_selection"]["warp_instructions"]
+            got = S * R / launch_s
+            out["issue_roofline"] = {"issue_slots_per_s": slots, "sms": sms, "sm_clock_hz": clock,
+                                     "warp_instructions_per_selection": nc["per_selection"]["warp_instructions"],
+                                     "selections_per_s_at_full_issue": at_full, "achieved_selections_per_s": got,
+                                     "frac": got / at_full,
+                                     "note": "4 issue slots per SM per cycle (one per sub-partition); the "
+                                             "instruction count per selection is the ncu capture's"}
     return out
 
 
