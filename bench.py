@@ -22,6 +22,9 @@ allocations/sec at 1/2/4/8 B200"):
 * ``e2e``: the same Phase-2 metric through ``ScenarioReplayer.run_from_host``:
   pinned host scenario descriptors -> H2D -> device DAG build -> replay ->
   D2H of per-request costs and chain hashes, all inside the timed region.
+* ``c4_full`` / ``c5``: the whole configs[3] job (10,000 scenarios x 10,000 requests, sharded over the ranks)
+  and the whole configs[4] two-phase schedule (3 sub-pools x 4,096 scenarios x 4,096 requests), each timed on the
+  device as the max over ranks (``--no-full-jobs`` skips them).
 * ``cpu_baseline`` / ``--impl reference``: the reference's CPU path on this box's host cores -- the
   unmodified reference package installed into baseline/_ref (``oracle/bench_ref.py``), with the
   golden-pinned oracle port beside it (``cpu_baseline_port``).
@@ -70,9 +73,12 @@ def parse():
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--full-c5", action="store_true",
-                    help="run C5 as the whole configs[4] job: 4,096 requests per scenario (default: --c5-steps launches)")
+                    help="run C5 as the whole configs[4] job: 4,096 requests per scenario (on by default)")
     ap.add_argument("--full-c4", action="store_true",
-                    help="also run the whole configs[3] job: 10k scenarios x 10k requests, sharded over the ranks")
+                    help="also run the whole configs[3] job: 10k scenarios x 10k requests, sharded over the ranks "
+                         "(on by default)")
+    ap.add_argument("--no-full-jobs", action="store_true",
+                    help="skip the whole configs[3] / configs[4] jobs (C5 then runs --c5-steps launches)")
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-admission", action="store_true")
     ap.add_argument("--no-sim", action="store_true")
@@ -80,7 +86,11 @@ def parse():
     ap.add_argument("--cpu-sample-scenarios", type=int, default=64)
     ap.add_argument("--cpu-sample-requests", type=int, default=64)
     ap.add_argument("--cpu-sample-pools", type=int, default=400)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if not args.no_full_jobs:          # the whole configs[3] / configs[4] jobs are part of the default run
+        args.full_c4 = True
+        args.full_c5 = True
+    return args
 
 
 def dist_env():
