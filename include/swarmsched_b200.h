@@ -67,8 +67,8 @@ typedef struct ss_dag_set {
     const double*  edge_val;    /* row-major R_l x R_{l+1}: row = source host, col = destination */
 } ss_dag_set;
 
-/* Per-scenario RTT matrices on device: out[s] = base_rtt (n_gpus x n_gpus, row-major) times the exact dyadic
- * pair jitter of seed s (replaces scenarios.py ScenarioSet.scenario_rtt + an H2D copy of S x N x N doubles). */
+/* Per-scenario RTT matrices on device: out[s] = base_rtt (n_gpus x n_gpus, row-major) times the pair jitter of
+ * seed s (one IEEE product by a LogNormal(0, 0.2) quantile from a 1,024-entry float32 table) (replaces scenarios.py ScenarioSet.scenario_rtt + an H2D copy of S x N x N doubles). */
 int ss_scenario_rtt(int32_t n_scen, int32_t n_gpus, const double* base_rtt, const int64_t* seeds, double* out,
                     void* stream);
 /* Dense RTT matrices, one per item (router.py:118-143 rtt_matrix and

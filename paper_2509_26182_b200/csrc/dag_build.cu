@@ -7,7 +7,7 @@
 //
 // These are byte/index-movement kernels: coalesced stores, warp-ballot stream
 // compaction that preserves sorted-id order, no floating-point arithmetic
-// except the exact dyadic jitter multiply of the scenario generator.
+// except the scenario generator's jitter multiply (one IEEE product by a LogNormal(0, 0.2) quantile).
 #include "ss_common.cuh"
 
 namespace {
@@ -147,7 +147,7 @@ __global__ void dag_edges_kernel(ss_dag_set D, const int64_t* rtt_off, const int
 }
 
 // out[s][a][b] = base[a][b] * jitter(seed_s, a, b) (scenarios.py:ScenarioSet.scenario_rtt: the pool matrix times the
-// scenario's exact dyadic pair jitter, diagonal untouched)
+// scenario's pair jitter: one IEEE product by the pair's LogNormal(0, 0.2) quantile, diagonal untouched)
 __global__ void scenario_rtt_kernel(int32_t n_gpus, const double* base, const int64_t* seeds, double* out) {
     const int s = blockIdx.y;
     const uint64_t mix = ss_splitmix64((uint64_t)seeds[s]);
