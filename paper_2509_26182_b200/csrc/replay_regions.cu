@@ -258,7 +258,7 @@ struct RgArgs {
     int pos_cap, rt, tp, nbuf, stage_bytes;
     int off_T, off_stage, off_bar, off_meta, meta_smem, off_cw, off_rw, off_cmin, off_bp, off_picks, off_tau,
         off_occ, off_stamp, off_slotgpu, off_cl, off_coff, off_red, off_misc, off_pow, pow_len, off_rel, off_seg,
-        off_bnd, off_jq, off_pg, off_lbg, total;
+        off_bnd, off_jq, off_lbg, total;
     int use_lbg;                 // 1: per-source cross-tile bounds staged in shared memory (off_lbg)
     unsigned long long* cross;   // diagnostics (env SS_REGION_STATS=1): [0] blocks tested [1] blocks relaxed
 };
@@ -339,7 +339,6 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     double* ub_s = lb_s + NTL * NTL;                                          // [NTL]
     const double* uni_s = ub_s + NTL;                                         // [NTL][NTL] uniform S->D entry or NaN
     float* jq_s = reinterpret_cast<float*>(smem + A.off_jq);                  // [1024] jitter quantiles
-    int* pg_all = reinterpret_cast<int*>(smem + A.off_pg);                    // [2][NTL][32] source gpu | pos << 16
     float* lbg_s = reinterpret_cast<float*>(smem + A.off_lbg);                // [n_gpus][NTL] per-source bounds
 
     // ---- setup ---------------------------------------------------------------
@@ -539,11 +538,14 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
         // (local slot | position << 8) of source `lane` of the next two columns (L1 / L2 reads in flight)
         int pr_n1 = rg_ld_pair(pw_g);
         int pr_n2 = rg_ld_pair(pw_g + 32);
+        const uint16_t* pw_next = pw_g + 64;                 // pair list of column b + 2
+        uint8_t* bp_prev = bp - PC;                          // backpointers of boundary b - 1
         for (int b = 0; b < nblk; ++b) {
             // ---- column b of this tile: costs (+ backpointers of boundary b-1), published for boundary b ------
             const int pr = pr_n1;
             pr_n1 = pr_n2;
-            if (b + 2 <= nblk) pr_n2 = rg_ld_pair(pw_g + (b + 2) * 32);
+            if (b + 2 <= nblk) pr_n2 = rg_ld_pair(pw_next);
+            pw_next += 32;
             const bool src = pr != RG_PAIR_NONE;
             const int n = __popc(__ballot_sync(0xffffffffu, src));       // sources are lanes 0..n-1
             const int sl = pr & 31, pos = (pr >> 8) & 0xff;
@@ -553,15 +555,15 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             } else {
                 c = __shfl_sync(0xffffffffu, cost_lane, sl);
                 const int bpk = __shfl_sync(0xffffffffu, bpos_lane, sl);
-                if (src) bp[(b - 1) * PC + pos] = (uint8_t)bpk;
+                if (src) bp_prev[pos] = (uint8_t)bpk;
             }
+            bp_prev += PC;
             if (!src) c = INF;
             const int boff = (b & 1) * NTL;
             double* cw = cw0 + boff * 32;
             int* rw = rw0 + boff * 32;
             cw[lane] = c;                                        // lanes >= n: +inf, row 0 (pairs of sources)
             rw[lane] = sl * (TP * 8);
-            pg_all[boff * 32 + w * 32 + lane] = sg_w[sl] | (pos << 16);   // source lane's GPU and position
             // bounds on this column's minimum cost from the high words (costs are >= 0, so their bit patterns
             // order like the values): [hi:0] <= min <= [hi+1:0] -- one REDUX instead of a 5-step shuffle tree
             const unsigned hmin = __reduce_min_sync(0xffffffffu, (unsigned)__double2hiint(c));
@@ -618,13 +620,14 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                 const bool uniform = uS == uS;
                 const double* cwS = cw_all + (boff + S) * 32;
                 // sources of S: lanes whose cost is finite (lanes >= the column length publish +inf)
-                const int pgl = pg_all[(boff + S) * 32 + lane];          // lane k: source k's GPU and position
-                const int gsl = pgl & 0xffff;
+                // lane k: source k's GPU and position (tile S's pair list of column b; its slots are held through b)
+                const int prS = rg_ld_pair(pairs_g + ((int64_t)S * (nblk + 1) + b) * 32 + lane);
+                const int gsl = prS != RG_PAIR_NONE ? slot_gpu[S * 32 + (prS & 31)] : 0;
                 // source k can only reach a destination of this tile if c_k + (its own bound to the tile) <= vmax
                 const double lbk = (A.use_lbg && cwS[lane] < INF) ? (double)lbg_s[gsl * NTL + w] : lbS;
                 unsigned keep = __ballot_sync(0xffffffffu, cwS[lane] < INF && !(__dadd_rn(cwS[lane], lbk) > vmax));
                 if (A.cross) { n_cross += keep != 0; n_src += __popc(keep); }
-                const int psl = pgl >> 16;
+                const int psl = (prS >> 8) & 0xff;
                 const int gd = sg_w[lane];
                 // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
                 // from the shared-memory table, four sources per round
@@ -844,7 +847,6 @@ extern "C" int ss_replay_regions(const ss_dag_set* dags, const uint8_t* meta, in
     A.off_pow = o;     o += rg_align(A.pow_len * 8, 16);
     A.off_rel = o;     o += rg_align((L + 1) * 4, 16);
     A.off_seg = o;     o += rg_align(n_tiles * pos_cap, 16) + rg_align(n_tiles * 4, 16);
-    A.off_pg = o;      o += 2 * n_tiles * 32 * 4;
     A.off_jq = o;      o += jitter_seed ? 1024 * 4 : 0;
     A.off_lbg = o;     o += rg_align(D.max_gpus * n_tiles * 4, 16);   // last: dropped when it costs occupancy
     A.use_lbg = 1;
