@@ -502,7 +502,8 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
     const uint16_t* pw_g = pairs_g + (int64_t)w * (nblk + 1) * 32 + lane;   // column c: pw_g[c * 32]
     double* const cw0 = cw_all + w * 32;
     int* const rw0 = rw_all + w * 32;
-    unsigned n_test = 0, n_cross = 0, n_src = 0;
+    unsigned n_cross = 0, n_src = 0;
+    const bool stats = A.cross != nullptr;
     int done = 0;
     rg_bar_cons(NC);
 
@@ -575,8 +576,6 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             const double ubd = __dadd_rn(cmin_hi, ub_w);                                // >= every v_j here
             const bool keep_S = cross_lane && !(__dadd_rn(cmin_all[boff + (lane < NTL ? lane : 0)], lb_lane) > ubd);
             unsigned tiles = __ballot_sync(0xffffffffu, keep_S);
-            // destination slots of boundary b (the sources of column b + 1): only their minima bound the test below
-            const unsigned dmask = __reduce_or_sync(0xffffffffu, pr_n1 != RG_PAIR_NONE ? 1u << (pr_n1 & 31) : 0u);
 
             // ---- relax boundary b inside the tile: sources in position order, strict <, two chains (even / odd
             //      sources) merged lexicographically == numpy's first-index argmin ---------------------------------
@@ -597,9 +596,10 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
             int pv = ix < 32 ? pix : RG_POS_NONE;
             // ---- cross-tile blocks the bound test keeps (rare): only their sources whose candidates can still
             //      reach ubd, entries recomputed from the pool matrix eight at a time (one L2 round trip per batch)
-            if (A.cross) n_test += NTL - 1;
             double vmax = ubd;
             if (tiles) {
+                // destination slots of boundary b (the sources of column b + 1): only their minima bound the test
+                const unsigned dmask = __reduce_or_sync(0xffffffffu, pr_n1 != RG_PAIR_NONE ? 1u << (pr_n1 & 31) : 0u);
                 // the intra-region minima are known now: a source can only matter where fl(c + lb) <= some v_j,
                 // so bound by the largest destination minimum ([hi+1:0] >= v for v >= 0) instead of ubd
                 const unsigned hv = __reduce_max_sync(0xffffffffu, ((dmask >> lane) & 1u) ? (unsigned)__double2hiint(v) : 0u);
@@ -626,7 +626,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                 // source k can only reach a destination of this tile if c_k + (its own bound to the tile) <= vmax
                 const double lbk = (A.use_lbg && cwS[lane] < INF) ? (double)lbg_s[gsl * NTL + w] : lbS;
                 unsigned keep = __ballot_sync(0xffffffffu, cwS[lane] < INF && !(__dadd_rn(cwS[lane], lbk) > vmax));
-                if (A.cross) { n_cross += keep != 0; n_src += __popc(keep); }
+                if (stats) { n_cross += keep != 0; n_src += __popc(keep); }
                 const int psl = (prS >> 8) & 0xff;
                 const int gd = sg_w[lane];
                 // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
@@ -745,8 +745,8 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
         ++done;
     }
     rg_cp_async_wait_all();
-    if (A.cross && lane == 0) {
-        atomicAdd(&A.cross[0], (unsigned long long)n_test);
+    if (stats && lane == 0) {
+        atomicAdd(&A.cross[0], (unsigned long long)(NTL - 1) * (unsigned long long)nblk * (unsigned long long)done);
         atomicAdd(&A.cross[1], (unsigned long long)n_cross);
         atomicAdd(&A.cross[2], (unsigned long long)n_src);
     }
