@@ -604,8 +604,8 @@ def run_admission(args, rank, world, stream, barrier, reduce_max):
     with torch.cuda.stream(stream):
         rp = ScenarioReplayer(ss, window=W, mode="warp", stream=stream)
         rp.build()
-        rp.admit(8, tok_lo=lo, tok_hi=hi)
-        torch.cuda.synchronize()
+        rp.admit(steps, tok_lo=lo, tok_hi=hi)              # warm-up at full size: the output blocks come from
+        torch.cuda.synchronize()                           # the caching allocator, not cudaMalloc, when timed
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
