@@ -124,3 +124,22 @@ def test_regions_nonuniform_cross_links_vs_oracle(cuda_ready):
     T = t.n_tiles
     assert np.isnan(t.bounds[T * T + T:]).reshape(T, T)[~np.eye(T, dtype=bool)].all()
     _check(ss, 70, 16)
+
+
+@pytest.mark.parametrize("region_count", [1, 2, 3, 5, 6, 7])
+def test_regions_every_tile_count_vs_oracle(cuda_ready, region_count):
+    """Every replay_regions_kernel<NTL> instantiation the C4 (4) / C5 (8) tests do not reach: 16 GPUs per region,
+    L=32, churn + jitter, W=16 (releases from request 16 on); with three regions also a small-gap pool (cross
+    1.1 ms) so kept cross blocks run on an odd tile count."""
+    from paper_2509_26182_b200 import scenarios as scen
+    from paper_2509_26182_b200.batched import region_tiles
+    cl, model, plan = _pool(16 * region_count, 32, region_count=region_count, seed=2)
+    ss = scen.build_scenarios(cl, model, plan, 6, seed0=5, churn=0.05, jitter=True)
+    t = region_tiles(ss)
+    assert t.n_tiles == region_count and t.fits()
+    _check(ss, 96, 16)
+    if region_count == 3:
+        cl, model, plan = _pool(48, 32, region_count=3, cross=0.0011, seed=2)
+        ss = scen.build_scenarios(cl, model, plan, 6, seed0=7, churn=0.05, jitter=True)
+        assert region_tiles(ss).gap < 0
+        _check(ss, 96, 16)
