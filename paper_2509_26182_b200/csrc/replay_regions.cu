@@ -38,7 +38,10 @@ namespace {
 #define RG_MINB_WIDE 3                   // CTAs per SM the register budget is sized for (5..8 tiles)
 #endif
 #ifndef RG_KB
-#define RG_KB 4                          // kept cross-tile sources per round
+#define RG_KB 4                          // kept cross-tile sources per round (<= 4 tiles)
+#endif
+#ifndef RG_KB_WIDE
+#define RG_KB_WIDE 2                     // ... with 5-8 tiles (C5: +0.5-2% over 4; C4: 4 beats 2 and 8)
 #endif
 
 constexpr int RG_UNROLL_N = RG_UNROLL;
@@ -632,7 +635,7 @@ replay_regions_kernel(ss_dag_set D, RgArgs A, RgReplayArgs R) {
                 // entries: the tile pair's uniform pool value (or the pool matrix) x the pair's jitter quantile
                 // from the shared-memory table, four sources per round
                 while (keep) {
-                    constexpr int KB = RG_KB;
+                    constexpr int KB = NTL <= 4 ? RG_KB : RG_KB_WIDE;
                     int kk[KB], gs[KB];
                     double e[KB];
 #pragma unroll
