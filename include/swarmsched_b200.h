@@ -297,9 +297,11 @@ int ss_stage_counts_exact(const ss_pool_set* pools, const int64_t* koff, int32_t
                           int32_t* gsize, int32_t* pool_status, int32_t* pool_aux, const int32_t* exact_list,
                           int32_t n_exact, void* workspace, int64_t ws_bytes_per, int32_t frontier_cap,
                           int32_t children_cap, int32_t* sweep_stats /* [n_exact*4] or NULL */, void* stream);
+/* max_layers: the largest L among the batch's pools (0 = unknown); it only picks the serial kernel's register
+ * budget (<= 64: sized for 12 blocks of 64 per SM), never the result. */
 int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
                           int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k,
-                          int32_t n_cand, int32_t* stall, void* stream);
+                          int32_t n_cand, int32_t* stall, int32_t max_layers, void* stream);
 
 /* estimate_objective_params (allocator.py:516-538): per item, flops and a
  * dense rtt_s matrix in CLUSTER order; CPython 3.12 sum() semantics

@@ -124,7 +124,8 @@ _SIGS_P1 = {
     "ss_stage_counts_validate": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V]),
     "ss_stage_counts_exact": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, C.c_int64,
                                         C.c_int32, C.c_int32, _V, _V]),
-    "ss_stage_counts_cover": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, _V]),
+    "ss_stage_counts_cover": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, _V, C.c_int32,
+                                        _V]),
     "ss_objective": (C.c_int, [C.c_int32, _V, _V, _V, _V, C.c_double, _V, C.c_double, _V, _V, _V]),
     "ss_phase1_score": (C.c_int, [C.POINTER(PoolSet), _V, _V, _V, _V, _V, _V, _V, C.c_int32, C.c_int32, _V, _V,
                                   _V, _V, _V, _V, C.c_int32, _V]),

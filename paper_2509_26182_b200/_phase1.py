@@ -155,6 +155,7 @@ class PoolBatch:
         all_pool, all_k = all_pool[o], all_k[o]
         self.exact = exact
         self.n_cover = int(cand_pool.size)
+        self.max_layers = int(A.layers.max()) if A.layers.size else 0
         self.n_cand = int(all_pool.size)
         ints = np.concatenate([pool_ptr, caps, A.layers, km, exact, cand_pool, cand_k, all_pool,
                                all_k])
@@ -230,7 +231,7 @@ class PoolBatch:
             self._run_exact(lib, ps, st)
         N.check(lib.ss_stage_counts_cover(ps, N.ptr(self.koff), N.ptr(self.stages), N.ptr(self.members),
                                           N.ptr(self.gsize), N.ptr(self.status), N.ptr(self.cand_pool),
-                                          N.ptr(self.cand_k), self.n_cover, N.ptr(self.stall), st),
+                                          N.ptr(self.cand_k), self.n_cover, N.ptr(self.stall), self.max_layers, st),
                 "ss_stage_counts_cover")
 
     def _run_exact(self, lib, ps, st) -> None:

@@ -926,10 +926,15 @@ __device__ bool cover_try(const CoverCand& cc, int k, int m, Lists& G, Frame* fr
     return false;
 }
 
+#ifndef P1_NARROW_MAX_L
+#define P1_NARROW_MAX_L 64               // batches with every L <= this run cover_kernel_narrow
+#endif
+
 // one thread per (pool, k) on the constructive path; stage 0 = absent / stalled
-__global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members, int32_t* gsize,
-                             const int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k, int n_cand,
-                             int32_t* stall) {
+__device__ __forceinline__ void cover_candidate(const ss_pool_set& P, const int64_t* koff, int32_t* stages,
+                                                int32_t* members, int32_t* gsize, const int32_t* pool_status,
+                                                const int32_t* cand_pool, const int32_t* cand_k, int n_cand,
+                                                int32_t* stall) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_cand) return;
     const int p = cand_pool[c], k = cand_k[c];
@@ -947,6 +952,22 @@ __global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages
     for (int m = cc.m0; m <= cc.n; ++m)
         if (cover_try(cc, k, m, G, fr, reach, mout, gout, stages + cc.ko)) return;
     stall[cc.ko] = 1;                                            // constructive grouping stalled
+}
+
+__global__ void cover_kernel(ss_pool_set P, const int64_t* koff, int32_t* stages, int32_t* members, int32_t* gsize,
+                             const int32_t* pool_status, const int32_t* cand_pool, const int32_t* cand_k, int n_cand,
+                             int32_t* stall) {
+    cover_candidate(P, koff, stages, members, gsize, pool_status, cand_pool, cand_k, n_cand, stall);
+}
+
+// the same for batches whose pools all have L <= 64 (two live reach words): a register budget sized for 12 blocks of
+// 64 per SM (79 registers) -- their long m loops are latency-bound and more resident warps hide it (+4% at L = 64
+// in a same-box A/B, identical plans; the same bound costs ~3% at L = 80, which keeps cover_kernel's 84)
+__global__ void __launch_bounds__(64, 12) cover_kernel_narrow(ss_pool_set P, const int64_t* koff, int32_t* stages,
+                                                              int32_t* members, int32_t* gsize,
+                                                              const int32_t* pool_status, const int32_t* cand_pool,
+                                                              const int32_t* cand_k, int n_cand, int32_t* stall) {
+    cover_candidate(P, koff, stages, members, gsize, pool_status, cand_pool, cand_k, n_cand, stall);
 }
 
 // small batches, one round: thread (c, j) attempts m = m0 + m_off + j of candidate c unless an earlier round (a
@@ -1302,7 +1323,8 @@ extern "C" int ss_stage_counts_exact(const ss_pool_set* pools, const int64_t* ko
 
 extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* koff, int32_t* stages, int32_t* members,
                                      int32_t* gsize, int32_t* pool_status, const int32_t* cand_pool,
-                                     const int32_t* cand_k, int32_t n_cand, int32_t* stall, void* stream) {
+                                     const int32_t* cand_k, int32_t n_cand, int32_t* stall, int32_t max_layers,
+                                     void* stream) {
     cudaStream_t s = ss_stream(stream);
     // The cover kernels keep their peel frames / reach bitsets on the thread stack (~28 KB).  Reserving that
     // stack size once stops the driver from resizing the device's local-memory pool between launches of
@@ -1311,9 +1333,12 @@ extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* ko
     if (!stack_reserved) {
         size_t cur = 0;
         cudaFuncAttributes fa{};
-        if (cudaFuncGetAttributes(&fa, cover_kernel) == cudaSuccess && cudaDeviceGetLimit(&cur, cudaLimitStackSize) ==
-                cudaSuccess && cur < fa.localSizeBytes)
-            cudaDeviceSetLimit(cudaLimitStackSize, fa.localSizeBytes);
+        size_t need = 0;
+        if (cudaFuncGetAttributes(&fa, cover_kernel) == cudaSuccess) need = fa.localSizeBytes;
+        if (cudaFuncGetAttributes(&fa, cover_kernel_narrow) == cudaSuccess && fa.localSizeBytes > need)
+            need = fa.localSizeBytes;
+        if (need && cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && cur < need)
+            cudaDeviceSetLimit(cudaLimitStackSize, need);
         stack_reserved = true;
     }
     // A batch too small to fill the GPU (one allocate() call: ~4 regions x k_max candidates) tries every group
@@ -1337,8 +1362,9 @@ extern "C" int ss_stage_counts_cover(const ss_pool_set* pools, const int64_t* ko
         SS_CHECK_LAUNCH();
         cudaFreeAsync(best_m, s);
     } else if (n_cand > 0) {
-        cover_kernel<<<grid_for(n_cand, 64), 64, 0, s>>>(*pools, koff, stages, members, gsize, pool_status, cand_pool,
-                                                          cand_k, n_cand, stall);
+        auto kern = max_layers > 0 && max_layers <= P1_NARROW_MAX_L ? cover_kernel_narrow : cover_kernel;
+        kern<<<grid_for(n_cand, 64), 64, 0, s>>>(*pools, koff, stages, members, gsize, pool_status, cand_pool, cand_k,
+                                                  n_cand, stall);
         SS_CHECK_LAUNCH();
     }
     cover_fixup_kernel<<<grid_for(pools->n_pools, 128), 128, 0, s>>>(*pools, koff, stages, stall, pool_status);
